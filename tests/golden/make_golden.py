@@ -1,0 +1,339 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the reference package ``bitquorum`` from
+``$BQ_REFERENCE_SRC`` (default /root/reference/pkg/src), builds seeded
+inputs, runs the reference algorithms on them, checks that every reference
+algorithm agrees with the reference brute-force oracle, and writes inputs plus
+expected outputs to ``tests/golden/*.npz`` / ``kat.json``.  The fixtures are
+committed; the GPU box never needs the reference.
+
+Fixture layout (one .npz per family, one case per key prefix ``cNNN_``):
+  cNNN_in      concatenated input words (uint64)
+  cNNN_off     per-input offsets into cNNN_in (N + 1)
+  cNNN_bits    per-input bit_length
+  cNNN_out     expected output words (reference result ``.words``; trimmed)
+  cNNN_meta    JSON: n, t / accept, r, notes
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import random
+import sys
+
+import numpy as np
+
+REF = os.environ.get("BQ_REFERENCE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+from bitquorum import bitmaps as bm  # noqa: E402
+from bitquorum import counters, oracle, runmerge  # noqa: E402
+from bitquorum.circuits import (  # noqa: E402
+    CircuitLibrary,
+    build_sideways_sum,
+    build_tree_adder,
+    compile_circuit,
+    csv_threshold,
+    execute,
+    execute_horizontal,
+    looped_threshold,
+    optimize,
+)
+from bitquorum.errors import FormatError  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+MASK = (1 << 64) - 1
+
+
+# ---------------------------------------------------------------------------
+# independent pure-Python statement of the benchmark generator (K5), so the
+# C/CUDA generator in paper_1402_4073_b200/csrc/bq_gen.h is pinned too.
+
+GAMMA = 0x9E3779B97F4A7C15
+
+
+def mix64(z):
+    z &= MASK
+    z ^= z >> 30
+    z = (z * 0xBF58476D1CE4E5B9) & MASK
+    z ^= z >> 27
+    z = (z * 0x94D049BB133111EB) & MASK
+    z ^= z >> 31
+    return z
+
+
+def bitmap_key(seed, i):
+    return mix64((mix64(seed ^ 0x5851F42D4C957F2D) + (i + 1) * GAMMA) & MASK)
+
+
+def rand_word(key, ctr):
+    return mix64((key + (ctr + 1) * GAMMA) & MASK)
+
+
+def bernoulli_word(key, w, q):
+    if q <= 0:
+        return 0
+    if q >= 65536:
+        return MASK
+    x = 0
+    k0 = (q & -q).bit_length() - 1
+    for k in range(k0, 16):
+        r = rand_word(key, w * 16 + k)
+        x = (x | r) if (q >> k) & 1 else (x & r)
+    return x
+
+
+def density_q(seed, i, lo=655, hi=32768):
+    u = mix64(bitmap_key(seed, i) ^ 0xD1B54A32D192ED03) >> 40
+    return lo + ((u * (hi - lo)) >> 24)
+
+
+# ---------------------------------------------------------------------------
+
+def rand_bitmap(rng: random.Random, r: int, kind: str) -> list[int]:
+    nw = (r + 63) // 64
+    if kind == "zero":
+        words = [0] * nw
+    elif kind == "one":
+        words = [MASK] * nw
+    elif kind == "sparse":
+        words = [(rng.getrandbits(64) & rng.getrandbits(64) & rng.getrandbits(64)) for _ in range(nw)]
+    elif kind == "dense":
+        words = [(rng.getrandbits(64) | rng.getrandbits(64)) for _ in range(nw)]
+    elif kind == "runs":
+        words = []
+        bit = rng.random() < 0.3
+        cur = 0
+        pos = 0
+        while pos < nw * 64:
+            run = max(1, int(rng.expovariate(1 / (300 if not bit else 90))))
+            if bit:
+                for p in range(pos, min(pos + run, nw * 64)):
+                    cur |= 1 << p
+            pos += run
+            bit = not bit
+        words = [(cur >> (64 * k)) & MASK for k in range(nw)]
+    else:
+        words = [rng.getrandbits(64) for _ in range(nw)]
+    if r % 64 and nw:
+        words[-1] &= (1 << (r % 64)) - 1
+    return words
+
+
+def make_inputs(rng, n, r, mixed_lengths=True, kinds=None):
+    out = []
+    for i in range(n):
+        ri = r
+        if mixed_lengths and rng.random() < 0.3:
+            ri = rng.randint(0, r)
+        kind = rng.choice(kinds or ["sparse", "dense", "uniform", "runs", "sparse", "zero", "one"])
+        words = rand_bitmap(rng, ri, kind)
+        out.append(bm.UncompressedBitmap(words, ri))
+    # make sure r is attained by one input (result bit_length is the max)
+    if all(b.bit_length < r for b in out):
+        out[0] = bm.UncompressedBitmap(rand_bitmap(rng, r, "sparse"), r)
+    return out
+
+
+class Writer:
+    def __init__(self, name):
+        self.name = name
+        self.arrays = {}
+        self.k = 0
+
+    def add(self, inputs_words, bit_lengths, out_words, meta):
+        p = f"c{self.k:03d}_"
+        flat = [w for ws in inputs_words for w in ws]
+        off = np.cumsum([0] + [len(ws) for ws in inputs_words]).astype(np.uint64)
+        self.arrays[p + "in"] = np.array(flat, dtype=np.uint64)
+        self.arrays[p + "off"] = off
+        self.arrays[p + "bits"] = np.array(bit_lengths, dtype=np.uint64)
+        self.arrays[p + "out"] = np.array(out_words, dtype=np.uint64)
+        self.arrays[p + "meta"] = np.array(json.dumps(meta))
+        self.k += 1
+
+    def save(self):
+        path = os.path.join(HERE, self.name + ".npz")
+        np.savez_compressed(path, **self.arrays)
+        print(f"{path}: {self.k} cases, {os.path.getsize(path)} bytes")
+
+
+def positions(b):
+    return b.positions()
+
+
+def threshold_cases(rng):
+    wr = Writer("threshold")
+    shapes = [(1, 70), (2, 64), (3, 1), (3, 130), (5, 4000), (7, 777), (8, 2 ** 12), (8, 4096 + 63),
+              (15, 1500), (16, 2000), (17, 2049), (31, 999), (32, 5000), (33, 4097),
+              (47, 3000), (64, 4096), (64, 4200), (100, 1234), (130, 640), (256, 700), (300, 200)]
+    for n, r in shapes:
+        inputs = make_inputs(rng, n, r)
+        r_eff = max(b.bit_length for b in inputs)
+        ts = sorted({1, n, max(1, n // 2), max(1, (n + 1) // 2 + 1) if n > 1 else 1,
+                     rng.randint(1, n), min(n, 2), min(n, 3)})
+        sets = [positions(b) for b in inputs]
+        for t in ts:
+            exp = oracle.brute_threshold(sets, t)
+            got = counters.scan_count(inputs, t)
+            assert got.positions() == exp, (n, t)
+            assert looped_threshold(inputs, t).positions() == exp
+            if 2 <= t < n:
+                assert csv_threshold(inputs, t).positions() == exp
+            if n <= 64:
+                prog = compile_circuit(optimize(build_sideways_sum(n, t)))
+                assert execute(prog, inputs).positions() == exp
+                assert execute_horizontal(prog, inputs).positions() == exp
+            if n <= 40:
+                prog = compile_circuit(optimize(build_tree_adder(n, t)))
+                assert execute(prog, inputs).positions() == exp
+                assert CircuitLibrary(n_max=64).threshold(inputs, t).positions() == exp
+            wr.add([b.words for b in inputs], [b.bit_length for b in inputs], got.words,
+                   {"n": n, "t": t, "r": r_eff, "kind": "threshold",
+                    "card": got.cardinality()})
+    wr.save()
+
+
+def symmetric_cases(rng):
+    wr = Writer("symmetric")
+    shapes = [(1, 100), (3, 300), (8, 1024), (16, 2000), (33, 1500), (64, 4096), (100, 700), (256, 640)]
+    for n, r in shapes:
+        inputs = make_inputs(rng, n, r)
+        r_eff = max(b.bit_length for b in inputs)
+        sets = [positions(b) for b in inputs]
+        specs = [("threshold", oracle.SymmetricSpec.threshold(n, max(1, n // 3))),
+                 ("delta0", oracle.SymmetricSpec.delta(n, 0)),
+                 ("delta", oracle.SymmetricSpec.delta(n, min(n, 2))),
+                 ("interval", oracle.SymmetricSpec.interval(n, min(n, 2), min(n, 10))),
+                 ("parity", oracle.SymmetricSpec.parity(n)),
+                 ("random", oracle.SymmetricSpec(tuple(rng.random() < 0.5 for _ in range(n + 1)))),
+                 ("random0", oracle.SymmetricSpec((True,) + tuple(rng.random() < 0.3 for _ in range(n)))),
+                 ("all", oracle.SymmetricSpec(tuple(True for _ in range(n + 1))))]
+        for name, spec in specs:
+            exp = oracle.brute_symmetric(sets, spec, r_eff)
+            got = counters.scan_count_symmetric(inputs, spec)
+            assert got.positions() == exp, (n, name)
+            wr.add([b.words for b in inputs], [b.bit_length for b in inputs], got.words,
+                   {"n": n, "accept": [int(a) for a in spec.accept], "r": r_eff,
+                    "kind": "symmetric", "spec": name, "card": got.cardinality()})
+    wr.save()
+
+
+def rle_cases(rng):
+    """cdom over canonical RLE streams; expected output is the reference RleBitmap."""
+    wr = Writer("rle")
+    shapes = [(2, 500), (3, 64 * 40), (5, 64 * 100 + 17), (8, 64 * 300), (16, 64 * 200 + 5),
+              (33, 64 * 150), (64, 64 * 256), (130, 64 * 64 + 9)]
+    for n, r in shapes:
+        inputs = make_inputs(rng, n, r, kinds=["runs", "runs", "sparse", "zero", "one", "runs"])
+        comp = [bm.compress(b) for b in inputs]
+        r_eff = max(b.bit_length for b in inputs)
+        sets = [positions(b) for b in inputs]
+        for t in sorted({1, 2, max(1, n // 4), max(1, n // 2), n}):
+            exp = oracle.brute_threshold(sets, t)
+            got = runmerge.cdom_threshold(comp, t)
+            assert got.positions() == exp
+            sc = counters.scan_count(comp, t)  # RLE in -> RLE out (counters.py:33-37)
+            assert sc.words == got.words
+            wr.add([c.words for c in comp], [c.bit_length for c in comp], got.words,
+                   {"n": n, "t": t, "r": r_eff, "kind": "cdom_threshold",
+                    "uncompressed": [int(w) for w in bm.decompress(got).words]})
+        spec = oracle.SymmetricSpec.interval(n, 1, max(1, n // 3))
+        exp = oracle.brute_symmetric(sets, spec, r_eff)
+        got = runmerge.cdom_symmetric(comp, spec)
+        assert got.positions() == exp
+        wr.add([c.words for c in comp], [c.bit_length for c in comp], got.words,
+               {"n": n, "accept": [int(a) for a in spec.accept], "r": r_eff, "kind": "cdom_symmetric",
+                "uncompressed": [int(w) for w in bm.decompress(got).words]})
+        spec = oracle.SymmetricSpec((True,) + tuple(rng.random() < 0.5 for _ in range(n)))
+        exp = oracle.brute_symmetric(sets, spec, r_eff)
+        got = runmerge.cdom_symmetric(comp, spec)
+        assert got.positions() == exp
+        wr.add([c.words for c in comp], [c.bit_length for c in comp], got.words,
+               {"n": n, "accept": [int(a) for a in spec.accept], "r": r_eff, "kind": "cdom_symmetric",
+                "uncompressed": [int(w) for w in bm.decompress(got).words]})
+    wr.save()
+
+
+def codec_cases(rng):
+    """compress/decompress round trips and hand-built (non-canonical / malformed) streams."""
+    wr = Writer("codec")
+    for r, kind in [(0, "zero"), (1, "one"), (64, "one"), (65, "one"), (128, "zero"), (640, "runs"),
+                    (64 * 70 + 3, "runs"), (5000, "sparse"), (5000, "dense"), (64 * 33, "one")]:
+        words = rand_bitmap(rng, r, kind)
+        u = bm.UncompressedBitmap(list(words), r)
+        c = bm.compress(u)
+        assert bm.decompress(c) == u
+        wr.add([u.words], [r], c.words, {"kind": "compress", "r": r})
+    # hand-built streams that decode fine (decoder must accept them):
+    mk = lambda bit, run, dirty: bit | (run << 1) | (dirty << 33)  # noqa: E731
+    hand = [
+        ("implicit_tail", [mk(1, 2, 1), 0x5], 64 * 10),
+        ("fill_run_zero", [mk(0, 0, 2), 0x3, 0x9, mk(1, 0, 1), 0x7], 64 * 4),
+        ("literal_all0_all1", [mk(0, 1, 3), 0, MASK, 0x10, mk(0, 2, 0)], 64 * 6),
+        ("adjacent_markers", [mk(0, 1, 0), mk(0, 2, 0), mk(1, 1, 0), mk(1, 1, 1), 0xF0], 64 * 7),
+        ("empty_stream", [], 64 * 3 + 1),
+        ("split_fills", [mk(1, 1, 0), mk(1, 1, 0), mk(0, 1, 1), 0x1], 64 * 5),
+        ("partial_last", [mk(1, 2, 1), 0x7], 64 * 2 + 3),
+    ]
+    for name, stream, r in hand:
+        d = bm.decompress(bm.RleBitmap(list(stream), r))
+        wr.add([stream], [r], d.words, {"kind": "decode", "r": r, "name": name, "status": "ok"})
+    bad = [
+        ("truncated_literals", [mk(0, 1, 3), 0x1, 0x2], 64 * 10),
+        ("overlong_fill", [mk(0, 11, 0)], 64 * 10),
+        ("overlong_dirty", [mk(0, 9, 2), 0x1, 0x2], 64 * 10),
+        ("bits_beyond_r", [mk(0, 0, 1), 0xFF], 4),
+        ("one_fill_beyond_r", [mk(1, 1, 0)], 10),
+    ]
+    for name, stream, r in bad:
+        try:
+            bm.decompress(bm.RleBitmap(list(stream), r))
+            raise AssertionError(f"{name} should not decode")
+        except FormatError:
+            pass
+        wr.add([stream], [r], [], {"kind": "decode", "r": r, "name": name, "status": "format_error"})
+    wr.save()
+
+
+def generator_cases():
+    out = {"seed": 1402, "cases": []}
+    for (i, w, q) in [(0, 0, 6554), (0, 1, 6554), (3, 12345, 6554), (7, 0, 32768), (1, 99, 3277),
+                      (2, 5, 1), (2, 6, 65535), (9, 2 ** 22 - 1, 1311), (511, 2 ** 26 - 1, 32768),
+                      (4, 4, 0), (4, 4, 65536)]:
+        key = bitmap_key(1402, i)
+        out["cases"].append({"bitmap": i, "word": w, "q": q, "value": str(bernoulli_word(key, w, q))})
+    out["density_q"] = [density_q(1402, i) for i in range(64)]
+    out["keys"] = [str(bitmap_key(1402, i)) for i in range(4)]
+    return out
+
+
+def kat():
+    """Known-answer tests quoted in SPEC.md / PAPER.md, evaluated by the reference."""
+    res = {}
+    res["brute_threshold_spec160"] = oracle.brute_threshold([[1, 2, 7], [2, 7, 9], [7]], 2)
+    ins = [bm.UncompressedBitmap.from_positions(p, 16) for p in ([1], [1], [2])]
+    res["csv_spec542"] = csv_threshold(ins, 2).positions()
+    res["compress_empty128"] = bm.compress(bm.UncompressedBitmap.empty(128)).words
+    res["from_positions_1279"] = bm.UncompressedBitmap.from_positions([1, 2, 7, 9], 16).words
+    res["canonical_example"] = [str(w) for w in bm.compress(
+        bm.UncompressedBitmap([0, MASK, 3, 0, 0, 7], 64 * 6)).words]
+    res["generator"] = generator_cases()
+    path = os.path.join(HERE, "kat.json")
+    with open(path, "w") as fp:
+        json.dump(res, fp, indent=1)
+    print(path)
+
+
+if __name__ == "__main__":
+    rng = random.Random(14024073)
+    threshold_cases(rng)
+    symmetric_cases(rng)
+    rle_cases(rng)
+    codec_cases(rng)
+    kat()

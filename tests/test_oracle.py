@@ -1,0 +1,87 @@
+"""Pin the CPU oracle against fixtures produced by running the reference itself
+(tests/golden/make_golden.py).  CPU only."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, load_kat, padded
+from oracle import oracle as O
+
+THRESH = load_golden("threshold")
+SYM = load_golden("symmetric")
+RLE = load_golden("rle")
+CODEC = load_golden("codec")
+
+
+@pytest.mark.parametrize("case", THRESH, ids=lambda c: c.id)
+def test_scan_count_matches_reference(case):
+    t = case.meta["t"]
+    exp = padded(case.out, case.r)
+    assert np.array_equal(O.scan_count(case.inputs, case.r, t), exp)
+    assert np.array_equal(O.threshold_port(case.inputs, case.r, t, threads=2), exp)
+    assert int(sum(int(w).bit_count() for w in case.out)) == case.meta["card"]
+
+
+@pytest.mark.parametrize("case", SYM, ids=lambda c: c.id)
+def test_symmetric_matches_reference(case):
+    acc = case.meta["accept"]
+    exp = padded(case.out, case.r)
+    assert np.array_equal(O.scan_count_symmetric(case.inputs, case.r, acc), exp)
+    assert np.array_equal(O.symmetric_port(case.inputs, case.r, acc, threads=2), exp)
+
+
+@pytest.mark.parametrize("case", RLE, ids=lambda c: c.id)
+def test_cdom_matches_reference(case):
+    exp_u = padded(np.array(case.meta["uncompressed"], dtype=np.uint64), case.r)
+    if case.meta["kind"] == "cdom_threshold":
+        got = O.cdom_threshold(case.inputs, case.r, case.meta["t"])
+    else:
+        got = O.cdom_symmetric(case.inputs, case.r, case.meta["accept"])
+    assert np.array_equal(got, exp_u)
+    # the reference returns the canonical encoding of those words
+    assert np.array_equal(O.rle_compress(O.trim(got), case.r), case.out)
+
+
+@pytest.mark.parametrize("case", CODEC, ids=lambda c: c.id)
+def test_codec_matches_reference(case):
+    kind = case.meta["kind"]
+    if kind == "compress":
+        assert np.array_equal(O.rle_compress(case.inputs[0], case.r), case.out)
+        assert np.array_equal(O.rle_decompress(case.out, case.r), padded(case.inputs[0], case.r))
+    elif case.meta["status"] == "ok":
+        assert np.array_equal(O.rle_decompress(case.inputs[0], case.r), padded(case.out, case.r))
+    else:
+        with pytest.raises(O.OracleError) as ei:
+            O.rle_decompress(case.inputs[0], case.r)
+        assert ei.value.code == O.EFORMAT
+
+
+def test_known_answers():
+    kat = load_kat()
+    assert O.brute_threshold([[1, 2, 7], [2, 7, 9], [7]], 2) == kat["brute_threshold_spec160"] == [2, 7]
+    ins = [O.words_from_positions(p, 16) for p in ([1], [1], [2])]
+    assert O.positions_of(O.threshold_port(ins, 16, 2)) == kat["csv_spec542"] == [1]
+    assert O.rle_compress(np.zeros(0, np.uint64), 128).tolist() == kat["compress_empty128"] == [4]
+    assert O.words_from_positions([1, 2, 7, 9], 16).tolist() == kat["from_positions_1279"]
+    words = np.array([0, 2**64 - 1, 3, 0, 0, 7], dtype=np.uint64)
+    assert [str(w) for w in O.rle_compress(O.trim(words), 64 * 6).tolist()] == kat["canonical_example"]
+
+
+def test_complement_identity():
+    """theta(T, B) = NOT theta(N - T + 1, NOT B)."""
+    rng = np.random.default_rng(7)
+    n, r = 13, 64 * 50 - 3
+    ins = [rng.integers(0, 2**63, size=50, dtype=np.uint64) * np.uint64(2) for _ in range(n)]
+    mask = np.uint64((1 << (r % 64)) - 1)
+    for a in ins:
+        a[-1] &= mask
+    neg = [~a for a in ins]
+    for a in neg:
+        a[-1] &= mask
+    for t in range(1, n + 1):
+        lhs = O.scan_count(ins, r, t)
+        rhs = ~O.scan_count(neg, r, n - t + 1)
+        rhs[-1] &= mask
+        assert np.array_equal(lhs, rhs)
