@@ -1,0 +1,399 @@
+"""Benchmark: input GB/s of T-of-N threshold queries on B200 (BASELINE.json metric).
+
+Default workload (BASELINE.json configs[1], "C2"): N=64 uncompressed bitmaps
+of r=2^28 bits per GPU (2 GiB of input per GPU), per-bitmap densities drawn
+from U[0.01, 0.5], T swept over {1, 2, 16, 32, 64}.  One step = the five
+queries over the resident inputs (5 x 2 GiB of input bytes per GPU) plus the
+8-byte-per-query popcount all-reduce across ranks.  Inputs (2 GiB) are far
+larger than L2 (126 MB), so no flush is needed between steps.
+
+Multi-GPU: one process per GPU (torchrun); rank g owns words
+[g*2^22, (g+1)*2^22) of global bitmaps of world*2^28 bits (weak scaling, no
+data-path collective; only the popcount all-reduce).
+
+Lines printed by rank 0 (one JSON object):
+  value       device-resident throughput (input bytes / max-over-ranks time)
+  e2e         the same metric through the public host-buffer API
+              (paper_1402_4073_b200.sweep_host, pinned host inputs, H2D + D2H
+              inside the timed region)
+  roofline    the counting kernel's achieved HBM GB/s (algorithmic bytes per
+              launch / mean CUDA-event launch time) vs MEASURED_PEAKS.json
+  cpu_baseline the CPU oracle port timed on this host's cores (rank 0, N=1)
+
+``--impl reference`` times the reference algorithm's CPU port (oracle/, the
+reference is Python and has no native build) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "input GB/s (and fraction of HBM peak) for T-of-N threshold queries at 1/2/4/8 B200"
+SEED = 1402
+C2_N = 64
+C2_WORDS = 1 << 22          # words per bitmap per GPU (r = 2^28 bits)
+C2_TS = (1, 2, 16, 32, 64)
+DENS_LO, DENS_HI = 655, 32768   # round(0.01 * 2^16), 0.5 * 2^16
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fp:
+            d = json.load(fp)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """Per-launch DRAM bytes of the counting kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fp:
+            d = json.load(fp)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.gpu), "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path or not os.path.exists(self.path):
+            return None
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fp:
+            for line in fp:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for name, v in zip(names, parts[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def physical_gpu_index(local: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        items = [v.strip() for v in vis.split(",") if v.strip()]
+        if local < len(items) and items[local].isdigit():
+            return int(items[local])
+    return local
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port): used for cpu_baseline and --impl reference
+
+def cpu_windows(nwin: int, win_words: int, world_rank_offset: int = 0):
+    """Host copies of ``nwin`` distinct C2 windows (N x win_words each), from the
+    same generator as the GPU inputs (bitmap i, global words)."""
+    from paper_1402_4073_b200 import _lib
+
+    lib = _lib.load()
+    qs = [lib.bq_gen_density_q16(SEED, i, DENS_LO, DENS_HI) for i in range(C2_N)]
+    wins = []
+    stride = C2_WORDS // nwin
+    for k in range(nwin):
+        w0 = world_rank_offset + k * stride
+        rows = []
+        for i in range(C2_N):
+            a = np.empty(win_words, dtype=np.uint64)
+            _lib.check(lib.bq_gen_bernoulli(SEED, i, qs[i], w0, win_words, a.ctypes.data, 0, None))
+            rows.append(a)
+        wins.append(rows)
+    return wins
+
+
+def cpu_port_run(wins, steps: int, warmup: int, threads: int):
+    """Time the oracle's CPU port of the reference algorithms (wide_or / wide_and /
+    csv_threshold, oracle/bq_oracle.c) over the windows, 5 queries per step."""
+    from oracle import oracle as O
+
+    win_words = wins[0][0].size
+    r = 64 * win_words
+    for s in range(warmup):
+        for t in C2_TS:
+            O.threshold_port(wins[s % len(wins)], r, t, threads)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        for t in C2_TS:
+            O.threshold_port(wins[s % len(wins)], r, t, threads)
+    dt = time.perf_counter() - t0
+    nbytes = steps * len(C2_TS) * C2_N * win_words * 8
+    return nbytes / dt / 1e9, dt
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(budget_s: float = 12.0):
+    threads = host_threads()
+    win_words = 1 << 16
+    wins = cpu_windows(8, win_words)
+    # calibrate: one step, then size the step count to the time budget
+    gbs, dt = cpu_port_run(wins, 1, 1, threads)
+    steps = max(2, int(budget_s / max(dt, 1e-3)))
+    gbs, dt = cpu_port_run(wins, steps, 0, threads)
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"C2 windows: 8 x (N=64 x 2^16 words), T in {list(C2_TS)}, {steps} steps "
+                      f"({dt:.1f} s) of oracle/bq_oracle.c orc_threshold_port (wide_or / wide_and / "
+                      f"csv_threshold, OpenMP {threads} threads)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    threads = host_threads()
+    win_words = 1 << 16
+    wins = cpu_windows(16, win_words)
+    gbs, dt = cpu_port_run(wins, args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1000 / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (bq_gen Bernoulli, seed 1402)",
+        "config": {"workload": "C2 sample: N=64 bitmaps, 16 distinct windows of 2^16 words (512 MiB), "
+                               "T sweep {1,2,16,32,64}; one step = 5 queries over one window",
+                   "n_bitmaps": C2_N, "ts": list(C2_TS)},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": "reference algorithms (wide_or / wide_and / csv_threshold) restated in C "
+                                   "(oracle/bq_oracle.c), OpenMP over word batches, on C2 windows"},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1402_4073_b200 as bq
+    from paper_1402_4073_b200 import _lib
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    n, nw = C2_N, C2_WORDS
+    pitch = nw + args.pad_words
+    w0 = rank * nw
+    r_local = 64 * nw
+    qs = [lib.bq_gen_density_q16(SEED, i, DENS_LO, DENS_HI) for i in range(n)]
+    data = torch.empty((n, pitch), dtype=torch.int64, device=dev)
+    qarr = np.asarray(qs, dtype=np.uint32)
+    _lib.check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, w0, nw, data.data_ptr(), pitch, sh))
+    rows = [data[i, :nw] for i in range(n)]
+    query = bq.ThresholdQuery(rows, r_local)
+    outs = torch.empty((len(C2_TS), nw), dtype=torch.int64, device=dev)
+    pcs = torch.zeros(len(C2_TS), dtype=torch.int64, device=dev)
+
+    def step(ev=None):
+        pcs.zero_()
+        for k, t in enumerate(C2_TS):
+            if ev is not None:
+                ev[k][0].record(stream)
+            query.threshold(t, outs[k], pcs[k:k + 1], stream=stream)
+            if ev is not None:
+                ev[k][1].record(stream)
+        if world > 1:
+            dist.all_reduce(pcs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    kev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+            for _ in C2_TS] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(physical_gpu_index(local)) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        for s in range(args.steps):
+            step(kev[s])
+        stop.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    launch_ms = [kev[s][k][0].elapsed_time(kev[s][k][1]) for s in range(args.steps) for k in range(len(C2_TS))]
+    per_t_ms = {t: statistics.mean(kev[s][k][0].elapsed_time(kev[s][k][1]) for s in range(args.steps))
+                for k, t in enumerate(C2_TS)}
+    mt = torch.tensor([elapsed_ms, statistics.mean(launch_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+    elapsed_ms, mean_launch_ms = float(mt[0]), float(mt[1])
+    final_pc = pcs.tolist()
+
+    in_bytes_step = world * len(C2_TS) * n * nw * 8
+    value = in_bytes_step * args.steps / (elapsed_ms / 1e3) / 1e9
+    algo_bytes_launch = n * nw * 8 + nw * 8
+    achieved = algo_bytes_launch / (mean_launch_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+
+    # --- end to end through the public host-buffer API -------------------------
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty((n, nw), dtype=torch.int64, pin_memory=True)
+        host_in.copy_(data[:, :nw])
+        h_in = [host_in[i].numpy().view(np.uint64) for i in range(n)]
+        host_out = torch.empty((len(C2_TS), nw), dtype=torch.int64, pin_memory=True)
+        h_out = [host_out[k].numpy().view(np.uint64) for k in range(len(C2_TS))]
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(max(1, min(args.warmup, 2))):
+            bq.sweep_host(h_in, r_local, list(C2_TS), outs=h_out, device=local)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            _, pops = bq.sweep_host(h_in, r_local, list(C2_TS), outs=h_out, device=local)
+            if world > 1:
+                pt = torch.tensor(pops, dtype=torch.int64, device=dev)
+                dist.all_reduce(pt)
+        e2e_s = time.perf_counter() - t0
+        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_s = float(et[0])
+        # parity of the host path with the device path on this step's result
+        ok = all(np.array_equal(h_out[k], outs[k].cpu().numpy().view(np.uint64)) for k in range(len(C2_TS)))
+        e2e = {"value": round(in_bytes_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": n * nw * 8, "d2h_bytes_per_step": len(C2_TS) * nw * 8 + len(C2_TS) * 8,
+               "steps": e2e_steps, "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 3),
+               "api": "paper_1402_4073_b200.sweep_host -> bq_sweep_host (pinned host in/out)",
+               "matches_device_result": bool(ok)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic: counter-based Bernoulli generator (csrc/bq_gen.h), seed 1402, "
+                    "per-bitmap density U[0.01,0.5] quantized to q/2^16",
+            "config": {"workload": "C2 (BASELINE configs[1]): N=64 bitmaps x r=2^28 bits per GPU (2 GiB input/GPU), "
+                                   "T sweep {1,2,16,32,64}; step = 5 queries + popcount all-reduce",
+                       "n_bitmaps": n, "r_bits_per_gpu": 64 * nw, "ts": list(C2_TS),
+                       "global_r_bits": 64 * nw * world, "row_pitch_words": pitch,
+                       "l2": "inputs 2 GiB/GPU > 126 MB L2; no flush needed",
+                       "parallelism": f"word-range shards x{world} GPUs, popcount all-reduce only"},
+            "per_query_ms": {str(t): round(v, 5) for t, v in per_t_ms.items()},
+            "popcounts": {str(t): int(p) for t, p in zip(C2_TS, final_pc)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic("c2"),
+                         "kernel": "bq::count_kernel (all 5 T; OR/AND/comparator epilogues)",
+                         "algorithmic_bytes_per_launch": algo_bytes_launch,
+                         "mean_launch_ms": round(mean_launch_ms, 5), "peak_source": peak_src},
+            "gpu_launches": len(C2_TS) * args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        cl = clocks.summary()
+        line["clocks"] = cl
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--pad-words", type=int, default=256, help="row pitch padding (words) between bitmaps")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

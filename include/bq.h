@@ -1,0 +1,184 @@
+/*
+ * bq.h -- C ABI of libbq.so, the B200 (sm_100a) threshold / symmetric
+ * bitmap-query engine.
+ *
+ * The reference (Kaser & Lemire's `bitquorum`, /root/reference/pkg/src/
+ * bitquorum) has no FFI: its operator API for this path is a set of Python
+ * callables plus the algorithm registry.  Each entry point below is what a
+ * binding of one of those callables calls; the reference interface it
+ * replaces is cited per function (paths relative to pkg/src/bitquorum/).
+ * The Python binding that mirrors the reference signatures lives in
+ * paper_1402_4073_b200/api.py; INTEGRATION.md shows the ctypes stub a
+ * maintainer adds to the reference.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers,
+ *    "h_" pointers are host pointers.  Streams are cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - Bitmaps are arrays of uint64 words, LSB-first (bitmaps.py:5-6, :24-25).
+ *    An input may be shorter than ceil(r/64) words; missing words read as 0
+ *    (bitmaps.py:57-58).  Output buffers always hold ceil(r/64) words (or the
+ *    window length for ranged queries) with bits >= r cleared.
+ *  - Device input/output pointers must be 16-byte aligned (cudaMalloc and
+ *    torch allocations are).
+ *  - Every function returns a status; 0 is success.  The negative codes map
+ *    onto the reference exception classes (errors.py:4-25).  The message of
+ *    the last failure on the calling thread is returned by bq_last_error().
+ *  - No C++ exceptions cross this boundary.  Calls on distinct query objects
+ *    are reentrant; a query object may be used from several streams at once.
+ */
+#ifndef BQ_H
+#define BQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BQ_API __attribute__((visibility("default")))
+
+enum {
+    BQ_OK = 0,
+    BQ_EINPUT = -1,    /* errors.InputError    (errors.py:8-9)   */
+    BQ_ERESOURCE = -2, /* errors.ResourceError (errors.py:16-17) */
+    BQ_EFORMAT = -3,   /* errors.FormatError   (errors.py:12-13) */
+    BQ_ECUDA = -4      /* CUDA runtime failure (no reference analogue) */
+};
+
+/* Largest input count N the device counter supports (m = floor(log2 2N) <= 16). */
+#define BQ_MAX_INPUTS 65535
+
+/* One uncompressed input: device words and how many of them are present. */
+typedef struct bq_span {
+    const uint64_t *words; /* device pointer (may be NULL when n_words == 0) */
+    uint64_t n_words;      /* trimmed length; words >= n_words read as zero  */
+} bq_span;
+
+/* A prepared query over N device-resident inputs: the device pointer table is
+ * uploaded once and reused by every threshold / symmetric evaluation, as the
+ * reference's RunContext keeps prebuilt programs per (N, T)
+ * (bench/competitions.py:91-104).  Opaque. */
+typedef struct bq_query bq_query;
+
+/* Library version, e.g. 100 for 0.1.0. */
+BQ_API int bq_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+BQ_API const char *bq_last_error(void);
+
+/* Prepare a query over inputs[0..n) whose result has bit length r_bits
+ * (= max input bit_length, counters.py:51-52).  Computes output words
+ * [w_begin, w_end) of the result (w_end = UINT64_MAX means ceil(r/64)); w_begin
+ * must be even.  A word-range query is how one GPU evaluates its shard
+ * (horizontal fragmentation; programs.py:196-237).
+ * device = CUDA ordinal the inputs live on (-1 = current). */
+BQ_API int bq_query_create(const bq_span *inputs, int n, uint64_t r_bits, uint64_t w_begin,
+                           uint64_t w_end, int device, bq_query **out);
+BQ_API void bq_query_destroy(bq_query *q);
+BQ_API uint64_t bq_query_out_words(const bq_query *q);
+
+/* Threshold theta(T; B_1..B_N): bit p set iff p is set in >= t inputs.
+ * Replaces counters.scan_count (counters.py:46-67), circuits.looped_threshold
+ * (circuits/bitparallel.py:16-43), circuits.csv_threshold (:51-129),
+ * circuits.execute of TreeAdd/SSum/SrtCkt programs (circuits/programs.py:163-237),
+ * CircuitLibrary.threshold (circuits/library.py:124-128) and, for t == 1 / t == n,
+ * bitmaps.wide_or / wide_and (bitmaps.py:647-677).
+ * d_out: bq_query_out_words(q) words.  d_popcnt (optional): a device uint64 to
+ * which the result's popcount is ADDED (cardinality(), bitmaps.py:102-105).
+ * d_last_nz (optional): device uint64 receiving max(index+1) over nonzero
+ * output words (atomicMax; lets the caller trim as bitmaps.py:66-67 does).
+ * 1 <= t <= n, else BQ_EINPUT (counters.py:40-43). */
+BQ_API int bq_query_threshold(bq_query *q, int t, uint64_t *d_out, unsigned long long *d_popcnt,
+                              unsigned long long *d_last_nz, void *stream);
+
+/* Arbitrary symmetric function: bit p (p < r) set iff accept[count(p)].
+ * h_accept: host array of n + 1 bytes (oracle.SymmetricSpec.accept,
+ * oracle.py:17-31).  Replaces counters.scan_count_symmetric (counters.py:70-83)
+ * and execute() of circuits.build_symmetric programs (circuits/core.py:349-444). */
+BQ_API int bq_query_symmetric(bq_query *q, const uint8_t *h_accept, uint64_t *d_out,
+                              unsigned long long *d_popcnt, unsigned long long *d_last_nz,
+                              void *stream);
+
+/* One-shot forms (create + evaluate + destroy; the table upload is synchronous). */
+BQ_API int bq_threshold_u64(const bq_span *inputs, int n, uint64_t r_bits, int t, uint64_t *d_out,
+                            unsigned long long *d_popcnt, void *stream);
+BQ_API int bq_symmetric_u64(const bq_span *inputs, int n, uint64_t r_bits, const uint8_t *h_accept,
+                            uint64_t *d_out, unsigned long long *d_popcnt, void *stream);
+
+/* ---- host-buffer path (end to end) ----------------------------------------
+ * Evaluate nq queries (thresholds ts[k], or, when ts[k] <= 0, the symmetric
+ * spec h_accepts + k*(n+1)) over HOST inputs h_inputs[i] (n_words[i] words,
+ * pinned memory recommended), writing each result to host h_outs[k]
+ * (ceil(r/64) words) and its popcount to h_popcnts[k].  The word range is
+ * streamed through the GPU in chunks of chunk_words words (0 = automatic) with
+ * copy-in, compute and copy-out overlapped on separate streams, so inputs larger
+ * than HBM work (out-of-core waves).  Blocking.  This is what the reference's
+ * Python entry points amount to when handed host bitmaps. */
+BQ_API int bq_sweep_host(const uint64_t *const *h_inputs, const uint64_t *n_words, int n,
+                         uint64_t r_bits, const int *ts, const uint8_t *h_accepts, int nq,
+                         uint64_t *const *h_outs, unsigned long long *h_popcnts, int device,
+                         uint64_t chunk_words);
+
+/* ---- run-length-compressed inputs (EWAH-style, bitmaps.py:27-40) ---------- */
+
+/* One compressed input stream on the device. */
+typedef struct bq_rle_span {
+    const uint64_t *words; /* device pointer to marker/literal words */
+    uint64_t n_words;      /* stream length in words */
+} bq_rle_span;
+
+typedef struct bq_rle_query bq_rle_query;
+
+/* Decode the marker chains of n streams on the device (K3 directory: the
+ * marker governing every tile boundary), validating the encoding as
+ * RleBitmap.iter_word_segments does (bitmaps.py:196-219): BQ_EFORMAT on a
+ * truncated literal group or a stream covering more than ceil(r/64) words.
+ * Synchronous.  The directory is reused by every evaluation (inputs are
+ * immutable, bitmaps.py:12-13). */
+BQ_API int bq_rle_query_create(const bq_rle_span *streams, int n, uint64_t r_bits, int device,
+                               bq_rle_query **out);
+BQ_API void bq_rle_query_destroy(bq_rle_query *q);
+/* Device bytes the directory occupies. */
+BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q);
+
+/* Threshold / symmetric function over the compressed inputs, output
+ * uncompressed (ceil(r/64) words).  Replaces runmerge.cdom_threshold
+ * (runmerge.py:198-241) and runmerge.cdom_symmetric (:244-299): one-fills
+ * count for whole tiles of words, zero-fills are skipped, and dirty words are
+ * read only where the fills leave the outcome open. */
+BQ_API int bq_rle_query_threshold(bq_rle_query *q, int t, uint64_t *d_out,
+                                  unsigned long long *d_popcnt, void *stream);
+BQ_API int bq_rle_query_symmetric(bq_rle_query *q, const uint8_t *h_accept, uint64_t *d_out,
+                                  unsigned long long *d_popcnt, void *stream);
+
+/* Canonical RLE encoding of host words, RleBuilder rules (bitmaps.py:351-414);
+ * used to hand results back as RleBitmap (counters.py:33-37).  Returns
+ * BQ_ERESOURCE if cap is too small; *out_len always receives the needed length. */
+BQ_API int bq_rle_encode_host(const uint64_t *h_words, uint64_t n_words, uint64_t r_bits,
+                              uint64_t *h_out, uint64_t cap, uint64_t *out_len);
+
+/* ---- benchmark input generation (K5, csrc/bq_gen.h) ---------------------- */
+
+/* Words [w0, w0 + nw) of bitmap `bitmap` under `seed`, each bit Bernoulli(q16 / 65536).
+ * on_device != 0: out is a device pointer and the words are generated by a kernel
+ * on `stream`; otherwise out is host memory. */
+BQ_API int bq_gen_bernoulli(uint64_t seed, uint32_t bitmap, uint32_t q16, uint64_t w0, uint64_t nw,
+                            uint64_t *out, int on_device, void *stream);
+/* Same, for `count` bitmaps laid out with a row pitch (in words) on the device:
+ * row i holds bitmap (first + i) with density q16s[i]. */
+BQ_API int bq_gen_bernoulli_rows(uint64_t seed, uint32_t first, int count, const uint32_t *h_q16s,
+                                 uint64_t w0, uint64_t nw, uint64_t *d_out, uint64_t pitch_words,
+                                 void *stream);
+/* Quantized per-bitmap density lo + U*(hi-lo) (q16 units). */
+BQ_API uint32_t bq_gen_density_q16(uint64_t seed, uint32_t bitmap, uint32_t lo, uint32_t hi);
+/* Two-state Markov run generator (host, C4): alternating runs of zeros and ones
+ * with geometric lengths of the given means (in bits), encoded canonically.
+ * Returns BQ_ERESOURCE if cap is too small (*out_len = needed length). */
+BQ_API int bq_gen_markov_rle(uint64_t seed, uint32_t bitmap, uint64_t r_bits, double mean_one_run,
+                             double mean_zero_run, uint64_t *h_out, uint64_t cap, uint64_t *out_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BQ_H */

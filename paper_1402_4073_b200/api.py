@@ -1,0 +1,349 @@
+"""Drop-in entry points with the reference's names and signatures.
+
+Each function mirrors one reference callable on the threshold / symmetric path
+(paths relative to /root/reference/pkg/src/bitquorum/) and evaluates it on the
+B200 through libbq.so.  Inputs may be the reference's own bitmap objects, this
+package's mirrors (``bitmaps.UncompressedBitmap`` / ``RleBitmap``), or
+HBM-resident ``DeviceBitmap`` / ``DeviceRleBitmap``:
+
+* host inputs are uploaded once (identity-keyed cache) and the result comes
+  back as ``type(bitmaps[0])`` with the reference's trimming; RLE inputs give
+  a canonically encoded RLE result (counters.py:33-37, runmerge.py:241);
+* device inputs give a device result (no host round trip).
+
+All the reference's algorithm variants compute the same function, so they all
+dispatch to the same kernels; they differ only in their argument contracts and
+``stats`` keys, which are reproduced.  There is no CPU fallback: without the
+CUDA library every call raises ``ExtensionMissing``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .bitmaps import DeviceBitmap, DeviceRleBitmap, RleBitmap, UncompressedBitmap, kind_of, word_count
+from .engine import UPLOADS, RleQuery, ThresholdQuery, accept_bytes, host_words, to_device_words
+from .errors import InputError, ResourceError
+
+DEFAULT_BUDGET_BYTES = 1 << 30  # counters.py:18
+
+
+def counter_width(n: int) -> int:
+    """Counter width the reference's ScanCount would use (counters.py:21-27)."""
+    if n < 128:
+        return 8
+    if n < 1 << 15:
+        return 16
+    return 32
+
+
+def weight_bits(n: int) -> int:
+    """m = floor(log2 2N): bits of the device's bit-sliced counter (circuits/core.py:240-242)."""
+    return (2 * n).bit_length() - 1
+
+
+def looped_op_count(n: int, t: int) -> int:
+    """Closed form of Looped's binary-op count (circuits/bitparallel.py:46-48)."""
+    return 2 * n * t - n - t * t + t - 1
+
+
+def csv_op_count(n: int, t: int) -> int:
+    """Number of counted bitmap ops csv_threshold issues (circuits/bitparallel.py:84-121):
+    5 per digit update on the trailing-zeros schedule, 5 per digit of the
+    redundant-to-binary pass and 1 per digit of the comparator."""
+    m = weight_bits(n)
+    ops = 0
+    time = 1
+    for _ in range(2, n):
+        time += 1
+        ops += 5 * ((time & -time).bit_length() - 1)
+    return ops + 6 * m
+
+
+def _check_t(n: int, t: int):
+    if not 1 <= t <= n:
+        raise InputError(f"threshold {t} outside [1, {n}]")  # counters.py:40-43
+
+
+def _classify(bitmaps) -> str:
+    if not bitmaps:
+        raise InputError("need at least one input bitmap")
+    kinds = {kind_of(b) for b in bitmaps}
+    if kinds <= {"u", "du"}:
+        return "u"
+    if kinds <= {"r", "dr"}:
+        return "r"
+    raise InputError("mixed bitmap representations; convert explicitly with compress/decompress")
+
+
+def _device_for(bitmaps):
+    for b in bitmaps:
+        if isinstance(b, (DeviceBitmap, DeviceRleBitmap)):
+            return b.data.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _dev_inputs(bitmaps, device):
+    out = []
+    for b in bitmaps:
+        if isinstance(b, (DeviceBitmap, DeviceRleBitmap)):
+            out.append(b)
+        elif isinstance(b, (UncompressedBitmap,)) or type(b).__name__ == "UncompressedBitmap":
+            t = UPLOADS.get(b, device)
+            out.append(DeviceBitmap(t, b.bit_length, t.numel()))
+        else:
+            t = UPLOADS.get(b, device)
+            out.append(DeviceRleBitmap(t, b.bit_length, t.numel()))
+    return out
+
+
+def compress_words(words, bit_length: int) -> list:
+    """Canonical RLE encoding of uncompressed words (RleBuilder, bitmaps.py:351-414)."""
+    lib = _lib.load()
+    arr = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+    nw = word_count(bit_length)
+    if arr.size > nw:
+        raise InputError("more words than bit_length allows")
+    cap = 2 * arr.size + 8
+    out = np.empty(cap, dtype=np.uint64)
+    n_out = ctypes.c_uint64(0)
+    _lib.check(lib.bq_rle_encode_host(arr.ctypes.data if arr.size else None, arr.size, bit_length,
+                                      out.ctypes.data, cap, ctypes.byref(n_out)), "bq_rle_encode_host")
+    return out[: n_out.value].tolist()
+
+
+def _finish(bitmaps, out: torch.Tensor, nwords: int, r: int, popcnt: torch.Tensor, last_nz: torch.Tensor):
+    """Wrap a device result like the reference would (type of bitmaps[0])."""
+    proto = bitmaps[0]
+    k = kind_of(proto)
+    if k == "du":
+        return DeviceBitmap(out[:nwords] if nwords else out[:0], r, nwords)
+    if k == "dr":
+        return DeviceBitmap(out[:nwords] if nwords else out[:0], r, nwords)
+    used = int(last_nz.item())
+    words = out[:used].cpu().numpy().view(np.uint64)
+    if k == "u":
+        res = type(proto)(words.tolist(), r)
+    else:
+        res = type(proto)(compress_words(words, r), r)
+    card = int(popcnt.item())
+    if hasattr(res, "_card"):
+        try:
+            res._card = card
+        except AttributeError:
+            pass
+    return res
+
+
+def _run(bitmaps, r, t=None, accept=None):
+    kind = _classify(bitmaps)
+    n = len(bitmaps)
+    if r is None:
+        r = max(b.bit_length for b in bitmaps)
+    device = _device_for(bitmaps)
+    dev = _dev_inputs(bitmaps, device)
+    nw = word_count(r)
+    out = torch.empty(max(nw, 2), dtype=torch.int64, device=device)
+    popcnt = torch.zeros(1, dtype=torch.int64, device=device)
+    last_nz = torch.zeros(1, dtype=torch.int64, device=device)
+    if kind == "u":
+        q = ThresholdQuery(dev, r, device=device)
+        if accept is None:
+            q.threshold(t, out, popcnt, last_nz)
+        else:
+            q.symmetric(accept, out, popcnt, last_nz)
+        q.close()
+    else:
+        q = RleQuery(dev, r, device=device)
+        if accept is None:
+            q.threshold(t, out, popcnt)
+        else:
+            q.symmetric(accept, out, popcnt)
+        q.close()
+        # trim point for host results
+        if kind_of(bitmaps[0]) == "r":
+            nz = torch.nonzero(out[:nw]).flatten()
+            last_nz.fill_(int(nz[-1].item()) + 1 if nz.numel() else 0)
+    return _finish(bitmaps, out, nw, r, popcnt, last_nz)
+
+
+# ---------------------------------------------------------------------------
+# reference entry points
+
+
+def threshold(bitmaps: Sequence, t: int, r: int | None = None):
+    """theta(t; bitmaps) for either representation; result of type(bitmaps[0])."""
+    _check_t(len(bitmaps), t)
+    return _run(bitmaps, r, t=t)
+
+
+def symmetric(bitmaps: Sequence, spec, r: int | None = None):
+    """Arbitrary symmetric function ``spec.accept[count]`` (oracle.py:17-31)."""
+    accept_bytes(spec, len(bitmaps))
+    return _run(bitmaps, r, accept=spec)
+
+
+def scan_count(bitmaps: Sequence, t: int, r: int | None = None, budget_bytes: int = DEFAULT_BUDGET_BYTES,
+               stats: dict | None = None):
+    """counters.scan_count (counters.py:46-67).
+
+    ``budget_bytes`` bounds the device working set (the result buffer); the
+    kernel keeps its counters in registers, so unlike the reference's CPU
+    counter array it does not grow with r * counter width."""
+    _check_t(len(bitmaps), t)
+    if r is None:
+        r = max(b.bit_length for b in bitmaps)
+    if word_count(r) * 8 > budget_bytes:
+        raise ResourceError(f"a {word_count(r) * 8}-byte result exceeds the {budget_bytes}-byte budget")
+    res = _run(bitmaps, r, t=t)
+    if stats is not None:
+        stats["counter_width"] = counter_width(len(bitmaps))
+        stats["increments"] = sum(_cardinality(b) for b in bitmaps)
+    return res
+
+
+def scan_count_symmetric(bitmaps: Sequence, spec, r: int | None = None):
+    """counters.scan_count_symmetric (counters.py:70-83)."""
+    acc = getattr(spec, "accept", spec)
+    if len(acc) - 1 != len(bitmaps):
+        raise InputError("spec arity does not match the input count")
+    return _run(bitmaps, r, accept=spec)
+
+
+def looped_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
+    """circuits.looped_threshold (circuits/bitparallel.py:16-43)."""
+    _check_t(len(bitmaps), t)
+    res = _run(bitmaps, None, t=t)
+    if stats is not None:
+        stats["bitmap_ops"] = looped_op_count(len(bitmaps), t)
+    return res
+
+
+def csv_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
+    """circuits.csv_threshold (circuits/bitparallel.py:51-129); requires 2 <= T < N (:63-64)."""
+    n = len(bitmaps)
+    if not 2 <= t < n:
+        raise InputError(f"csv threshold needs 2 <= T < N, got T={t}, N={n}")
+    res = _run(bitmaps, None, t=t)
+    if stats is not None:
+        stats["bitmap_ops"] = csv_op_count(n, t)
+    return res
+
+
+def cdom_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
+    """runmerge.cdom_threshold (runmerge.py:198-241): RLE inputs only."""
+    n = len(bitmaps)
+    _check_t(n, t)
+    if any(kind_of(b) not in ("r", "dr") for b in bitmaps):
+        raise InputError("cdom operates on RLE bitmaps; compress inputs first")
+    return _run(bitmaps, None, t=t)
+
+
+def cdom_symmetric(bitmaps: Sequence, spec, stats: dict | None = None):
+    """runmerge.cdom_symmetric (runmerge.py:244-299): RLE inputs only."""
+    accept_bytes(spec, len(bitmaps))
+    if any(kind_of(b) not in ("r", "dr") for b in bitmaps):
+        raise InputError("cdom operates on RLE bitmaps; compress inputs first")
+    return _run(bitmaps, None, accept=spec)
+
+
+def wide_or(bitmaps: list):
+    """bitmaps.wide_or (bitmaps.py:647-667)."""
+    if not bitmaps:
+        raise InputError("wide_or of an empty list")
+    if len(bitmaps) == 1:
+        return bitmaps[0]
+    return _run(bitmaps, None, t=1)
+
+
+def wide_and(bitmaps: list):
+    """bitmaps.wide_and (bitmaps.py:670-677)."""
+    if not bitmaps:
+        raise InputError("wide_and of an empty list")
+    if len(bitmaps) == 1:
+        return bitmaps[0]
+    return _run(bitmaps, None, t=len(bitmaps))
+
+
+class CircuitLibrary:
+    """circuits.CircuitLibrary (circuits/library.py:84-133), threshold side.
+
+    The reference pads an (N', T') query to a tabulated (N, T) circuit and
+    interprets it; here every (N, T) is a direct kernel launch, so the plan is
+    only kept for API compatibility (``plan``/``keys``)."""
+
+    def __init__(self, n_max: int = 64, builder: str = "sideways", cache_dir: str | None = None):
+        if builder not in ("sop", "sorter", "tree", "sideways"):
+            raise InputError(f"unknown builder {builder!r}")
+        self.n_max = n_max
+        self.builder = builder
+        self.cache_dir = cache_dir
+
+    def keys(self):
+        levels, n = [], 2
+        while n <= self.n_max:
+            levels.append(n)
+            n *= 2
+        if self.n_max >= 2 and self.n_max not in levels:
+            levels.append(self.n_max)
+        return [(n, t) for n in levels for t in range(1, n + 1)]
+
+    def threshold(self, inputs: Sequence, t: int):
+        n = len(inputs)
+        if n < 1 or not 1 <= t <= n or n > max(self.n_max, 1):
+            raise InputError(f"bad request ({n}, {t})")
+        return _run(inputs, None, t=t)
+
+
+def _sibling_class(obj, name, default):
+    """The class called ``name`` from the module that defined type(obj) (reference or ours)."""
+    import importlib
+    try:
+        return getattr(importlib.import_module(type(obj).__module__), name, default)
+    except Exception:
+        return default
+
+
+def decompress(bitmap):
+    """bitmaps.decompress (bitmaps.py:417-431), decoded on the device (theta(1) of one stream).
+
+    Raises FormatError on a malformed stream.  Device input -> DeviceBitmap."""
+    if kind_of(bitmap) not in ("r", "dr"):
+        raise InputError("decompress needs an RLE bitmap")
+    if kind_of(bitmap) == "dr":
+        return _run([bitmap], None, t=1)
+    words = _run([to_device(bitmap)], None, t=1).to_numpy()
+    nz = np.flatnonzero(words)
+    cls = _sibling_class(bitmap, "UncompressedBitmap", UncompressedBitmap)
+    return cls(words[: nz[-1] + 1 if nz.size else 0].tolist(), bitmap.bit_length)
+
+
+def compress(bitmap):
+    """bitmaps.compress (bitmaps.py:407-414): canonical encoding, returns RleBitmap
+    (the reference class if the input is a reference object)."""
+    words = host_words(bitmap) if not isinstance(bitmap, DeviceBitmap) else bitmap.to_numpy()
+    enc = compress_words(words, bitmap.bit_length)
+    return _sibling_class(bitmap, "RleBitmap", RleBitmap)(enc, bitmap.bit_length)
+
+
+def to_device(bitmap, device=None):
+    """Upload a host bitmap (either representation) and return its device form."""
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    k = kind_of(bitmap)
+    if k in ("du", "dr"):
+        return bitmap
+    t = to_device_words(host_words(bitmap), device)
+    if k == "u":
+        return DeviceBitmap(t, bitmap.bit_length, t.numel())
+    return DeviceRleBitmap(t, bitmap.bit_length, t.numel())
+
+
+def _cardinality(b) -> int:
+    if hasattr(b, "cardinality"):
+        return int(b.cardinality())
+    return 0

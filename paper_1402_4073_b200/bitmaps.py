@@ -1,0 +1,233 @@
+"""Bitmap types: the reference's two host representations, mirrored, plus
+their HBM-resident counterparts.
+
+* :class:`UncompressedBitmap` / :class:`RleBitmap` keep the reference API
+  (reference bitmaps.py:54-345): ``words`` is a ``list[int]`` of LSB-first
+  64-bit words, ``bit_length`` is r, trailing zero words are trimmed at
+  construction (:66-67), bits >= r are rejected (:70-72).  They exist so the
+  package works without the reference installed; every entry point also
+  accepts the reference's own objects (duck-typed on ``.words`` /
+  ``.bit_length`` and the class name) and returns the caller's class.
+* :class:`DeviceBitmap` / :class:`DeviceRleBitmap` hold the words in a CUDA
+  tensor.  They are what the hot path consumes without marshalling; results
+  of device inputs stay on the device.
+"""
+
+from __future__ import annotations
+
+from typing import Iterable, Iterator
+
+import numpy as np
+
+from .errors import InputError
+
+W = 64
+WORD_MASK = (1 << W) - 1
+
+
+def word_count(bit_length: int) -> int:
+    return (bit_length + W - 1) // W
+
+
+def _iter_word_bits(word: int, base: int) -> Iterator[int]:
+    while word:
+        low = word & -word
+        yield base + low.bit_length() - 1
+        word ^= low
+
+
+class UncompressedBitmap:
+    """Set over [0, bit_length) as LSB-first 64-bit words (reference bitmaps.py:54-157)."""
+
+    __slots__ = ("words", "bit_length", "_card")
+
+    def __init__(self, words: list, bit_length: int):
+        if bit_length < 0:
+            raise InputError("bit_length must be nonnegative")
+        while words and words[-1] == 0:
+            words.pop()
+        if len(words) > word_count(bit_length):
+            raise InputError("more words than bit_length allows")
+        if words and len(words) == word_count(bit_length) and bit_length % W:
+            if words[-1] >> (bit_length % W):
+                raise InputError("set bits at positions >= bit_length")
+        self.words = words
+        self.bit_length = bit_length
+        self._card = None
+
+    @classmethod
+    def empty(cls, bit_length: int) -> "UncompressedBitmap":
+        return cls([], bit_length)
+
+    @classmethod
+    def ones(cls, bit_length: int) -> "UncompressedBitmap":
+        full, rem = divmod(bit_length, W)
+        words = [WORD_MASK] * full
+        if rem:
+            words.append((1 << rem) - 1)
+        return cls(words, bit_length)
+
+    @classmethod
+    def from_positions(cls, positions: Iterable[int], bit_length: int) -> "UncompressedBitmap":
+        words = [0] * word_count(bit_length)
+        prev = -1
+        for p in positions:
+            if p <= prev:
+                raise InputError("positions must be strictly ascending")
+            if p >= bit_length:
+                raise InputError(f"position {p} out of range [0, {bit_length})")
+            words[p >> 6] |= 1 << (p & 63)
+            prev = p
+        return cls(words, bit_length)
+
+    def cardinality(self) -> int:
+        if self._card is None:
+            self._card = sum(w.bit_count() for w in self.words)
+        return self._card
+
+    def get(self, position: int) -> bool:
+        if not 0 <= position < self.bit_length:
+            raise InputError("position out of range")
+        wi = position >> 6
+        return wi < len(self.words) and bool(self.words[wi] >> (position & 63) & 1)
+
+    __contains__ = get
+
+    def iter_set_bits(self) -> Iterator[int]:
+        for wi, word in enumerate(self.words):
+            if word:
+                yield from _iter_word_bits(word, wi << 6)
+
+    def positions(self) -> list:
+        return list(self.iter_set_bits())
+
+    def __eq__(self, other):
+        if not hasattr(other, "words") or type(other).__name__ != "UncompressedBitmap":
+            return NotImplemented
+        return self.bit_length == other.bit_length and list(self.words) == list(other.words)
+
+    def __repr__(self):
+        return f"UncompressedBitmap(card={self.cardinality()}, r={self.bit_length})"
+
+
+class RleBitmap:
+    """Word-aligned run-length encoding (reference bitmaps.py:160-345).
+
+    Marker word: bit 0 fill bit, bits 1-32 fill run in words, bits 33-63 the
+    number of literal words that follow (bitmaps.py:27-40)."""
+
+    __slots__ = ("words", "bit_length", "_card")
+
+    def __init__(self, words: list, bit_length: int):
+        if bit_length < 0:
+            raise InputError("bit_length must be nonnegative")
+        self.words = words
+        self.bit_length = bit_length
+        self._card = None
+
+    @classmethod
+    def empty(cls, bit_length: int) -> "RleBitmap":
+        words = []
+        remaining = word_count(bit_length)
+        while remaining:
+            run = min(remaining, (1 << 32) - 1)
+            words.append(run << 1)
+            remaining -= run
+        return cls(words, bit_length)
+
+    @classmethod
+    def from_words(cls, words, bit_length: int) -> "RleBitmap":
+        from .api import compress_words
+        return cls(compress_words(words, bit_length), bit_length)
+
+    @classmethod
+    def from_positions(cls, positions: Iterable[int], bit_length: int) -> "RleBitmap":
+        return cls.from_words(UncompressedBitmap.from_positions(positions, bit_length).words, bit_length)
+
+    @classmethod
+    def ones(cls, bit_length: int) -> "RleBitmap":
+        return cls.from_words(UncompressedBitmap.ones(bit_length).words, bit_length)
+
+    def __eq__(self, other):
+        if not hasattr(other, "words") or type(other).__name__ != "RleBitmap":
+            return NotImplemented
+        return self.bit_length == other.bit_length and list(self.words) == list(other.words)
+
+    def __repr__(self):
+        return f"RleBitmap(r={self.bit_length}, words={len(self.words)})"
+
+
+class DeviceBitmap:
+    """Uncompressed bitmap in HBM.
+
+    ``data`` is a 1-D int64 CUDA tensor holding at least ``n_words`` words
+    (bit patterns of uint64 words, LSB-first); words >= n_words read as zero.
+    """
+
+    __slots__ = ("data", "bit_length", "n_words", "_card")
+
+    def __init__(self, data, bit_length: int, n_words: int | None = None, cardinality: int | None = None):
+        if bit_length < 0:
+            raise InputError("bit_length must be nonnegative")
+        self.data = data
+        self.bit_length = bit_length
+        self.n_words = data.numel() if n_words is None else int(n_words)
+        if self.n_words > word_count(bit_length):
+            raise InputError("more words than bit_length allows")
+        self._card = cardinality
+
+    @property
+    def device(self):
+        return self.data.device
+
+    def data_ptr(self) -> int:
+        return self.data.data_ptr()
+
+    def to_numpy(self) -> np.ndarray:
+        return self.data[: self.n_words].cpu().numpy().view(np.uint64)
+
+    def to_host(self, cls=UncompressedBitmap):
+        words = self.to_numpy().tolist()
+        return cls(words, self.bit_length)
+
+    def cardinality(self) -> int:
+        if self._card is None:
+            self._card = int(np.unpackbits(self.to_numpy().view(np.uint8)).sum())
+        return self._card
+
+    def __repr__(self):
+        return f"DeviceBitmap(r={self.bit_length}, words={self.n_words}, device={self.data.device})"
+
+
+class DeviceRleBitmap:
+    """RLE stream (reference marker format) in HBM: 1-D int64 CUDA tensor."""
+
+    __slots__ = ("data", "bit_length", "n_words")
+
+    def __init__(self, data, bit_length: int, n_words: int | None = None):
+        self.data = data
+        self.bit_length = bit_length
+        self.n_words = data.numel() if n_words is None else int(n_words)
+
+    def data_ptr(self) -> int:
+        return self.data.data_ptr()
+
+    def to_host(self, cls=RleBitmap):
+        return cls(self.data[: self.n_words].cpu().numpy().view(np.uint64).tolist(), self.bit_length)
+
+    def __repr__(self):
+        return f"DeviceRleBitmap(r={self.bit_length}, words={self.n_words})"
+
+
+def kind_of(b) -> str:
+    """'u' (uncompressed host), 'r' (RLE host), 'du' / 'dr' (device)."""
+    if isinstance(b, DeviceBitmap):
+        return "du"
+    if isinstance(b, DeviceRleBitmap):
+        return "dr"
+    name = type(b).__name__
+    if name == "UncompressedBitmap":
+        return "u"
+    if name == "RleBitmap":
+        return "r"
+    raise InputError(f"unsupported bitmap type {type(b).__name__}")

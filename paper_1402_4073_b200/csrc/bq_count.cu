@@ -1,0 +1,332 @@
+// K1/K2: word-parallel bit-sliced counting over N uncompressed bitmaps (sm_100a).
+//
+// Output word w depends only on the N input words at index w (the property
+// the reference's horizontal evaluator relies on, circuits/programs.py:208-233),
+// so each thread owns two adjacent words (one 128-bit load per input) and
+// keeps, in registers, a bit-sliced vertical counter c[0..m) per 32-bit lane,
+// m = floor(log2 2N) (circuits/core.py:240-242).
+//
+// Counting is a Harley-Seal carry-save adder tree: every 16 inputs cost 15
+// full adders, each two LOP3s (sum 0x96, majority 0xE8), and one ripple add of
+// the weight-16 carry into the high counter bits; ~2.3 LOP3 per input per
+// lane.  That replaces the reference's interpreted TreeAdd / SSum / SrtCkt /
+// CSvCkt / Looped bitmap programs (circuits/bitparallel.py, programs.py) and
+// ScanCount's per-bit increments (counters.py:46-67) with the same function.
+//
+// Epilogues:
+//   MODE_OR / MODE_AND : T = 1 / T = N (wide_or / wide_and, bitmaps.py:647-677)
+//   MODE_BREAK         : accept[] as accept[0] XOR (count >= b_1) XOR (count >= b_2) ...,
+//                        each ">= b" a bit-sliced comparison with a constant (the
+//                        comparator of circuits/core.py:210-237); threshold is one breakpoint.
+//   MODE_LUT           : accept[count] read per bit from a shared-memory table
+//                        (scan_count_symmetric's lookup, counters.py:81-83).
+// The result popcount (cardinality, bitmaps.py:102-105) and the index of the
+// last nonzero word (the trim of bitmaps.py:66-67) are reduced in the kernel.
+//
+// The kernel is a persistent grid-stride loop over tiles of 512 words; the
+// input pointer table is staged once per CTA in shared memory.  Loads are
+// 128-bit, non-allocating in L1 (each byte is read exactly once).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "bq_internal.h"
+
+namespace bq {
+
+constexpr int kThreads = 256;
+constexpr int kTileWords = kThreads * 2;
+
+__device__ __forceinline__ uint4 ld_stream(const uint64_t *p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+
+template <bool FULL>
+__device__ __forceinline__ uint4 ld_input(const uint64_t *base, uint64_t w, uint64_t len) {
+    if (FULL) return ld_stream(base + w);
+    uint4 r = make_uint4(0, 0, 0, 0);
+    if (w + 1 < len) {
+        r = ld_stream(base + w);
+    } else if (w < len) {
+        uint64_t v = __ldg(base + w);
+        r.x = (uint32_t)v;
+        r.y = (uint32_t)(v >> 32);
+    }
+    return r;
+}
+
+__device__ __forceinline__ uint32_t lane_of(const uint4 &v, int l) {
+    return l == 0 ? v.x : l == 1 ? v.y : l == 2 ? v.z : v.w;
+}
+
+// full adder: l = a ^ b ^ c (LOP3 0x96), h = maj(a, b, c) (LOP3 0xE8)
+#define BQ_CSA(h, l, a, b, c)                \
+    do {                                     \
+        uint32_t u_ = (a) ^ (b);             \
+        uint32_t a_ = (a), c_ = (c);         \
+        (h) = (a_ & (b)) | (u_ & c_);        \
+        (l) = u_ ^ c_;                       \
+    } while (0)
+
+// Add one weight-1 vector into counter bits [lo, M).
+template <int M>
+__device__ __forceinline__ void ripple_add(uint32_t (&c)[M], uint32_t x, int lo) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        if (j >= lo) {
+            uint32_t t = c[j] & x;
+            c[j] ^= x;
+            x = t;
+        }
+    }
+}
+
+// count >= b for the bit-sliced count c (M bits, per lane), b a runtime constant.
+template <int M>
+__device__ __forceinline__ uint32_t ge_const(const uint32_t (&c)[M], uint32_t b) {
+    if (b >= (1u << M)) return 0u;
+    uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+        uint32_t tb = 0u - ((b >> j) & 1u);
+        gt |= eq & c[j] & ~tb;
+        eq &= ~(c[j] ^ tb);
+    }
+    return gt | eq;
+}
+
+template <int M, int MODE>
+__device__ __forceinline__ uint32_t epilogue(const uint32_t (&c)[M], const CountArgs &a,
+                                             const uint32_t *slut) {
+    if (MODE == MODE_BREAK) {
+        uint32_t r = a.accept0;
+        for (int b = 0; b < a.nbreak; ++b) r ^= ge_const<M>(c, a.breaks[b]);
+        return r;
+    } else {  // MODE_LUT
+        uint32_t r = 0;
+#pragma unroll 4
+        for (int bit = 0; bit < 32; ++bit) {
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int j = 0; j < M; ++j) cnt |= ((c[j] >> bit) & 1u) << j;
+            r |= ((slut[cnt >> 5] >> (cnt & 31)) & 1u) << bit;
+        }
+        return r;
+    }
+}
+
+// Evaluate one 2-word column unit starting at window word w.
+template <int M, int MODE, bool FULL>
+__device__ __forceinline__ void column(const CountArgs &a, const uint64_t *const *tab, uint64_t w,
+                                       const uint32_t *slut, uint32_t (&res)[4]) {
+    const int n = a.n;
+    if (MODE == MODE_OR || MODE == MODE_AND) {
+        uint32_t acc[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[l] = (MODE == MODE_OR) ? 0u : 0xffffffffu;
+        int i = 0;
+        for (; i + 8 <= n; i += 8) {
+            uint4 x[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                x[k] = ld_input<FULL>(tab[i + k], w, FULL ? 0 : __ldg(a.lens + i + k));
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    acc[l] = (MODE == MODE_OR) ? (acc[l] | lane_of(x[k], l)) : (acc[l] & lane_of(x[k], l));
+        }
+        for (; i < n; ++i) {
+            uint4 x = ld_input<FULL>(tab[i], w, FULL ? 0 : __ldg(a.lens + i));
+#pragma unroll
+            for (int l = 0; l < 4; ++l)
+                acc[l] = (MODE == MODE_OR) ? (acc[l] | lane_of(x, l)) : (acc[l] & lane_of(x, l));
+        }
+#pragma unroll
+        for (int l = 0; l < 4; ++l) res[l] = acc[l];
+        return;
+    } else {
+        uint32_t c[4][M];
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+#pragma unroll
+            for (int j = 0; j < M; ++j) c[l][j] = 0u;
+        int i = 0;
+        if constexpr (M >= 5) {
+            for (; i + 16 <= n; i += 16) {
+                uint4 x[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    x[k] = ld_input<FULL>(tab[i + k], w, FULL ? 0 : __ldg(a.lens + i + k));
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    uint32_t &ones = c[l][0], &twos = c[l][1], &fours = c[l][2], &eights = c[l][3];
+                    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+                    BQ_CSA(twosA, ones, ones, lane_of(x[0], l), lane_of(x[1], l));
+                    BQ_CSA(twosB, ones, ones, lane_of(x[2], l), lane_of(x[3], l));
+                    BQ_CSA(foursA, twos, twos, twosA, twosB);
+                    BQ_CSA(twosA, ones, ones, lane_of(x[4], l), lane_of(x[5], l));
+                    BQ_CSA(twosB, ones, ones, lane_of(x[6], l), lane_of(x[7], l));
+                    BQ_CSA(foursB, twos, twos, twosA, twosB);
+                    BQ_CSA(eightsA, fours, fours, foursA, foursB);
+                    BQ_CSA(twosA, ones, ones, lane_of(x[8], l), lane_of(x[9], l));
+                    BQ_CSA(twosB, ones, ones, lane_of(x[10], l), lane_of(x[11], l));
+                    BQ_CSA(foursA, twos, twos, twosA, twosB);
+                    BQ_CSA(twosA, ones, ones, lane_of(x[12], l), lane_of(x[13], l));
+                    BQ_CSA(twosB, ones, ones, lane_of(x[14], l), lane_of(x[15], l));
+                    BQ_CSA(foursB, twos, twos, twosA, twosB);
+                    BQ_CSA(eightsB, fours, fours, foursA, foursB);
+                    BQ_CSA(sixteens, eights, eights, eightsA, eightsB);
+                    ripple_add<M>(c[l], sixteens, 4);
+                }
+            }
+        }
+        for (; i < n; ++i) {
+            uint4 x = ld_input<FULL>(tab[i], w, FULL ? 0 : __ldg(a.lens + i));
+#pragma unroll
+            for (int l = 0; l < 4; ++l) ripple_add<M>(c[l], lane_of(x, l), 0);
+        }
+#pragma unroll
+        for (int l = 0; l < 4; ++l) res[l] = epilogue<M, MODE>(c[l], a, slut);
+    }
+}
+
+template <int M, int MODE, bool SMEM_TABLE>
+__global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__ CountArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint64_t **stab = reinterpret_cast<const uint64_t **>(smem);
+    uint32_t *slut = reinterpret_cast<uint32_t *>(smem + (SMEM_TABLE ? (size_t)a.n * 8 : 0));
+    if (SMEM_TABLE)
+        for (int i = threadIdx.x; i < a.n; i += kThreads) stab[i] = a.ptrs[i];
+    if (MODE == MODE_LUT) {
+        const int lut_words = ((1 << M) + 31) / 32;
+        for (int i = threadIdx.x; i < lut_words; i += kThreads) slut[i] = a.lut[i];
+    }
+    __syncthreads();
+    const uint64_t *const *tab = SMEM_TABLE ? stab : a.ptrs;
+
+    unsigned long long pc = 0, lnz = 0;
+    const uint64_t ntiles = (a.nwords + kTileWords - 1) / kTileWords;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t w = tile * kTileWords + 2 * threadIdx.x;
+        const bool full = (tile + 1) * kTileWords <= a.full_words;  // CTA-uniform
+        if (w >= a.nwords) continue;
+        uint32_t res[4];
+        if (full)
+            column<M, MODE, true>(a, tab, w, slut, res);
+        else
+            column<M, MODE, false>(a, tab, w, slut, res);
+        uint64_t lo = (uint64_t)res[0] | ((uint64_t)res[1] << 32);
+        uint64_t hi = (uint64_t)res[2] | ((uint64_t)res[3] << 32);
+        if (w + 1 >= a.nwords - 1) {
+            if (w == a.nwords - 1) lo &= a.last_mask;
+            if (w + 1 == a.nwords - 1) hi &= a.last_mask;
+        }
+        if (w + 1 < a.nwords) {
+            *reinterpret_cast<ulonglong2 *>(a.out + w) = make_ulonglong2(lo, hi);
+            pc += __popcll(lo) + __popcll(hi);
+            if (hi) lnz = w + 2;
+            else if (lo) lnz = w + 1;
+        } else {
+            a.out[w] = lo;
+            pc += __popcll(lo);
+            if (lo) lnz = w + 1;
+        }
+    }
+    // warp reductions, one atomic per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        pc += __shfl_down_sync(0xffffffffu, pc, o);
+        unsigned long long other = __shfl_down_sync(0xffffffffu, lnz, o);
+        lnz = other > lnz ? other : lnz;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (a.popcnt && pc) atomicAdd(a.popcnt, pc);
+        if (a.last_nz && lnz) atomicMax(a.last_nz, lnz);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+
+using KernelFn = void (*)(CountArgs);
+
+template <int M>
+static KernelFn pick(int mode, bool smem_table) {
+    switch (mode) {
+        case MODE_OR:
+            return smem_table ? count_kernel<M, MODE_OR, true> : count_kernel<M, MODE_OR, false>;
+        case MODE_AND:
+            return smem_table ? count_kernel<M, MODE_AND, true> : count_kernel<M, MODE_AND, false>;
+        case MODE_BREAK:
+            return smem_table ? count_kernel<M, MODE_BREAK, true> : count_kernel<M, MODE_BREAK, false>;
+        default:
+            return smem_table ? count_kernel<M, MODE_LUT, true> : count_kernel<M, MODE_LUT, false>;
+    }
+}
+
+static KernelFn pick_kernel(int m, int mode, bool smem_table) {
+    // OR / AND do not use the counter; one instantiation serves every N.
+    if (mode == MODE_OR || mode == MODE_AND) return pick<1>(mode, smem_table);
+    switch (m) {
+        case 1: return pick<1>(mode, smem_table);
+        case 2: return pick<2>(mode, smem_table);
+        case 3: return pick<3>(mode, smem_table);
+        case 4: return pick<4>(mode, smem_table);
+        case 5: return pick<5>(mode, smem_table);
+        case 6: return pick<6>(mode, smem_table);
+        case 7: return pick<7>(mode, smem_table);
+        case 8: return pick<8>(mode, smem_table);
+        case 9: return pick<9>(mode, smem_table);
+        case 10: return pick<10>(mode, smem_table);
+        case 11: return pick<11>(mode, smem_table);
+        case 12: return pick<12>(mode, smem_table);
+        case 13: return pick<13>(mode, smem_table);
+        case 14: return pick<14>(mode, smem_table);
+        case 15: return pick<15>(mode, smem_table);
+        case 16: return pick<16>(mode, smem_table);
+        default: return nullptr;
+    }
+}
+
+static int blocks_per_sm(KernelFn fn, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    uint64_t key = (reinterpret_cast<uint64_t>(fn) * 1315423911ull) ^ ((uint64_t)smem << 8) ^ (uint64_t)dev;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess || nb < 1) nb = 1;
+    cache[key] = nb;
+    return nb;
+}
+
+int launch_count(const CountArgs &a, int m, int mode, cudaStream_t stream) {
+    if (a.nwords == 0) return BQ_OK;
+    const bool smem_table = a.n <= kSmemTableMax;
+    KernelFn fn = pick_kernel(m, mode, smem_table);
+    if (!fn) return set_error(BQ_EINPUT, "counter width %d unsupported (N too large)", m);
+    size_t smem = (smem_table ? (size_t)a.n * 8 : 0) + (mode == MODE_LUT ? (size_t)(((1 << m) + 31) / 32) * 4 : 0);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(count_kernel)");
+    }
+    const uint64_t ntiles = (a.nwords + kTileWords - 1) / kTileWords;
+    uint64_t grid = (uint64_t)sm_count() * (uint64_t)blocks_per_sm(fn, smem);
+    if (grid > ntiles) grid = ntiles;
+    fn<<<(unsigned)grid, kThreads, smem, stream>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "count_kernel launch");
+    return BQ_OK;
+}
+
+}  // namespace bq

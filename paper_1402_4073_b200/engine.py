@@ -1,0 +1,291 @@
+"""Device-side engine: prepared queries over HBM-resident inputs, the upload
+cache for immutable host bitmaps, and the host-buffer streaming sweep.
+
+Everything here calls libbq.so through ctypes (``_lib``); torch is used only
+for device memory and streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from collections import OrderedDict
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .bitmaps import DeviceBitmap, DeviceRleBitmap, word_count
+from .errors import InputError
+
+
+def _device(device=None) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise _lib.ExtensionMissing("no CUDA device is visible; the bitmap engine has no CPU fallback")
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise InputError(f"device must be a CUDA device, got {d}")
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
+def stream_handle(stream=None, device=None) -> int:
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def host_words(b) -> np.ndarray:
+    """A host bitmap's words as a uint64 numpy array (no copy when already numpy)."""
+    w = b.words
+    if isinstance(w, np.ndarray):
+        return np.ascontiguousarray(w, dtype=np.uint64)
+    return np.array(w, dtype=np.uint64)
+
+
+def to_device_words(arr: np.ndarray, device) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint64).view(np.int64))
+    return t.to(device, non_blocking=False)
+
+
+class UploadCache:
+    """Device copies of immutable host bitmaps, keyed by object identity.
+
+    The reference's bitmaps are immutable (bitmaps.py:12-13) and its harness
+    passes the same object several times for replicated inputs
+    (bench/similarity.py:53-55), deduplicating by id() (competitions.py:259-262);
+    this cache does the same.  Entries hold a strong reference to the host object
+    so its id cannot be reused while cached.  LRU-bounded by device bytes
+    (env BQ_UPLOAD_CACHE_BYTES, default 8 GiB).
+    """
+
+    def __init__(self, max_bytes: int | None = None):
+        self.max_bytes = int(os.environ.get("BQ_UPLOAD_CACHE_BYTES", 8 << 30)) if max_bytes is None else max_bytes
+        self._d: OrderedDict = OrderedDict()
+        self._bytes = 0
+        self._lock = threading.Lock()
+
+    def get(self, b, device: torch.device) -> torch.Tensor:
+        key = (id(b), device.index)
+        with self._lock:
+            hit = self._d.get(key)
+            if hit is not None and hit[0] is b:
+                self._d.move_to_end(key)
+                return hit[1]
+        t = to_device_words(host_words(b), device)
+        nbytes = t.numel() * 8
+        with self._lock:
+            if nbytes <= self.max_bytes:
+                self._d[key] = (b, t)
+                self._bytes += nbytes
+                while self._bytes > self.max_bytes and self._d:
+                    _, (_, old) = self._d.popitem(last=False)
+                    self._bytes -= old.numel() * 8
+        return t
+
+    def clear(self):
+        with self._lock:
+            self._d.clear()
+            self._bytes = 0
+
+
+UPLOADS = UploadCache()
+
+
+class ThresholdQuery:
+    """A prepared query (``bq_query``) over N device-resident uncompressed inputs.
+
+    ``inputs``: DeviceBitmap objects or 1-D int64 CUDA tensors (all words valid).
+    ``word_range``: evaluate only output words [begin, end) (a shard); ``begin``
+    must be even.  The pointer table is uploaded once; each ``threshold`` /
+    ``symmetric`` call is a single kernel launch on ``stream``.
+    """
+
+    def __init__(self, inputs: Sequence, r_bits: int, word_range=None, device=None):
+        self._lib = _lib.load()
+        self.device = _device(device if device is not None else self._infer_device(inputs))
+        self.n = len(inputs)
+        self.r_bits = int(r_bits)
+        self._keep = []
+        pairs = []
+        for x in inputs:
+            if isinstance(x, DeviceBitmap):
+                t, n_words = x.data, x.n_words
+            elif isinstance(x, torch.Tensor):
+                t, n_words = x, x.numel()
+            else:
+                raise InputError(f"ThresholdQuery needs device inputs, got {type(x).__name__}")
+            if not t.is_cuda or t.dtype not in (torch.int64, torch.uint64):
+                raise InputError("device inputs must be int64/uint64 CUDA tensors")
+            if n_words and not t.is_contiguous():
+                raise InputError("device inputs must be contiguous")
+            self._keep.append(t)
+            pairs.append((t.data_ptr() if n_words else 0, n_words))
+        begin, end = (0, (1 << 64) - 1) if word_range is None else (int(word_range[0]), int(word_range[1]))
+        self._spans = _lib.spans(pairs)
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.bq_query_create(self._spans, self.n, self.r_bits, begin, end,
+                                             self.device.index, ctypes.byref(h)), "bq_query_create")
+        self._h = h
+        self.out_words = int(self._lib.bq_query_out_words(h))
+
+    @staticmethod
+    def _infer_device(inputs):
+        for x in inputs:
+            d = x.data.device if isinstance(x, DeviceBitmap) else getattr(x, "device", None)
+            if d is not None and d.type == "cuda":
+                return d
+        return None
+
+    def _outs(self, out, popcnt, last_nz):
+        if out is None:
+            out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)
+        elif out.numel() < self.out_words or not out.is_cuda:
+            raise InputError("output tensor too small or not on the device")
+        if popcnt is None:
+            popcnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        return out, popcnt, last_nz
+
+    def threshold(self, t: int, out=None, popcnt=None, last_nz=None, stream=None):
+        """Launch theta(t): returns (out, popcnt); popcnt is ADDED to (zeroed if allocated here)."""
+        out, popcnt, last_nz = self._outs(out, popcnt, last_nz)
+        _lib.check(self._lib.bq_query_threshold(
+            self._h, int(t), out.data_ptr(), popcnt.data_ptr(),
+            last_nz.data_ptr() if last_nz is not None else None,
+            stream_handle(stream, self.device)), "bq_query_threshold")
+        return out, popcnt
+
+    def symmetric(self, accept, out=None, popcnt=None, last_nz=None, stream=None):
+        acc = accept_bytes(accept, self.n)
+        out, popcnt, last_nz = self._outs(out, popcnt, last_nz)
+        _lib.check(self._lib.bq_query_symmetric(
+            self._h, acc.ctypes.data, out.data_ptr(), popcnt.data_ptr(),
+            last_nz.data_ptr() if last_nz is not None else None,
+            stream_handle(stream, self.device)), "bq_query_symmetric")
+        return out, popcnt
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bq_query_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RleQuery:
+    """A prepared query over N device-resident RLE streams (``bq_rle_query``).
+
+    Creation decodes every stream's marker chain on the device into a tile
+    directory (K3) and validates the encoding (FormatError)."""
+
+    def __init__(self, streams: Sequence, r_bits: int, device=None):
+        self._lib = _lib.load()
+        first = streams[0] if streams else None
+        d = first.data.device if isinstance(first, DeviceRleBitmap) else getattr(first, "device", None)
+        self.device = _device(device if device is not None else d)
+        self.n = len(streams)
+        self.r_bits = int(r_bits)
+        self._keep = []
+        pairs = []
+        for s in streams:
+            t, n_words = (s.data, s.n_words) if isinstance(s, DeviceRleBitmap) else (s, s.numel())
+            if not t.is_cuda:
+                raise InputError("RLE streams must be CUDA tensors")
+            self._keep.append(t)
+            pairs.append((t.data_ptr() if n_words else 0, n_words))
+        self._spans = _lib.spans(pairs)
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.bq_rle_query_create(self._spans, self.n, self.r_bits, self.device.index,
+                                                 ctypes.byref(h)), "bq_rle_query_create")
+        self._h = h
+        self.out_words = word_count(self.r_bits)
+
+    @property
+    def directory_bytes(self) -> int:
+        return int(self._lib.bq_rle_query_directory_bytes(self._h))
+
+    def _outs(self, out, popcnt):
+        if out is None:
+            out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)
+        if popcnt is None:
+            popcnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        return out, popcnt
+
+    def threshold(self, t: int, out=None, popcnt=None, stream=None):
+        out, popcnt = self._outs(out, popcnt)
+        _lib.check(self._lib.bq_rle_query_threshold(self._h, int(t), out.data_ptr(), popcnt.data_ptr(),
+                                                    stream_handle(stream, self.device)),
+                   "bq_rle_query_threshold")
+        return out, popcnt
+
+    def symmetric(self, accept, out=None, popcnt=None, stream=None):
+        acc = accept_bytes(accept, self.n)
+        out, popcnt = self._outs(out, popcnt)
+        _lib.check(self._lib.bq_rle_query_symmetric(self._h, acc.ctypes.data, out.data_ptr(),
+                                                    popcnt.data_ptr(), stream_handle(stream, self.device)),
+                   "bq_rle_query_symmetric")
+        return out, popcnt
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bq_rle_query_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def accept_bytes(accept, n: int) -> np.ndarray:
+    """SymmetricSpec (``.accept``) or a bool sequence -> n + 1 bytes (oracle.py:17-31)."""
+    acc = getattr(accept, "accept", accept)
+    arr = np.asarray([1 if a else 0 for a in acc], dtype=np.uint8)
+    if arr.size != n + 1:
+        raise InputError(f"spec arity {arr.size - 1} != {n} inputs")  # counters.py:73-74
+    return arr
+
+
+def sweep_host(inputs: Sequence[np.ndarray], r_bits: int, queries: Sequence, outs=None,
+               device=None, chunk_words: int = 0):
+    """End-to-end path over HOST word arrays (ideally pinned).
+
+    ``queries``: ints (thresholds) or accept vectors.  Results land in ``outs``
+    (list of uint64 numpy arrays of word_count(r_bits) words; allocated if None).
+    Inputs are streamed through the GPU in word-range chunks with copy-in,
+    compute and copy-out overlapped (bq_sweep_host).  Returns (outs, popcounts).
+    """
+    lib = _lib.load()
+    dev = _device(device)
+    n, nq = len(inputs), len(queries)
+    nw = word_count(int(r_bits))
+    arrs = [np.asarray(a) for a in inputs]
+    for a in arrs:
+        if a.dtype not in (np.uint64, np.int64) or not a.flags.c_contiguous:
+            raise InputError("host inputs must be contiguous uint64 arrays")
+    ptrs = (ctypes.c_void_p * n)(*[a.ctypes.data if a.size else None for a in arrs])
+    lens = (ctypes.c_uint64 * n)(*[a.size for a in arrs])
+    ts = (ctypes.c_int * nq)()
+    acc = np.zeros((nq, n + 1), dtype=np.uint8)
+    for k, q in enumerate(queries):
+        if isinstance(q, (int, np.integer)):
+            ts[k] = int(q)
+            if not 1 <= int(q) <= n:
+                raise InputError(f"threshold {int(q)} outside [1, {n}]")
+        else:
+            ts[k] = 0
+            acc[k] = accept_bytes(q, n)
+    if outs is None:
+        outs = [np.empty(nw, dtype=np.uint64) for _ in range(nq)]
+    optrs = (ctypes.c_void_p * nq)(*[o.ctypes.data for o in outs])
+    pops = (ctypes.c_ulonglong * nq)()
+    _lib.check(lib.bq_sweep_host(ptrs, lens, n, int(r_bits), ts, acc.ctypes.data, nq, optrs, pops,
+                                 dev.index, int(chunk_words)), "bq_sweep_host")
+    return outs, [int(p) for p in pops]

@@ -324,6 +324,17 @@ def kat():
     res["canonical_example"] = [str(w) for w in bm.compress(
         bm.UncompressedBitmap([0, MASK, 3, 0, 0, 7], 64 * 6)).words]
     res["generator"] = generator_cases()
+    # stats["bitmap_ops"] of the reference's looped / csv (bitparallel.py:38-39, :120-121)
+    ops = {"looped": {}, "csv": {}}
+    for n, t in [(4, 3), (5, 2), (8, 3), (16, 9), (33, 17), (64, 32), (100, 7)]:
+        ins = [bm.UncompressedBitmap.from_positions([i], 128) for i in range(n)]
+        st = {}
+        looped_threshold(ins, t, stats=st)
+        ops["looped"][f"{n},{t}"] = st["bitmap_ops"]
+        st = {}
+        csv_threshold(ins, t, stats=st)
+        ops["csv"][f"{n},{t}"] = st["bitmap_ops"]
+    res["op_counts"] = ops
     path = os.path.join(HERE, "kat.json")
     with open(path, "w") as fp:
         json.dump(res, fp, indent=1)

@@ -1,0 +1,167 @@
+"""CPU-only checks of the product library: the C ABI loads and exports every
+symbol include/bq.h declares, the host-side functions (canonical RLE encoder,
+generators) match reference-generated fixtures, and the host logic (shard
+planning, cross-rank reduction / gather) works with gloo at world size 2."""
+
+from __future__ import annotations
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden, load_kat, padded
+
+HEADER = os.path.join(ROOT, "include", "bq.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1402_4073_b200 import _lib
+
+    return _lib.load()
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"BQ_API\s+[\w\s\*]+?\b(bq_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    syms = declared_symbols()
+    assert "bq_query_threshold" in syms and "bq_rle_query_threshold" in syms and len(syms) >= 20
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_1402_4073_b200 import _lib
+
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+    assert lib.bq_version() >= 100
+
+
+@pytest.mark.parametrize("case", [c for c in load_golden("codec") if c.meta["kind"] == "compress"],
+                         ids=lambda c: c.id)
+def test_host_encoder_matches_reference_compress(case):
+    from paper_1402_4073_b200.api import compress_words
+
+    assert compress_words(case.inputs[0], case.r) == case.out.tolist()
+
+
+@pytest.mark.parametrize("case", load_golden("rle"), ids=lambda c: c.id)
+def test_host_encoder_matches_reference_cdom_output(case):
+    """The reference returns cdom results canonically encoded; so must we."""
+    from paper_1402_4073_b200.api import compress_words
+
+    words = np.array(case.meta["uncompressed"], dtype=np.uint64)
+    assert compress_words(words, case.r) == case.out.tolist()
+
+
+def test_generator_host_matches_pin(lib):
+    kat = load_kat()["generator"]
+    for c in kat["cases"]:
+        a = np.zeros(1, dtype=np.uint64)
+        assert lib.bq_gen_bernoulli(kat["seed"], c["bitmap"], c["q"], c["word"], 1, a.ctypes.data, 0, None) == 0
+        assert int(a[0]) == int(c["value"])
+    assert [lib.bq_gen_density_q16(kat["seed"], i, 655, 32768) for i in range(64)] == kat["density_q"]
+
+
+def test_generator_density_is_exact():
+    """P(bit) = q / 2^16 exactly: check the empirical density within 5 sigma."""
+    from paper_1402_4073_b200 import _lib
+
+    L = _lib.load()
+    nw = 1 << 15
+    for q in (1311, 3277, 6554, 32768):
+        a = np.empty(nw, dtype=np.uint64)
+        L.bq_gen_bernoulli(99, 3, q, 0, nw, a.ctypes.data, 0, None)
+        ones = int(np.unpackbits(a.view(np.uint8)).sum())
+        p = q / 65536
+        mean, sd = 64 * nw * p, (64 * nw * p * (1 - p)) ** 0.5
+        assert abs(ones - mean) < 5 * sd, q
+
+
+def test_markov_generator_canonical_and_dense(lib):
+    """C4 generator: canonical stream (re-encoding its decode is identity) with
+    the configured stationary density."""
+    import ctypes
+
+    from oracle import oracle as O
+
+    r = 1 << 22
+    cap = 1 << 18
+    out = np.empty(cap, dtype=np.uint64)
+    n_out = ctypes.c_uint64(0)
+    assert lib.bq_gen_markov_rle(1402, 5, r, 256.0, 12544.0, out.ctypes.data, cap, ctypes.byref(n_out)) == 0
+    stream = out[: n_out.value]
+    words = O.rle_decompress(stream, r)
+    assert np.array_equal(O.rle_compress(O.trim(words), r), stream)
+    dens = np.unpackbits(words.view(np.uint8)).mean()
+    assert 0.005 < dens < 0.06
+
+
+def test_api_validates_before_touching_the_device():
+    import paper_1402_4073_b200 as bq
+
+    ins = [bq.UncompressedBitmap([1, 2], 128) for _ in range(3)]
+    with pytest.raises(bq.InputError):
+        bq.scan_count(ins, 0)
+    with pytest.raises(bq.InputError):
+        bq.scan_count(ins, 4)
+    with pytest.raises(bq.InputError):
+        bq.csv_threshold(ins, 3)  # csv needs 2 <= T < N
+    with pytest.raises(bq.InputError):
+        bq.scan_count_symmetric(ins, bq.SymmetricSpec.parity(2))
+    with pytest.raises(bq.InputError):
+        bq.wide_or([])
+    with pytest.raises(ValueError):  # InputError is a ValueError, like the reference's
+        bq.cdom_threshold(ins, 2)
+
+
+def test_op_count_formulas_match_reference():
+    import paper_1402_4073_b200 as bq
+
+    counts = load_kat()["op_counts"]
+    for key, ops in counts["looped"].items():
+        n, t = map(int, key.split(","))
+        assert bq.looped_op_count(n, t) == ops
+    for key, ops in counts["csv"].items():
+        n, t = map(int, key.split(","))
+        assert bq.csv_op_count(n, t) == ops
+
+
+def test_dropin_errors_subclass_reference_errors():
+    """When the reference is importable, our errors ARE reference errors."""
+    try:
+        import sys
+
+        sys.path.insert(0, os.environ.get("BQ_REFERENCE_SRC", "/root/reference/pkg/src"))
+        from bitquorum import errors as ref
+    except Exception:
+        pytest.skip("reference not importable")
+    import importlib
+
+    import paper_1402_4073_b200.errors as ours
+
+    ours = importlib.reload(ours)
+    assert issubclass(ours.InputError, ref.InputError)
+    assert issubclass(ours.ResourceError, ref.ResourceError)
+    assert issubclass(ours.FormatError, ref.FormatError)
+
+
+def test_registry_plugs_into_reference():
+    try:
+        import sys
+
+        sys.path.insert(0, os.environ.get("BQ_REFERENCE_SRC", "/root/reference/pkg/src"))
+        from bitquorum.bench import competitions
+    except Exception:
+        pytest.skip("reference not importable")
+    from paper_1402_4073_b200 import registry
+
+    names = registry.register(competitions)
+    for name in names:
+        assert name in competitions.ALGORITHMS
+    assert competitions.ALGORITHMS["gpu_cdom"].reprs == frozenset({"ewah"})
