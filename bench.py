@@ -376,8 +376,248 @@ def run_ours(args):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# the other BASELINE configs (parity-test cases; extra lines via --workload)
+
+def _timed_launches(torch, launch, steps, warmup, stream, flush=None):
+    """Run `launch()` (which enqueues kernels on `stream`) warmup+steps times;
+    return per-launch CUDA-event times in ms.  `flush()` (L2 flush) runs
+    between launches outside the events."""
+    for _ in range(warmup):
+        if flush:
+            flush()
+        launch()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for s in range(steps):
+        if flush:
+            flush()
+        ev[s][0].record(stream)
+        launch()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def _line(workload, value, per_launch_ms, algo_bytes, steps, warmup, config, extra=None, unit="GB/s",
+          traffic_key=None):
+    peak, peak_src = measured_peak()
+    mean_ms = statistics.mean(per_launch_ms)
+    achieved = algo_bytes / (mean_ms / 1e3) / 1e9
+    line = {"metric": METRIC, "workload": workload, "value": round(value, 3), "unit": unit, "n_gpus": 1,
+            "steps": steps, "warmup": warmup, "ms_per_step": round(sum(per_launch_ms) / len(per_launch_ms), 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (csrc/bq_gen.h generators, seed 1402)", "config": config,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(traffic_key or workload),
+                         "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": round(mean_ms, 5),
+                         "peak_source": peak_src},
+            "gpu_launches": len(per_launch_ms)}
+    if extra:
+        line.update(extra)
+    return line
+
+
+def run_c1(args, torch, bq, lib, dev, stream):
+    """Config 1: N=8, r=2^20, p=0.1, T=3 (1 MiB: L2-resident, launch-bound)."""
+    n, nw, t = 8, 1 << 14, 3
+    data = torch.empty((n, nw), dtype=torch.int64, device=dev)
+    qarr = np.full(n, 6554, dtype=np.uint32)
+    _lib_check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, 0, nw, data.data_ptr(), nw, stream.cuda_stream))
+    q = bq.ThresholdQuery([data[i] for i in range(n)], 64 * nw)
+    out = torch.empty(nw, dtype=torch.int64, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    ms = _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), args.steps, args.warmup, stream,
+                         flush=lambda: scratch.fill_(1))
+    in_bytes = n * nw * 8
+    from oracle import oracle as O
+    host = [data[i].cpu().numpy().view(np.uint64) for i in range(n)]
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 2.0:
+        O.threshold_port(host, 64 * nw, t, host_threads())
+        reps += 1
+    cpu_gbs = reps * in_bytes / (time.perf_counter() - t0) / 1e9
+    exact = np.array_equal(out.cpu().numpy().view(np.uint64), O.scan_count(host, 64 * nw, t))
+    return _line("c1", in_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, in_bytes + nw * 8, args.steps, args.warmup,
+                 {"workload": "C1: N=8, r=2^20 bits, p=0.1 (q=6554), T=3; L2 flushed (256 MB write) between launches",
+                  "n_bitmaps": n, "r_bits": 64 * nw, "t": t},
+                 {"matches_oracle": bool(exact),
+                  "cpu_baseline": {"value": round(cpu_gbs, 3), "unit": "GB/s", "cores": host_threads(), "kind": "port",
+                                   "sample": "full C1, orc_threshold_port (csv_threshold port), 2 s"}})
+
+
+def run_c3(args, torch, bq, lib, dev, stream):
+    """Config 3: N=256, r=2^26, p=0.05, accept = count in [2, 10] (2 GiB)."""
+    n, nw = 256, 1 << 20
+    pitch = nw + args.pad_words
+    data = torch.empty((n, pitch), dtype=torch.int64, device=dev)
+    qarr = np.full(n, 3277, dtype=np.uint32)
+    _lib_check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, 0, nw, data.data_ptr(), pitch,
+                                         stream.cuda_stream))
+    q = bq.ThresholdQuery([data[i, :nw] for i in range(n)], 64 * nw)
+    acc = [2 <= k <= 10 for k in range(n + 1)]
+    out = torch.empty(nw, dtype=torch.int64, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    ms = _timed_launches(torch, lambda: q.symmetric(acc, out, pc, stream=stream), args.steps, args.warmup, stream)
+    pc.zero_()
+    q.symmetric(acc, out, pc, stream=stream)
+    in_bytes = n * nw * 8
+    from oracle import oracle as O
+    win = 1 << 14
+    host = [data[i, :win].cpu().numpy().view(np.uint64) for i in range(n)]
+    exact = np.array_equal(out[:win].cpu().numpy().view(np.uint64), O.scan_count_symmetric(host, 64 * win, acc))
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 5.0:
+        O.symmetric_port(host, 64 * win, acc, host_threads())
+        reps += 1
+    cpu_gbs = reps * n * win * 8 / (time.perf_counter() - t0) / 1e9
+    return _line("c3", in_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, in_bytes + nw * 8, args.steps, args.warmup,
+                 {"workload": "C3: N=256, r=2^26 bits, p=0.05 (q=3277), accept = [2 <= count <= 10] (2 GiB)",
+                  "n_bitmaps": n, "r_bits": 64 * nw, "accept": "interval [2,10]"},
+                 {"matches_oracle_window": bool(exact), "popcount": int(pc.item()),
+                  "cpu_baseline": {"value": round(cpu_gbs, 3), "unit": "GB/s", "cores": host_threads(), "kind": "port",
+                                   "sample": "C3 window N=256 x 2^14 words, orc_symmetric_port, 5 s"}})
+
+
+def _markov_streams(lib, n, r, m1, m0, threads):
+    """Generate n C4 streams on the host (ctypes releases the GIL -> threads)."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(i):
+        cap = max(4096, int(r / 64 * 0.2))
+        while True:
+            buf = np.empty(cap, dtype=np.uint64)
+            nout = ctypes.c_uint64(0)
+            rc = lib.bq_gen_markov_rle(SEED, i, r, m1, m0, buf.ctypes.data, cap, ctypes.byref(nout))
+            if rc == 0:
+                return buf[: nout.value].copy()
+            cap = int(nout.value) + 16
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        return list(ex.map(one, range(n)))
+
+
+def run_c4(args, torch, bq, lib, dev, stream):
+    """Config 4: N=1024 RLE bitmaps, r=2^30, one-runs mean 256 bits, zero-runs mean
+    12544 (density 0.02, interpretation A of SURVEY App. B), T=50; output uncompressed."""
+    n, r, t = 1024, 1 << 30, 50
+    m1, m0 = 256.0, 12544.0
+    t_gen = time.perf_counter()
+    streams = _markov_streams(lib, n, r, m1, m0, host_threads())
+    t_gen = time.perf_counter() - t_gen
+    comp_words = sum(s.size for s in streams)
+    flat = torch.empty(comp_words + 2 * n, dtype=torch.int64, pin_memory=True)
+    offs = []
+    o = 0
+    fnp = flat.numpy().view(np.uint64)
+    for s in streams:
+        fnp[o:o + s.size] = s
+        offs.append((o, s.size))
+        o += s.size + (s.size & 1)
+    dflat = flat.to(dev)
+    dstreams = [bq.DeviceRleBitmap(dflat[a:a + b] if b else dflat[:0], r, b) for a, b in offs]
+    torch.cuda.synchronize()
+    t_dir = time.perf_counter()
+    q = bq.RleQuery(dstreams, r)
+    t_dir = time.perf_counter() - t_dir
+    nw = r // 64
+    out = torch.empty(nw, dtype=torch.int64, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    ms = _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), args.steps, args.warmup, stream,
+                         flush=lambda: scratch.fill_(1))
+    pc.zero_()
+    q.threshold(t, out, pc, stream=stream)
+    comp_bytes = comp_words * 8
+    from oracle import oracle as O
+    # parity on a window: the first 2^20 bits of every stream (the generator is sequential, so a
+    # run with r = 2^20 reproduces exactly the prefix of the full stream)
+    wr = 1 << 20
+    wstreams = _markov_streams(lib, n, wr, m1, m0, host_threads())
+    t0 = time.perf_counter()
+    wexp = O.cdom_threshold(wstreams, wr, t)
+    cpu_s = time.perf_counter() - t0
+    exact_window = np.array_equal(out[: wr // 64].cpu().numpy().view(np.uint64), wexp)
+    wbytes = sum(s.size for s in wstreams) * 8
+    line = _line("c4", comp_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, comp_bytes + nw * 8, args.steps,
+                 args.warmup,
+                 {"workload": "C4: N=1024 RLE (EWAH-style) bitmaps, r=2^30 bits, Markov runs (ones mean 256, zeros "
+                              "mean 12544 bits; density 0.02), T=50; output uncompressed; L2 flushed between launches",
+                  "n_bitmaps": n, "r_bits": r, "t": t, "compressed_bytes": comp_bytes,
+                  "uncompressed_equivalent_bytes": n * nw * 8},
+                 {"value_uncompressed_equivalent_gbs": round(n * nw * 8 / (statistics.mean(ms) / 1e3) / 1e9, 1),
+                  "popcount": int(pc.item()), "directory_build_s": round(t_dir, 4),
+                  "directory_bytes": q.directory_bytes, "host_generation_s": round(t_gen, 2),
+                  "matches_oracle_window": bool(exact_window),
+                  "cpu_baseline": {"value": round(wbytes / cpu_s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                                   "sample": "oracle cdom_threshold (runmerge.py heap sweep restated in C, single "
+                                             f"thread as the reference) on the first 2^20 bits of all 1024 streams "
+                                             f"({wbytes} compressed bytes, {cpu_s:.2f} s)"}})
+    return line
+
+
+def run_c5(args, torch, bq, lib, dev, stream):
+    """Config 5 at one GPU: N=511, r=2^32, p=0.5, T=256 (256 GiB) does not fit in
+    HBM, so it runs as generate -> compute waves of 2^23 words (32 GiB) each;
+    only the query kernels are timed.  Each wave is one GPU's shard at 8 GPUs."""
+    n, total, t = 511, 1 << 26, 256
+    wave = 1 << 23
+    pitch = wave + args.pad_words
+    data = torch.empty((n, pitch), dtype=torch.int64, device=dev)
+    qarr = np.full(n, 32768, dtype=np.uint32)
+    out = torch.empty(wave, dtype=torch.int64, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    ms_all = []
+    steps = max(1, args.steps // 10)
+    for w0 in range(0, total, wave):
+        _lib_check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, w0, wave, data.data_ptr(), pitch,
+                                             stream.cuda_stream))
+        q = bq.ThresholdQuery([data[i, :wave] for i in range(n)], 64 * wave)
+        ms_all += _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), steps,
+                                  1 if w0 else args.warmup, stream)
+        q.close()
+    in_bytes_wave = n * wave * 8
+    per = statistics.mean(ms_all)
+    return _line("c5", in_bytes_wave / (per / 1e3) / 1e9, ms_all, in_bytes_wave + wave * 8, len(ms_all), args.warmup,
+                 {"workload": "C5 at 1 GPU: N=511, r=2^32 bits, p=0.5, T=256 (256 GiB) as 8 generate->compute "
+                              "waves of 2^23 words (32 GiB, = one GPU's shard at 8 GPUs); kernels timed only",
+                  "n_bitmaps": n, "r_bits": 64 * total, "t": t, "wave_words": wave},
+                 {"full_query_ms_at_1gpu": round(per * total / wave, 3)})
+
+
+def _lib_check(rc):
+    from paper_1402_4073_b200 import _lib
+    _lib.check(rc)
+
+
+def run_extra(args):
+    import torch
+
+    import paper_1402_4073_b200 as bq
+    from paper_1402_4073_b200 import _lib
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    fn = {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5}[args.workload]
+    with ClockSampler(physical_gpu_index(local)) as clocks:
+        line = fn(args, torch, bq, lib, dev, stream)
+    line["clocks"] = clocks.summary()
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c2",
+                    help="BASELINE config; c2 (the default) is the headline line")
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
@@ -392,6 +632,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload != "c2":
+        return run_extra(args)
     return run_ours(args)
 
 

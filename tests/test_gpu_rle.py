@@ -1,0 +1,180 @@
+"""Parity of the device RLE path (K3 directory + K4 tile decode-and-count) with
+the reference cdom algorithms and decoder.  Needs a B200."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, padded
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+RLE = load_golden("rle")
+CODEC = load_golden("codec")
+
+
+@pytest.fixture(scope="module")
+def bq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1402_4073_b200 as bq
+
+    bq._lib.load()
+    return bq
+
+
+def dev(arrs):
+    out = []
+    for a in arrs:
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        t = torch.from_numpy(a.view(np.int64)).cuda() if a.size else torch.zeros(1, dtype=torch.int64, device="cuda")
+        out.append(bq_stream(t, a.size))
+    return out
+
+
+def bq_stream(t, n):
+    import paper_1402_4073_b200 as bq
+
+    return bq.DeviceRleBitmap(t, 0, n)
+
+
+def host(t, nw):
+    return t[:nw].cpu().numpy().view(np.uint64)
+
+
+def popcount(words):
+    return int(np.unpackbits(np.ascontiguousarray(words, dtype=np.uint64).view(np.uint8)).sum())
+
+
+def markov(lib, seed, i, r, m1, m0):
+    cap = max(1024, (r // 64) * 2 + 16)
+    out = np.empty(cap, dtype=np.uint64)
+    n = ctypes.c_uint64(0)
+    assert lib.bq_gen_markov_rle(seed, i, r, m1, m0, out.ctypes.data, cap, ctypes.byref(n)) == 0
+    return out[: n.value].copy()
+
+
+@pytest.mark.parametrize("case", RLE, ids=lambda c: c.id)
+def test_cdom_golden(bq, case):
+    q = bq.RleQuery(dev(case.inputs), case.r)
+    if case.meta["kind"] == "cdom_threshold":
+        out, pc = q.threshold(case.meta["t"])
+    else:
+        out, pc = q.symmetric(case.meta["accept"])
+    nw = (case.r + 63) // 64
+    exp = padded(np.array(case.meta["uncompressed"], dtype=np.uint64), case.r)
+    assert np.array_equal(host(out, nw), exp)
+    assert int(pc.item()) == popcount(exp)
+
+
+@pytest.mark.parametrize("case", RLE[::2], ids=lambda c: c.id)
+def test_cdom_golden_dropin(bq, case):
+    """Reference-style RleBitmap in -> canonical RleBitmap out, word for word."""
+    ins = [bq.RleBitmap(a.tolist(), b) for a, b in zip(case.inputs, case.bits)]
+    if case.meta["kind"] == "cdom_threshold":
+        got = bq.cdom_threshold(ins, case.meta["t"])
+        assert bq.scan_count(ins, case.meta["t"]).words == case.out.tolist()  # RLE in -> RLE out
+    else:
+        got = bq.cdom_symmetric(ins, bq.SymmetricSpec(tuple(bool(x) for x in case.meta["accept"])))
+    assert isinstance(got, bq.RleBitmap)
+    assert got.words == case.out.tolist()
+    assert got.bit_length == case.r
+
+
+@pytest.mark.parametrize("case", CODEC, ids=lambda c: c.id)
+def test_device_decoder_codec(bq, case):
+    if case.meta["kind"] == "compress":
+        stream, expect = case.out, padded(case.inputs[0], case.r)
+    else:
+        stream, expect = case.inputs[0], padded(case.out, case.r)
+    rb = bq.RleBitmap(stream.tolist(), case.r)
+    if case.meta.get("status") == "format_error":
+        with pytest.raises(bq.FormatError):
+            bq.decompress(rb)
+        return
+    got = bq.decompress(rb)
+    assert isinstance(got, bq.UncompressedBitmap)
+    assert np.array_equal(padded(np.array(got.words, dtype=np.uint64), case.r), expect)
+
+
+@pytest.mark.parametrize("n,r,m1,m0", [(1, 64 * 5000, 40.0, 300.0), (7, 64 * 20000 + 3, 256.0, 12544.0),
+                                      (64, (1 << 20) + 17, 30.0, 90.0), (300, 1 << 21, 256.0, 12544.0),
+                                      (33, 64 * 4096 * 3, 5000.0, 5000.0), (16, 64 * 100, 3.0, 3.0)])
+def test_markov_vs_oracle_cdom(bq, n, r, m1, m0):
+    lib = bq._lib.load()
+    streams = [markov(lib, 77, i, r, m1, m0) for i in range(n)]
+    q = bq.RleQuery(dev(streams), r)
+    nw = (r + 63) // 64
+    for t in sorted({1, 2, 3, max(1, n // 10), max(1, n // 2), n}):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+    for acc in ([k % 2 == 1 for k in range(n + 1)], [k == 0 or 2 <= k <= 4 for k in range(n + 1)]):
+        out, pc = q.symmetric(acc)
+        exp = O.cdom_symmetric(streams, r, acc)
+        assert np.array_equal(host(out, nw), exp)
+        assert int(pc.item()) == popcount(exp)
+
+
+def test_ragged_and_degenerate_streams(bq):
+    """Empty streams, short streams (implicit tail), fill_run=0 markers, literal
+    all-0/all-1 words, dirty runs across tile boundaries, long one-fills."""
+    mk = lambda bit, run, dirty: bit | (run << 1) | (dirty << 33)  # noqa: E731
+    r = 64 * 4096 * 3 + 7
+    nw = (r + 63) // 64
+    rng = np.random.default_rng(3)
+    lits = [int(x) for x in rng.integers(1, 2**63, size=40)]
+    streams = [
+        np.array([], dtype=np.uint64),
+        np.array([mk(1, 4090, 10)] + lits[:10], dtype=np.uint64),          # dirty run across tile 0/1
+        np.array([mk(0, 0, 2), lits[10], lits[11], mk(1, 9000, 0)], dtype=np.uint64),
+        np.array([mk(1, 0, 3), 0, 2**64 - 1, lits[12], mk(0, 4093, 0), mk(1, 2, 5)] + lits[13:18],
+                 dtype=np.uint64),
+        np.array([mk(1, nw - 1, 0)], dtype=np.uint64),                     # ones to the last full word
+        np.array([mk(0, 4095, 1), lits[20], mk(0, 0, 0), mk(0, 0, 1), lits[21]], dtype=np.uint64),
+    ]
+    q = bq.RleQuery(dev(streams), r)
+    n = len(streams)
+    for t in range(1, n + 1):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        dec = [O.rle_decompress(s, r) for s in streams]
+        assert np.array_equal(exp, O.scan_count(dec, r, t))
+
+
+def test_c4_shape_scaled(bq):
+    """Config 4 generator (one-runs mean 256, zero-runs 12544, density 0.02) at
+    N=1024 and r=2^24 bits, T=50 (the config's T) and T=5,10,20 where the dirty
+    literal path is exercised, against the oracle's cdom sweep."""
+    lib = bq._lib.load()
+    n, r = 1024, 1 << 24
+    streams = [markov(lib, 1402, i, r, 256.0, 12544.0) for i in range(n)]
+    q = bq.RleQuery(dev(streams), r)
+    nw = r // 64
+    for t in (5, 10, 20, 50):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+
+
+def test_rle_errors(bq):
+    mk = lambda bit, run, dirty: bit | (run << 1) | (dirty << 33)  # noqa: E731
+    good = np.array([mk(0, 2, 0)], dtype=np.uint64)
+    with pytest.raises(bq.FormatError):
+        bq.RleQuery(dev([good, np.array([mk(0, 1, 3), 1, 2], dtype=np.uint64)]), 64 * 10)
+    with pytest.raises(bq.FormatError):
+        bq.RleQuery(dev([good, np.array([mk(0, 11, 0)], dtype=np.uint64)]), 64 * 10)
+    q = bq.RleQuery(dev([good, good]), 64 * 10)
+    with pytest.raises(bq.InputError):
+        q.threshold(3)
+    with pytest.raises(bq.InputError):
+        q.symmetric([True, False])
