@@ -46,8 +46,16 @@ constexpr int kRleTile = 4096;        // output words per K4 tile (and directory
 constexpr int kRleThreads = 256;
 constexpr int kSlotsPerBatch = 256;   // undecided words resolved per phase-C pass
 constexpr uint16_t kNoSlot = 0xFFFF;
-constexpr size_t kRleSmemBytes = (size_t)(kRleTile + 4) * 4 + (size_t)kSlotsPerBatch * 128 + (size_t)kRleTile * 4 +
-                                 (size_t)kSlotsPerBatch * 2;
+constexpr int kStageWords = 4096;       // words per cp.async stage buffer (two buffers)
+constexpr int kMaxStagedInputs = 4096;  // N up to this stages segments through shared memory
+constexpr int kMaxBatches = 64;
+constexpr size_t kCntBytes = (size_t)(kRleTile + 4) * 4;
+constexpr size_t kPhaseCBytes = (size_t)kSlotsPerBatch * 128 + (size_t)kRleTile * 4 + (size_t)kSlotsPerBatch * 2;
+constexpr size_t kRegionBytes = (2 * (size_t)kStageWords * 8 > kPhaseCBytes) ? 2 * (size_t)kStageWords * 8 : kPhaseCBytes;
+
+inline size_t rle_smem_bytes(bool staged, int n) {
+    return kCntBytes + kRegionBytes + (staged ? (((size_t)n + 1) * 4 + 15) / 16 * 16 : 0);
+}
 
 enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };
 
@@ -164,40 +172,177 @@ __device__ __forceinline__ void walk_tile(const RleCountArgs &a, int st, uint32_
     }
 }
 
-__global__ void __launch_bounds__(kRleThreads) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
-    // dynamic shared memory (kRleSmemBytes): see the carve-up below
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Exclusive prefix sum of arr[0..n) in place (arr[n] receives the total).
+__device__ void block_exclusive_scan(uint32_t *arr, int n, uint32_t *warp_sums) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + kRleThreads - 1) / kRleThreads;
+    const int lo = min(n, tid * per), hi = min(n, lo + per);
+    uint32_t sum = 0;
+    for (int k = lo; k < hi; ++k) sum += arr[k];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    uint32_t off = incl - sum;
+    for (int w = 0; w < warp; ++w) off += warp_sums[w];
+    for (int k = lo; k < hi; ++k) {
+        const uint32_t v = arr[k];
+        arr[k] = off;
+        off += v;
+    }
+    if (tid == kRleThreads - 1) arr[n] = off;
+    __syncthreads();
+}
+
+// Marker sweep of one stream over tile [ts, te) reading words from `src` (shared
+// memory or global), src[0] being the stream's marker at directory index e.x.
+template <typename Visit>
+__device__ __forceinline__ void walk_words(const uint64_t *src, uint64_t first, uint64_t L, uint64_t pos,
+                                           uint64_t ts, uint64_t te, Visit &&visit) {
+    uint64_t i = first;
+    while (i < L && pos < te) {
+        const uint64_t mk = src[i - first];
+        const uint64_t run = (mk >> 1) & 0xFFFFFFFFull;
+        const uint64_t dirty = mk >> 33;
+        const uint64_t fe = pos + run, de = fe + dirty;
+        if (de > ts) visit(pos, fe, (uint32_t)(mk & 1), fe, de);
+        pos = de;
+        i += 1 + dirty;
+    }
+}
+
+// STAGED: the tile's segment of every stream (from its directory entry to the
+// marker covering the next tile boundary) is copied to shared memory with
+// cp.async in batches of kStageWords words, double buffered, so the
+// pointer-chasing marker walk reads shared memory while the next batch streams
+// in from HBM at full width.  Without staging (N > kMaxStagedInputs) the walk
+// reads global memory directly.
+template <bool STAGED>
+__global__ void __launch_bounds__(kRleThreads, 2) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
     extern __shared__ __align__(16) uint8_t rle_smem[];
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);                         // [kRleTile + 4] packed (ones | dirty << 16)
-    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(cnt + kRleTile + 4);  // [kSlotsPerBatch][32]
-    uint16_t *slot_of = reinterpret_cast<uint16_t *>(bitcnt + kSlotsPerBatch);       // [kRleTile]
-    uint16_t *undecided = slot_of + kRleTile;                                         // [kRleTile]
-    uint16_t *slot_word = undecided + kRleTile;                                       // [kSlotsPerBatch]
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);  // [kRleTile + 4] packed (ones | dirty << 16)
+    uint8_t *region = rle_smem + kCntBytes;                  // phase A: stage buffers; phase C: bit counters
+    uint64_t *stage = reinterpret_cast<uint64_t *>(region);  // [2][kStageWords]
+    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);                   // [kSlotsPerBatch][32]
+    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + kSlotsPerBatch * 128);       // [kRleTile]
+    uint16_t *undecided = slot_of + kRleTile;                                                // [kRleTile]
+    uint16_t *slot_word = undecided + kRleTile;                                              // [kSlotsPerBatch]
+    uint32_t *seg_off = reinterpret_cast<uint32_t *>(rle_smem + kCntBytes + kRegionBytes);  // [n + 1] (STAGED)
     __shared__ uint32_t n_undecided;
     __shared__ uint32_t warp_sums[kRleThreads / 32];
+    __shared__ uint32_t bounds[kMaxBatches + 1];
+    __shared__ uint32_t n_batches;
 
     const uint32_t tile = blockIdx.x;
     const uint64_t ts = (uint64_t)tile * kRleTile;
     const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
     const int width = (int)(te - ts);
     const int tid = threadIdx.x;
+    const int n = a.n;
 
     for (int k = tid; k <= kRleTile; k += kRleThreads) cnt[k] = 0u;
     if (tid == 0) n_undecided = 0;
-    __syncthreads();
+
+    auto sweep = [&](uint64_t fs, uint64_t fe, uint32_t bit, uint64_t ds, uint64_t de) {
+        if (bit && fe > ts && fs < te) {
+            atomicAdd(&cnt[max(fs, ts) - ts], 1u);
+            atomicAdd(&cnt[min(fe, te) - ts], 0xFFFFFFFFu);
+        }
+        if (de > ds && de > ts && ds < te) {
+            atomicAdd(&cnt[max(ds, ts) - ts], 0x10000u);
+            atomicAdd(&cnt[min(de, te) - ts], 0xFFFF0000u);
+        }
+    };
 
     // ---- A: run sweep over markers only -> difference array ------------------
-    for (int st = tid; st < a.n; st += kRleThreads) {
-        walk_tile(a, st, tile, ts, te,
-                  [&](uint64_t fs, uint64_t fe, uint32_t bit, uint64_t ds, uint64_t de, uint64_t, const uint64_t *) {
-                      if (bit && fe > ts && fs < te) {
-                          atomicAdd(&cnt[max(fs, ts) - ts], 1u);
-                          atomicAdd(&cnt[min(fe, te) - ts], 0xFFFFFFFFu);
-                      }
-                      if (de > ds && de > ts && ds < te) {
-                          atomicAdd(&cnt[max(ds, ts) - ts], 0x10000u);
-                          atomicAdd(&cnt[min(de, te) - ts], 0xFFFF0000u);
-                      }
-                  });
+    if constexpr (!STAGED) {
+        __syncthreads();
+        for (int st = tid; st < n; st += kRleThreads) {
+            const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
+            const uint64_t *s = a.ptrs[st];
+            walk_words(s + e.x, e.x, a.lens[st], e.y, ts, te, sweep);
+        }
+    } else {
+        // segment length of every stream in this tile, then offsets
+        for (int st = tid; st < n; st += kRleThreads) {
+            const uint64_t L = a.lens[st];
+            const uint32_t first = a.dir[(size_t)st * a.ntiles + tile].x;
+            const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)st * a.ntiles + tile + 1].x : L;
+            const uint64_t end = min(next + 1, L);
+            seg_off[st] = (first < L) ? (uint32_t)(end - first) : 0u;
+        }
+        __syncthreads();
+        block_exclusive_scan(seg_off, n, warp_sums);
+        int s_done = 0;
+        while (s_done < n) {
+            if (tid == 0) {  // greedy batches of consecutive streams that fit one stage buffer
+                uint32_t nb = 0;
+                int s = s_done;
+                bounds[0] = (uint32_t)s;
+                while (s < n && nb < kMaxBatches) {
+                    int lo = s + 1, hi = n;  // largest s1 in [s+1, n] with seg_off[s1] - seg_off[s] <= kStageWords
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (seg_off[mid] - seg_off[s] <= (uint32_t)kStageWords) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    s = lo;
+                    bounds[++nb] = (uint32_t)s;
+                }
+                n_batches = nb;
+            }
+            __syncthreads();
+            const uint32_t nb = n_batches;
+            auto issue = [&](uint32_t k) {
+                const int s0 = (int)bounds[k], s1 = (int)bounds[k + 1];
+                if (seg_off[s1] - seg_off[s0] > (uint32_t)kStageWords) return;  // one oversize stream: walk from HBM
+                uint64_t *buf = stage + (size_t)(k & 1) * kStageWords;
+                const int lane = tid & 31;
+                for (int st = s0 + (tid >> 5); st < s1; st += kRleThreads / 32) {
+                    const uint32_t len = seg_off[st + 1] - seg_off[st];
+                    if (!len) continue;
+                    const uint64_t *src = a.ptrs[st] + a.dir[(size_t)st * a.ntiles + tile].x;
+                    uint64_t *dst = buf + (seg_off[st] - seg_off[s0]);
+                    for (uint32_t j = lane; j < len; j += 32) cp_async8(dst + j, src + j);
+                }
+            };
+            issue(0);
+            cp_async_commit();
+            for (uint32_t k = 0; k < nb; ++k) {
+                if (k + 1 < nb) {
+                    issue(k + 1);
+                    cp_async_commit();
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
+                }
+                __syncthreads();
+                const int s0 = (int)bounds[k], s1 = (int)bounds[k + 1];
+                const bool oversize = seg_off[s1] - seg_off[s0] > (uint32_t)kStageWords;
+                const uint64_t *buf = stage + (size_t)(k & 1) * kStageWords;
+                for (int st = s0 + tid; st < s1; st += kRleThreads) {
+                    const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
+                    const uint64_t *src = oversize ? a.ptrs[st] + e.x : buf + (seg_off[st] - seg_off[s0]);
+                    walk_words(src, e.x, a.lens[st], e.y, ts, te, sweep);
+                }
+                __syncthreads();
+            }
+            s_done = (int)bounds[nb];
+        }
     }
     __syncthreads();
 
@@ -444,13 +589,19 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.const_until = static_cast<const uint32_t *>(d_tab) + nbits_words;
     a.out = d_out;
     a.popcnt = d_popcnt;
-    static bool attr_set = false;
-    if (!attr_set) {
-        e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRleSmemBytes);
-        if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(rle_count_kernel)");
-        attr_set = true;
+    const bool staged = n <= kMaxStagedInputs;
+    const size_t smem = rle_smem_bytes(staged, n);
+    if (staged) {
+        e = cudaFuncSetAttribute(rle_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) rle_count_kernel<true><<<q->ntiles, kRleThreads, smem, s>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(rle_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) rle_count_kernel<false><<<q->ntiles, kRleThreads, smem, s>>>(a);
     }
-    rle_count_kernel<<<q->ntiles, kRleThreads, kRleSmemBytes, s>>>(a);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(d_tab, s);
+        return cuda_error(e, "cudaFuncSetAttribute(rle_count_kernel)");
+    }
     e = cudaGetLastError();
     cudaFreeAsync(d_tab, s);
     if (e != cudaSuccess) return cuda_error(e, "rle_count_kernel launch");
