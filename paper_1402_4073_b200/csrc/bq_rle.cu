@@ -33,6 +33,7 @@
 //   Output is uncompressed (BASELINE config 4), with a fused popcount.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -42,19 +43,24 @@
 
 namespace bq {
 
-constexpr int kRleTile = 4096;        // output words per K4 tile (and directory granularity)
+constexpr int kRleTile = 1024;        // output words per K4 tile (and directory granularity)
 constexpr int kRleThreads = 256;
 constexpr int kSlotsPerBatch = 256;   // undecided words resolved per phase-C pass
 constexpr uint16_t kNoSlot = 0xFFFF;
-constexpr int kStageWords = 4096;       // words per cp.async stage buffer (two buffers)
-constexpr int kMaxStagedInputs = 4096;  // N up to this stages segments through shared memory
-constexpr int kMaxBatches = 64;
+constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
+constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
+                                        // C4 needs ~613 words per 32 streams on average, 760 at p99
+constexpr int kMetaMax = 2048;          // N up to this caches the tile's directory entries in smem
 constexpr size_t kCntBytes = (size_t)(kRleTile + 4) * 4;
-constexpr size_t kPhaseCBytes = (size_t)kSlotsPerBatch * 128 + (size_t)kRleTile * 4 + (size_t)kSlotsPerBatch * 2;
-constexpr size_t kRegionBytes = (2 * (size_t)kStageWords * 8 > kPhaseCBytes) ? 2 * (size_t)kStageWords * 8 : kPhaseCBytes;
+constexpr int kSlotsUnstaged = 64;      // phase-C batch when nothing is staged (keeps L1 large)
+constexpr size_t phase_c_bytes(int slots) { return (size_t)slots * 128 + (size_t)kRleTile * 4 + (size_t)slots * 2; }
+constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * 2 * kPoolWords * 8;
+constexpr size_t kRegionBytes = kPoolBytes > phase_c_bytes(kSlotsPerBatch) ? kPoolBytes : phase_c_bytes(kSlotsPerBatch);
+
+inline size_t rle_meta_bytes(int n) { return n <= kMetaMax ? (size_t)n * 8 + ((size_t)n * 2 + 15) / 16 * 16 : 0; }
 
 inline size_t rle_smem_bytes(bool staged, int n) {
-    return kCntBytes + kRegionBytes + (staged ? (((size_t)n + 1) * 4 + 15) / 16 * 16 : 0);
+    return kCntBytes + (staged ? kRegionBytes + rle_meta_bytes(n) : phase_c_bytes(kSlotsUnstaged));
 }
 
 enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };
@@ -172,182 +178,221 @@ __device__ __forceinline__ void walk_tile(const RleCountArgs &a, int st, uint32_
     }
 }
 
-__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Exclusive prefix sum of arr[0..n) in place (arr[n] receives the total).
-__device__ void block_exclusive_scan(uint32_t *arr, int n, uint32_t *warp_sums) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (n + kRleThreads - 1) / kRleThreads;
-    const int lo = min(n, tid * per), hi = min(n, lo + per);
-    uint32_t sum = 0;
-    for (int k = lo; k < hi; ++k) sum += arr[k];
-    uint32_t incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+// Marker sweep of one stream over a tile of W words in 32-bit tile-relative
+// coordinates.  src[0] is the marker named by the stream's directory entry
+// (its fill run starts at word `pos`, at or before the tile); lim = stream
+// words available from there.  Each marker adds at most three entries to the
+// packed difference array: +1 at a one-fill's start, (-1 | +dirty) where the
+// fill ends and the literals begin, -dirty where the literals end.
+template <bool GLOBAL>
+__device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, uint32_t pos, uint64_t ts, int W,
+                                             uint32_t *cnt) {
+    auto load = [src](uint32_t k) { return GLOBAL ? __ldg(src + k) : src[k]; };
+    if (lim == 0) return;
+    const uint32_t Wu = (uint32_t)W;
+    // first marker: its fill starts at or before the tile (64-bit positions)
+    uint64_t mk = load(0);
+    uint32_t dirty = (uint32_t)(mk >> 33);
+    {
+        const int64_t fs64 = (int64_t)pos - (int64_t)ts;
+        const int64_t fe64 = fs64 + (int64_t)(uint32_t)(mk >> 1);
+        const int64_t de64 = fe64 + dirty;
+        auto cl = [W](int64_t v) { return (uint32_t)(v < 0 ? 0 : (v > W ? W : v)); };
+        const uint32_t fs = cl(fs64), fe = cl(fe64), de = cl(de64);
+        if ((mk & 1) && fe > fs) {
+            atomicAdd(&cnt[fs], 1u);
+            atomicAdd(&cnt[fe], 0xFFFFFFFFu);
+        }
+        if (de > fe) {
+            atomicAdd(&cnt[fe], 0x10000u);
+            atomicAdd(&cnt[de], 0xFFFF0000u);
+        }
+        if (de64 >= W) return;
+        pos = (uint32_t)de64;  // reused as the tile-relative start of the next marker
     }
-    if (lane == 31) warp_sums[warp] = incl;
-    __syncthreads();
-    uint32_t off = incl - sum;
-    for (int w = 0; w < warp; ++w) off += warp_sums[w];
-    for (int k = lo; k < hi; ++k) {
-        const uint32_t v = arr[k];
-        arr[k] = off;
-        off += v;
-    }
-    if (tid == kRleThreads - 1) arr[n] = off;
-    __syncthreads();
-}
-
-// Marker sweep of one stream over tile [ts, te) reading words from `src` (shared
-// memory or global), src[0] being the stream's marker at directory index e.x.
-template <typename Visit>
-__device__ __forceinline__ void walk_words(const uint64_t *src, uint64_t first, uint64_t L, uint64_t pos,
-                                           uint64_t ts, uint64_t te, Visit &&visit) {
-    uint64_t i = first;
-    while (i < L && pos < te) {
-        const uint64_t mk = src[i - first];
-        const uint64_t run = (mk >> 1) & 0xFFFFFFFFull;
-        const uint64_t dirty = mk >> 33;
-        const uint64_t fe = pos + run, de = fe + dirty;
-        if (de > ts) visit(pos, fe, (uint32_t)(mk & 1), fe, de);
-        pos = de;
+    uint32_t rel = pos;
+    uint32_t i = 1 + dirty;
+    while (i < lim) {
+        mk = load(i);
+        dirty = (uint32_t)(mk >> 33);
+        const uint32_t run = min((uint32_t)(mk >> 1), Wu);
+        const uint32_t ones = (uint32_t)(mk & 1) & (run != 0u);
+        const uint32_t fe_raw = rel + run;           // <= 2W
+        const uint32_t de_raw = fe_raw + dirty;      // < 2^32: dirty < 2^31
+        const uint32_t fe = min(fe_raw, Wu), de = min(de_raw, Wu);
+        const bool lit = (dirty != 0u) & (fe < Wu);
+        if (ones) atomicAdd(&cnt[rel], 1u);
+        const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
+        if (at_fe) atomicAdd(&cnt[fe], at_fe);
+        if (lit) atomicAdd(&cnt[de], 0xFFFF0000u);
+        if (de_raw >= Wu) break;
+        rel = de_raw;
         i += 1 + dirty;
     }
 }
 
-// STAGED: the tile's segment of every stream (from its directory entry to the
-// marker covering the next tile boundary) is copied to shared memory with
-// cp.async in batches of kStageWords words, double buffered, so the
-// pointer-chasing marker walk reads shared memory while the next batch streams
-// in from HBM at full width.  Without staging (N > kMaxStagedInputs) the walk
-// reads global memory directly.
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+// Phase A strategies.
+//  STAGED (default): warp-private, double-buffered staging.  Lane l of warp w
+//    owns stream k*NT + 32w + l of batch k.  It computes its stream's segment for
+//    this tile (directory entry -> marker covering the next tile boundary,
+//    widened to 16-byte alignment), claims room in the warp's pool with a warp
+//    prefix sum, and copies the segment with cp.async.cg while the previous
+//    batch is being walked.  Each lane waits only for its own copies, so the
+//    warps never meet at a CTA barrier in phase A; __syncwarp guards pool reuse.
+//    A segment that does not fit the pool is walked straight from HBM.
+//  !STAGED: every lane walks its streams directly from global memory (kept for
+//    A/B measurement, BQ_RLE_STAGED=0).
 template <bool STAGED>
-__global__ void __launch_bounds__(kRleThreads, 2) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
+__global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED ? 3 : 6)
+    rle_count_kernel(const __grid_constant__ RleCountArgs a) {
+    constexpr int NT = STAGED ? kStagedThreads : kRleThreads;
+    constexpr int kSlots = STAGED ? kSlotsPerBatch : kSlotsUnstaged;
     extern __shared__ __align__(16) uint8_t rle_smem[];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);  // [kRleTile + 4] packed (ones | dirty << 16)
-    uint8_t *region = rle_smem + kCntBytes;                  // phase A: stage buffers; phase C: bit counters
-    uint64_t *stage = reinterpret_cast<uint64_t *>(region);  // [2][kStageWords]
-    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);                   // [kSlotsPerBatch][32]
-    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + kSlotsPerBatch * 128);       // [kRleTile]
-    uint16_t *undecided = slot_of + kRleTile;                                                // [kRleTile]
-    uint16_t *slot_word = undecided + kRleTile;                                              // [kSlotsPerBatch]
-    uint32_t *seg_off = reinterpret_cast<uint32_t *>(rle_smem + kCntBytes + kRegionBytes);  // [n + 1] (STAGED)
+    uint8_t *region = rle_smem + kCntBytes;                  // phase A: warp pools; phase C: bit counters
+    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);       // [kSlots][32]
+    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + kSlots * 128);   // [kRleTile]
+    uint16_t *undecided = slot_of + kRleTile;                                    // [kRleTile]
+    uint16_t *slot_word = undecided + kRleTile;                                  // [kSlots]
     __shared__ uint32_t n_undecided;
-    __shared__ uint32_t warp_sums[kRleThreads / 32];
-    __shared__ uint32_t bounds[kMaxBatches + 1];
-    __shared__ uint32_t n_batches;
+    __shared__ uint32_t warp_sums[NT / 32];
 
     const uint32_t tile = blockIdx.x;
     const uint64_t ts = (uint64_t)tile * kRleTile;
     const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
     const int width = (int)(te - ts);
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const int n = a.n;
 
-    for (int k = tid; k <= kRleTile; k += kRleThreads) cnt[k] = 0u;
+    for (int k = tid; k <= kRleTile; k += NT) cnt[k] = 0u;
     if (tid == 0) n_undecided = 0;
-
-    auto sweep = [&](uint64_t fs, uint64_t fe, uint32_t bit, uint64_t ds, uint64_t de) {
-        if (bit && fe > ts && fs < te) {
-            atomicAdd(&cnt[max(fs, ts) - ts], 1u);
-            atomicAdd(&cnt[min(fe, te) - ts], 0xFFFFFFFFu);
-        }
-        if (de > ds && de > ts && ds < te) {
-            atomicAdd(&cnt[max(ds, ts) - ts], 0x10000u);
-            atomicAdd(&cnt[min(de, te) - ts], 0xFFFF0000u);
-        }
-    };
+    __syncthreads();
 
     // ---- A: run sweep over markers only -> difference array ------------------
     if constexpr (!STAGED) {
-        __syncthreads();
-        for (int st = tid; st < n; st += kRleThreads) {
-            const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
-            const uint64_t *s = a.ptrs[st];
-            walk_words(s + e.x, e.x, a.lens[st], e.y, ts, te, sweep);
-        }
-    } else {
-        // segment length of every stream in this tile, then offsets
-        for (int st = tid; st < n; st += kRleThreads) {
+        // high occupancy, no staging: the next stream's segment is prefetched into
+        // L2 while the current one is walked, so marker loads are L2 hits and
+        // thousands of independent chains per SM hide their latency.
+        auto prefetch = [&](int st) {
             const uint64_t L = a.lens[st];
             const uint32_t first = a.dir[(size_t)st * a.ntiles + tile].x;
+            if (first >= L) return;
             const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)st * a.ntiles + tile + 1].x : L;
-            const uint64_t end = min(next + 1, L);
-            seg_off[st] = (first < L) ? (uint32_t)(end - first) : 0u;
+            const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + first) & ~(uintptr_t)127;
+            const uintptr_t p1 = reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L));
+            for (uintptr_t p = p0; p < p1; p += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+        };
+        if (tid < n) prefetch(tid);
+        for (int st = tid; st < n; st += NT) {
+            if (st + NT < n) prefetch(st + NT);
+            const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
+            const uint64_t L = a.lens[st];
+            if (e.x < L) sweep_stream<true>(a.ptrs[st] + e.x, (uint32_t)(L - e.x), e.y, ts, width, cnt);
         }
-        __syncthreads();
-        block_exclusive_scan(seg_off, n, warp_sums);
-        int s_done = 0;
-        while (s_done < n) {
-            if (tid == 0) {  // greedy batches of consecutive streams that fit one stage buffer
-                uint32_t nb = 0;
-                int s = s_done;
-                bounds[0] = (uint32_t)s;
-                while (s < n && nb < kMaxBatches) {
-                    int lo = s + 1, hi = n;  // largest s1 in [s+1, n] with seg_off[s1] - seg_off[s] <= kStageWords
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (seg_off[mid] - seg_off[s] <= (uint32_t)kStageWords) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    s = lo;
-                    bounds[++nb] = (uint32_t)s;
-                }
-                n_batches = nb;
+    } else {
+        // the tile's directory entries and aligned segment lengths, loaded once
+        // with full memory-level parallelism (one latency per tile, not per batch)
+        const bool use_meta = n <= kMetaMax;
+        uint2 *meta = reinterpret_cast<uint2 *>(region + kRegionBytes);              // [n]
+        uint16_t *seglen = reinterpret_cast<uint16_t *>(meta + (use_meta ? n : 0));   // [n]
+        auto segment = [&](int st, uint2 &e, uint32_t &len) {
+            const uint64_t L = a.lens[st];
+            e = a.dir[(size_t)st * a.ntiles + tile];
+            len = 0;
+            if (e.x < L) {
+                const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)st * a.ntiles + tile + 1].x : L;
+                const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + e.x) & ~(uintptr_t)15;
+                const uintptr_t b1 = (reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L)) + 15) & ~(uintptr_t)15;
+                len = (uint32_t)((b1 - b0) / 8);
+            }
+        };
+        if (use_meta) {
+            for (int st = tid; st < n; st += NT) {
+                uint2 e;
+                uint32_t len;
+                segment(st, e, len);
+                meta[st] = e;
+                seglen[st] = (uint16_t)min(len, 65535u);
             }
             __syncthreads();
-            const uint32_t nb = n_batches;
-            auto issue = [&](uint32_t k) {
-                const int s0 = (int)bounds[k], s1 = (int)bounds[k + 1];
-                if (seg_off[s1] - seg_off[s0] > (uint32_t)kStageWords) return;  // one oversize stream: walk from HBM
-                uint64_t *buf = stage + (size_t)(k & 1) * kStageWords;
-                const int lane = tid & 31;
-                for (int st = s0 + (tid >> 5); st < s1; st += kRleThreads / 32) {
-                    const uint32_t len = seg_off[st + 1] - seg_off[st];
-                    if (!len) continue;
-                    const uint64_t *src = a.ptrs[st] + a.dir[(size_t)st * a.ntiles + tile].x;
-                    uint64_t *dst = buf + (seg_off[st] - seg_off[s0]);
-                    for (uint32_t j = lane; j < len; j += 32) cp_async8(dst + j, src + j);
-                }
-            };
-            issue(0);
-            cp_async_commit();
-            for (uint32_t k = 0; k < nb; ++k) {
-                if (k + 1 < nb) {
-                    issue(k + 1);
-                    cp_async_commit();
-                    cp_async_wait<1>();
-                } else {
-                    cp_async_wait<0>();
-                }
-                __syncthreads();
-                const int s0 = (int)bounds[k], s1 = (int)bounds[k + 1];
-                const bool oversize = seg_off[s1] - seg_off[s0] > (uint32_t)kStageWords;
-                const uint64_t *buf = stage + (size_t)(k & 1) * kStageWords;
-                for (int st = s0 + tid; st < s1; st += kRleThreads) {
-                    const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
-                    const uint64_t *src = oversize ? a.ptrs[st] + e.x : buf + (seg_off[st] - seg_off[s0]);
-                    walk_words(src, e.x, a.lens[st], e.y, ts, te, sweep);
-                }
-                __syncthreads();
-            }
-            s_done = (int)bounds[nb];
         }
+        uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * 2 * kPoolWords;
+        struct Seg {
+            const uint64_t *g;  // global address of the directory marker
+            uint32_t lim, pos, off;
+            bool staged;
+        };
+        auto plan = [&](int st, uint64_t *buf, Seg &sg) {
+            sg.lim = 0;
+            sg.staged = false;
+            uint32_t len = 0;
+            uintptr_t b0 = 0;
+            if (st < n) {
+                uint2 e;
+                if (use_meta) {
+                    e = meta[st];
+                    len = seglen[st];
+                } else {
+                    segment(st, e, len);
+                }
+                if (len) {
+                    sg.g = a.ptrs[st] + e.x;
+                    sg.lim = (uint32_t)(a.lens[st] - e.x);
+                    sg.pos = e.y;
+                    b0 = reinterpret_cast<uintptr_t>(sg.g) & ~(uintptr_t)15;
+                }
+            }
+            uint32_t incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (len && incl <= (uint32_t)kPoolWords) {
+                const uint32_t off = incl - len;
+                sg.staged = true;
+                sg.off = off + (uint32_t)((reinterpret_cast<uintptr_t>(sg.g) >> 3) & 1);
+                const uint64_t *gs = reinterpret_cast<const uint64_t *>(b0);
+                for (uint32_t j = 0; j < len; j += 2) cp_async16(buf + off + j, gs + j);
+            }
+        };
+        const int nk = (n + NT - 1) / NT;
+        Seg cur, nxt;
+        nxt.lim = 0;
+        nxt.staged = false;
+        plan(warp * 32 + lane, pool, cur);
+        cp_async_commit();
+        for (int k = 0; k < nk; ++k) {
+            if (k + 1 < nk) plan((k + 1) * NT + warp * 32 + lane, pool + (size_t)((k + 1) & 1) * kPoolWords, nxt);
+            cp_async_commit();
+            cp_async_wait<1>();  // this lane's copies for batch k have landed
+            if (cur.lim) {
+                if (cur.staged)
+                    sweep_stream<false>(pool + (size_t)(k & 1) * kPoolWords + cur.off, cur.lim, cur.pos, ts, width, cnt);
+                else
+                    sweep_stream<true>(cur.g, cur.lim, cur.pos, ts, width, cnt);
+            }
+            __syncwarp();  // batch k's pool half may be refilled for batch k + 2
+            cur = nxt;
+        }
+        cp_async_wait<0>();
     }
     __syncthreads();
 
-    // ---- inclusive prefix scan of cnt[0..kRleTile) (16 words per thread) ------
-    constexpr int kPer = kRleTile / kRleThreads;
+    // ---- inclusive prefix scan of cnt[0..kRleTile) (kPer words per thread) -----
+    constexpr int kPer = kRleTile / NT;
     uint32_t local[kPer];
     uint32_t run_sum = 0;
 #pragma unroll
@@ -356,7 +401,6 @@ __global__ void __launch_bounds__(kRleThreads, 2) rle_count_kernel(const __grid_
         local[k] = run_sum;
     }
     uint32_t incl = run_sum;
-    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -369,12 +413,12 @@ __global__ void __launch_bounds__(kRleThreads, 2) rle_count_kernel(const __grid_
     const uint32_t excl = warp_off + incl - run_sum;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) cnt[tid * kPer + k] = local[k] + excl;
-    for (int k = tid; k < kRleTile; k += kRleThreads) slot_of[k] = kNoSlot;
+    for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
     __syncthreads();
 
     // ---- B: decide from (k, d) ----------------------------------------------
     unsigned long long pc = 0;
-    for (int k = tid; k < width; k += kRleThreads) {
+    for (int k = tid; k < width; k += NT) {
         const uint32_t c = cnt[k];
         const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
         if (ones + dirty <= __ldg(a.const_until + ones)) {
@@ -390,16 +434,16 @@ __global__ void __launch_bounds__(kRleThreads, 2) rle_count_kernel(const __grid_
     const uint32_t nu = n_undecided;
 
     // ---- C: read dirty literals only where the fills leave the outcome open ----
-    for (uint32_t base = 0; base < nu; base += kSlotsPerBatch) {
-        const uint32_t nb = min((uint32_t)kSlotsPerBatch, nu - base);
-        for (uint32_t u = tid; u < nb; u += kRleThreads) {
+    for (uint32_t base = 0; base < nu; base += kSlots) {
+        const uint32_t nb = min((uint32_t)kSlots, nu - base);
+        for (uint32_t u = tid; u < nb; u += NT) {
             const uint16_t wk = undecided[base + u];
             slot_word[u] = wk;
             slot_of[wk] = (uint16_t)u;
         }
-        for (int k = tid; k < kSlotsPerBatch * 32; k += kRleThreads) (&bitcnt[0][0])[k] = 0u;
+        for (int k = tid; k < kSlots * 32; k += NT) (&bitcnt[0][0])[k] = 0u;
         __syncthreads();
-        for (int st = tid; st < a.n; st += kRleThreads) {
+        for (int st = tid; st < a.n; st += NT) {
             walk_tile(a, st, tile, ts, te,
                       [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit, const uint64_t *s) {
                           const uint64_t lo = max(ds, ts), hi = min(de, te);
@@ -416,7 +460,7 @@ __global__ void __launch_bounds__(kRleThreads, 2) rle_count_kernel(const __grid_
                       });
         }
         __syncthreads();
-        for (uint32_t u = tid; u < nb; u += kRleThreads) {
+        for (uint32_t u = tid; u < nb; u += NT) {
             const uint16_t wk = slot_word[u];
             const uint32_t ones = cnt[wk] & 0xFFFFu;
             uint64_t w = 0;
@@ -589,11 +633,13 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.const_until = static_cast<const uint32_t *>(d_tab) + nbits_words;
     a.out = d_out;
     a.popcnt = d_popcnt;
-    const bool staged = n <= kMaxStagedInputs;
+    // BQ_RLE_STAGED=0 selects the unstaged phase A (A/B measurement)
+    static const char *env = getenv("BQ_RLE_STAGED");
+    const bool staged = !(env && env[0] == '0');
     const size_t smem = rle_smem_bytes(staged, n);
     if (staged) {
         e = cudaFuncSetAttribute(rle_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) rle_count_kernel<true><<<q->ntiles, kRleThreads, smem, s>>>(a);
+        if (e == cudaSuccess) rle_count_kernel<true><<<q->ntiles, kStagedThreads, smem, s>>>(a);
     } else {
         e = cudaFuncSetAttribute(rle_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) rle_count_kernel<false><<<q->ntiles, kRleThreads, smem, s>>>(a);

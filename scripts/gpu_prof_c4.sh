@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python bench.py --workload c4 --steps 3 --warmup 3 > gpurun_out/bench_c4_small.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:rle_count -s 3 -c 1 -o gpurun_out/prof_c4 python bench.py --workload c4 --steps 3 --warmup 3 > gpurun_out/ncu_c4.log 2>&1
+echo done
