@@ -51,7 +51,7 @@ constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a priva
 constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
 constexpr int kMetaMax = 2048;          // N up to this caches the tile's directory entries in smem
-constexpr size_t kCntBytes = (size_t)(kRleTile + 4) * 4;
+constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
 constexpr int kSlotsUnstaged = 64;      // phase-C batch when nothing is staged (keeps L1 large)
 constexpr size_t phase_c_bytes(int slots) { return (size_t)slots * 128 + (size_t)kRleTile * 4 + (size_t)slots * 2; }
 constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * 2 * kPoolWords * 8;
@@ -72,7 +72,7 @@ struct RleDirArgs {
     uint64_t total_words;  // ceil(r/64)
     uint64_t tail_mask;    // valid bits of the last word when r % 64 != 0, else 0
     uint32_t ntiles;
-    uint2 *dir;            // [n][ntiles]: (marker index, run start word)
+    uint2 *dir;            // [ntiles][n]: (marker index, run start word); tile-major so a K4 CTA reads one row
     int *err;              // first error code
     unsigned long long *err_stream;
 };
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
     if (stream >= a.n) return;
     const uint64_t *s = a.ptrs[stream];
     const uint64_t L = a.lens[stream];
-    uint2 *dir = a.dir + (size_t)stream * a.ntiles;
+    uint2 *dir = a.dir + stream;  // stride n between tiles
     uint64_t i = 0;     // stream index of the next marker
     uint64_t pos = 0;   // word position where that marker's fill run starts
     while (i < L) {
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
             // record every tile boundary b with start <= b < end
             uint64_t b = (start + kRleTile - 1) / kRleTile * kRleTile;
             for (; b < end && b < a.total_words; b += kRleTile)
-                dir[b / kRleTile] = make_uint2((uint32_t)idx, (uint32_t)start);
+                dir[(b / kRleTile) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
         }
         const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
         pos += total;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
     }
     // tiles past the encoded coverage: stream exhausted, implicit zero tail
     uint64_t b = (pos + kRleTile - 1) / kRleTile * kRleTile;
-    for (uint64_t t = b / kRleTile + lane; t < a.ntiles; t += 32) dir[t] = make_uint2((uint32_t)L, (uint32_t)pos);
+    for (uint64_t t = b / kRleTile + lane; t < a.ntiles; t += 32) dir[t * a.n] = make_uint2((uint32_t)L, (uint32_t)pos);
 }
 
 struct RleCountArgs {
@@ -153,6 +153,7 @@ struct RleCountArgs {
     const uint32_t *const_until;  // [n + 1]: largest j >= k with accept[k..j] constant
     uint64_t *out;
     unsigned long long *popcnt;
+    int debug;  // experiment knob (BQ_RLE_DEBUG): 1 = skip marker walks, 2 = also skip copies
 };
 
 __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { return (bits[c >> 5] >> (c & 31)) & 1u; }
@@ -165,7 +166,7 @@ __device__ __forceinline__ void walk_tile(const RleCountArgs &a, int st, uint32_
                                           Visit &&visit) {
     const uint64_t *s = a.ptrs[st];
     const uint64_t L = a.lens[st];
-    const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
+    const uint2 e = a.dir[(size_t)tile * a.n + st];
     uint64_t i = e.x, pos = e.y;
     while (i < L && pos < te) {
         const uint64_t mk = __ldg(s + i);
@@ -218,6 +219,7 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
     }
     uint32_t rel = pos;
     uint32_t i = 1 + dirty;
+    const uint32_t dummy = Wu + 1 + (threadIdx.x & 31);
     while (i < lim) {
         mk = load(i);
         dirty = (uint32_t)(mk >> 33);
@@ -227,10 +229,11 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
         const uint32_t de_raw = fe_raw + dirty;      // < 2^32: dirty < 2^31
         const uint32_t fe = min(fe_raw, Wu), de = min(de_raw, Wu);
         const bool lit = (dirty != 0u) & (fe < Wu);
-        if (ones) atomicAdd(&cnt[rel], 1u);
+        // branchless: an empty contribution goes to this lane's dummy slot past the tile
         const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
-        if (at_fe) atomicAdd(&cnt[fe], at_fe);
-        if (lit) atomicAdd(&cnt[de], 0xFFFF0000u);
+        atomicAdd(&cnt[ones ? rel : dummy], 1u);
+        atomicAdd(&cnt[at_fe ? fe : dummy], at_fe);
+        atomicAdd(&cnt[lit ? de : dummy], 0xFFFF0000u);
         if (de_raw >= Wu) break;
         rel = de_raw;
         i += 1 + dirty;
@@ -287,9 +290,9 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
         // thousands of independent chains per SM hide their latency.
         auto prefetch = [&](int st) {
             const uint64_t L = a.lens[st];
-            const uint32_t first = a.dir[(size_t)st * a.ntiles + tile].x;
+            const uint32_t first = a.dir[(size_t)tile * a.n + st].x;
             if (first >= L) return;
-            const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)st * a.ntiles + tile + 1].x : L;
+            const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : L;
             const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + first) & ~(uintptr_t)127;
             const uintptr_t p1 = reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L));
             for (uintptr_t p = p0; p < p1; p += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
         if (tid < n) prefetch(tid);
         for (int st = tid; st < n; st += NT) {
             if (st + NT < n) prefetch(st + NT);
-            const uint2 e = a.dir[(size_t)st * a.ntiles + tile];
+            const uint2 e = a.dir[(size_t)tile * a.n + st];
             const uint64_t L = a.lens[st];
             if (e.x < L) sweep_stream<true>(a.ptrs[st] + e.x, (uint32_t)(L - e.x), e.y, ts, width, cnt);
         }
@@ -309,32 +312,67 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
         uint16_t *seglen = reinterpret_cast<uint16_t *>(meta + (use_meta ? n : 0));   // [n]
         auto segment = [&](int st, uint2 &e, uint32_t &len) {
             const uint64_t L = a.lens[st];
-            e = a.dir[(size_t)st * a.ntiles + tile];
+            e = a.dir[(size_t)tile * a.n + st];
             len = 0;
             if (e.x < L) {
-                const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)st * a.ntiles + tile + 1].x : L;
+                const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : L;
                 const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + e.x) & ~(uintptr_t)15;
                 const uintptr_t b1 = (reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L)) + 15) & ~(uintptr_t)15;
                 len = (uint32_t)((b1 - b0) / 8);
             }
         };
         if (use_meta) {
-            for (int st = tid; st < n; st += NT) {
-                uint2 e;
-                uint32_t len;
-                segment(st, e, len);
-                meta[st] = e;
-                seglen[st] = (uint16_t)min(len, 65535u);
+            constexpr int U = 4;  // loads of U streams in flight per thread
+            for (int base = 0; base < n; base += NT * U) {
+                uint64_t L[U];
+                uint2 e[U];
+                uint32_t nx[U];
+                const uint64_t *p[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int st = base + u * NT + tid;
+                    if (st < n) {
+                        L[u] = a.lens[st];
+                        e[u] = a.dir[(size_t)tile * a.n + st];
+                        nx[u] = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : 0xFFFFFFFFu;
+                        p[u] = a.ptrs[st];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int st = base + u * NT + tid;
+                    if (st < n) {
+                        uint32_t len = 0;
+                        if (e[u].x < L[u]) {
+                            const uint64_t next = nx[u] == 0xFFFFFFFFu ? L[u] : nx[u];
+                            const uintptr_t b0 = reinterpret_cast<uintptr_t>(p[u] + e[u].x) & ~(uintptr_t)15;
+                            const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p[u] + min(next + 1, L[u])) + 15) & ~(uintptr_t)15;
+                            len = (uint32_t)((b1 - b0) / 8);
+                        }
+                        meta[st] = e[u];
+                        seglen[st] = (uint16_t)min(len, 65535u);
+                    }
+                }
             }
             __syncthreads();
         }
         uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * 2 * kPoolWords;
+        // one mbarrier per pool half; 32 arrivals (one per lane) + the TMA byte count complete a phase
+        uint64_t *bars = reinterpret_cast<uint64_t *>(cnt + kRleTile + 36) + warp * 2;
+        const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar0) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar0 + 8) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncwarp();
         struct Seg {
             const uint64_t *g;  // global address of the directory marker
             uint32_t lim, pos, off;
             bool staged;
         };
-        auto plan = [&](int st, uint64_t *buf, Seg &sg) {
+        // Stage batch k's segment of this lane's stream: one TMA bulk copy per lane.
+        auto plan = [&](int st, int k, Seg &sg) {
             sg.lim = 0;
             sg.staged = false;
             uint32_t len = 0;
@@ -360,25 +398,50 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
                 const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
-            if (len && incl <= (uint32_t)kPoolWords) {
-                const uint32_t off = incl - len;
+            const uint32_t off = incl - len;
+            const uint32_t bar = bar0 + 8 * (k & 1);
+            if (len && incl <= (uint32_t)kPoolWords && a.debug < 2) {
                 sg.staged = true;
                 sg.off = off + (uint32_t)((reinterpret_cast<uintptr_t>(sg.g) >> 3) & 1);
-                const uint64_t *gs = reinterpret_cast<const uint64_t *>(b0);
-                for (uint32_t j = 0; j < len; j += 2) cp_async16(buf + off + j, gs + j);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pool + (size_t)(k & 1) * kPoolWords + off);
+                const uint32_t bytes = len * 8;
+                asm volatile(
+                    "{\n\t.reg .b64 st;\n\t"
+                    "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
+                    "r"(bytes)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                    "l"(b0), "r"(bytes), "r"(bar)
+                    : "memory");
+            } else {
+                asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
+            }
+        };
+        auto wait_batch = [&](int k) {
+            const uint32_t bar = bar0 + 8 * (k & 1);
+            const uint32_t parity = (uint32_t)((k >> 1) & 1);
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(done)
+                    : "r"(bar), "r"(parity)
+                    : "memory");
             }
         };
         const int nk = (n + NT - 1) / NT;
         Seg cur, nxt;
         nxt.lim = 0;
         nxt.staged = false;
-        plan(warp * 32 + lane, pool, cur);
-        cp_async_commit();
+        plan(warp * 32 + lane, 0, cur);
         for (int k = 0; k < nk; ++k) {
-            if (k + 1 < nk) plan((k + 1) * NT + warp * 32 + lane, pool + (size_t)((k + 1) & 1) * kPoolWords, nxt);
-            cp_async_commit();
-            cp_async_wait<1>();  // this lane's copies for batch k have landed
-            if (cur.lim) {
+            if (k + 1 < nk) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
+                plan((k + 1) * NT + warp * 32 + lane, k + 1, nxt);
+            }
+            wait_batch(k);  // every lane's bulk copy for batch k has landed
+            if (cur.lim && !a.debug) {
                 if (cur.staged)
                     sweep_stream<false>(pool + (size_t)(k & 1) * kPoolWords + cur.off, cur.lim, cur.pos, ts, width, cnt);
                 else
@@ -387,7 +450,6 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             __syncwarp();  // batch k's pool half may be refilled for batch k + 2
             cur = nxt;
         }
-        cp_async_wait<0>();
     }
     __syncthreads();
 
@@ -637,6 +699,8 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     static const char *env = getenv("BQ_RLE_STAGED");
     const bool staged = !(env && env[0] == '0');
     const size_t smem = rle_smem_bytes(staged, n);
+    static const char *dbg = getenv("BQ_RLE_DEBUG");
+    a.debug = dbg ? atoi(dbg) : 0;
     if (staged) {
         e = cudaFuncSetAttribute(rle_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) rle_count_kernel<true><<<q->ntiles, kStagedThreads, smem, s>>>(a);
