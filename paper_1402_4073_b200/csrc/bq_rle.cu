@@ -50,17 +50,15 @@ constexpr uint16_t kNoSlot = 0xFFFF;
 constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
 constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
-constexpr int kMetaMax = 2048;          // N up to this caches the tile's directory entries in smem
 constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
 constexpr int kSlotsUnstaged = 64;      // phase-C batch when nothing is staged (keeps L1 large)
 constexpr size_t phase_c_bytes(int slots) { return (size_t)slots * 128 + (size_t)kRleTile * 4 + (size_t)slots * 2; }
 constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * 2 * kPoolWords * 8;
 constexpr size_t kRegionBytes = kPoolBytes > phase_c_bytes(kSlotsPerBatch) ? kPoolBytes : phase_c_bytes(kSlotsPerBatch);
 
-inline size_t rle_meta_bytes(int n) { return n <= kMetaMax ? (size_t)n * 8 + ((size_t)n * 2 + 15) / 16 * 16 : 0; }
-
 inline size_t rle_smem_bytes(bool staged, int n) {
-    return kCntBytes + (staged ? kRegionBytes + rle_meta_bytes(n) : phase_c_bytes(kSlotsUnstaged));
+    (void)n;
+    return kCntBytes + (staged ? kRegionBytes : phase_c_bytes(kSlotsUnstaged));
 }
 
 enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };
@@ -257,7 +255,7 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
 //  !STAGED: every lane walks its streams directly from global memory (kept for
 //    A/B measurement, BQ_RLE_STAGED=0).
 template <bool STAGED>
-__global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED ? 3 : 6)
+__global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED ? 4 : 6)
     rle_count_kernel(const __grid_constant__ RleCountArgs a) {
     constexpr int NT = STAGED ? kStagedThreads : kRleThreads;
     constexpr int kSlots = STAGED ? kSlotsPerBatch : kSlotsUnstaged;
@@ -305,57 +303,24 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             if (e.x < L) sweep_stream<true>(a.ptrs[st] + e.x, (uint32_t)(L - e.x), e.y, ts, width, cnt);
         }
     } else {
-        // the tile's directory entries and aligned segment lengths, loaded once
-        // with full memory-level parallelism (one latency per tile, not per batch)
-        const bool use_meta = n <= kMetaMax;
-        uint2 *meta = reinterpret_cast<uint2 *>(region + kRegionBytes);              // [n]
-        uint16_t *seglen = reinterpret_cast<uint16_t *>(meta + (use_meta ? n : 0));   // [n]
-        auto segment = [&](int st, uint2 &e, uint32_t &len) {
-            const uint64_t L = a.lens[st];
-            e = a.dir[(size_t)tile * a.n + st];
-            len = 0;
-            if (e.x < L) {
-                const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : L;
-                const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + e.x) & ~(uintptr_t)15;
-                const uintptr_t b1 = (reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L)) + 15) & ~(uintptr_t)15;
-                len = (uint32_t)((b1 - b0) / 8);
+        // directory metadata of a lane's stream in batch k (tile-major rows: coalesced),
+        // fetched one batch ahead of use so its latency hides behind a walk
+        struct Pre {
+            uint2 e;
+            uint32_t nx;
+            uint64_t L;
+            const uint64_t *p;
+        };
+        auto fetch = [&](int st, Pre &q) {
+            q.e = make_uint2(0u, 0u);
+            q.L = 0;
+            if (st < n) {
+                q.L = a.lens[st];
+                q.e = a.dir[(size_t)tile * a.n + st];
+                q.nx = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : 0xFFFFFFFFu;
+                q.p = a.ptrs[st];
             }
         };
-        if (use_meta) {
-            constexpr int U = 4;  // loads of U streams in flight per thread
-            for (int base = 0; base < n; base += NT * U) {
-                uint64_t L[U];
-                uint2 e[U];
-                uint32_t nx[U];
-                const uint64_t *p[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int st = base + u * NT + tid;
-                    if (st < n) {
-                        L[u] = a.lens[st];
-                        e[u] = a.dir[(size_t)tile * a.n + st];
-                        nx[u] = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : 0xFFFFFFFFu;
-                        p[u] = a.ptrs[st];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int st = base + u * NT + tid;
-                    if (st < n) {
-                        uint32_t len = 0;
-                        if (e[u].x < L[u]) {
-                            const uint64_t next = nx[u] == 0xFFFFFFFFu ? L[u] : nx[u];
-                            const uintptr_t b0 = reinterpret_cast<uintptr_t>(p[u] + e[u].x) & ~(uintptr_t)15;
-                            const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p[u] + min(next + 1, L[u])) + 15) & ~(uintptr_t)15;
-                            len = (uint32_t)((b1 - b0) / 8);
-                        }
-                        meta[st] = e[u];
-                        seglen[st] = (uint16_t)min(len, 65535u);
-                    }
-                }
-            }
-            __syncthreads();
-        }
         uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * 2 * kPoolWords;
         // one mbarrier per pool half; 32 arrivals (one per lane) + the TMA byte count complete a phase
         uint64_t *bars = reinterpret_cast<uint64_t *>(cnt + kRleTile + 36) + warp * 2;
@@ -372,25 +337,19 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             bool staged;
         };
         // Stage batch k's segment of this lane's stream: one TMA bulk copy per lane.
-        auto plan = [&](int st, int k, Seg &sg) {
+        auto plan = [&](const Pre &q, int k, Seg &sg) {
             sg.lim = 0;
             sg.staged = false;
             uint32_t len = 0;
             uintptr_t b0 = 0;
-            if (st < n) {
-                uint2 e;
-                if (use_meta) {
-                    e = meta[st];
-                    len = seglen[st];
-                } else {
-                    segment(st, e, len);
-                }
-                if (len) {
-                    sg.g = a.ptrs[st] + e.x;
-                    sg.lim = (uint32_t)(a.lens[st] - e.x);
-                    sg.pos = e.y;
-                    b0 = reinterpret_cast<uintptr_t>(sg.g) & ~(uintptr_t)15;
-                }
+            if (q.e.x < q.L) {
+                const uint64_t next = q.nx == 0xFFFFFFFFu ? q.L : q.nx;
+                sg.g = q.p + q.e.x;
+                sg.lim = (uint32_t)(q.L - q.e.x);
+                sg.pos = q.e.y;
+                b0 = reinterpret_cast<uintptr_t>(sg.g) & ~(uintptr_t)15;
+                const uintptr_t b1 = (reinterpret_cast<uintptr_t>(q.p + min(next + 1, q.L)) + 15) & ~(uintptr_t)15;
+                len = (uint32_t)((b1 - b0) / 8);
             }
             uint32_t incl = len;
 #pragma unroll
@@ -431,14 +390,19 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             }
         };
         const int nk = (n + NT - 1) / NT;
+        const int my = warp * 32 + lane;
         Seg cur, nxt;
         nxt.lim = 0;
         nxt.staged = false;
-        plan(warp * 32 + lane, 0, cur);
+        Pre q0, q1;
+        fetch(my, q0);
+        fetch(NT + my, q1);
+        plan(q0, 0, cur);
         for (int k = 0; k < nk; ++k) {
             if (k + 1 < nk) {
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
-                plan((k + 1) * NT + warp * 32 + lane, k + 1, nxt);
+                plan(q1, k + 1, nxt);
+                fetch((k + 2) * NT + my, q1);
             }
             wait_batch(k);  // every lane's bulk copy for batch k has landed
             if (cur.lim && !a.debug) {
