@@ -23,7 +23,8 @@
 // The result popcount (cardinality, bitmaps.py:102-105) and the index of the
 // last nonzero word (the trim of bitmaps.py:66-67) are reduced in the kernel.
 //
-// The kernel is a persistent grid-stride loop over tiles of 512 words; the
+// The kernel is a persistent grid-stride loop over tiles of 2 x blockDim words
+// (512; narrower CTAs for inputs too small to fill the GPU); the
 // input pointer table is staged once per CTA in shared memory.  Loads are
 // 128-bit, non-allocating in L1 (each byte is read exactly once).
 #include <cuda_runtime.h>
@@ -142,11 +143,18 @@ __device__ __forceinline__ void column(const CountArgs &a, const uint64_t *const
                 for (int l = 0; l < 4; ++l)
                     acc[l] = (MODE == MODE_OR) ? (acc[l] | lane_of(x[k], l)) : (acc[l] & lane_of(x[k], l));
         }
-        for (; i < n; ++i) {
-            uint4 x = ld_input<FULL>(tab[i], w, FULL ? 0 : __ldg(a.lens + i));
+        if (i < n) {  // tail: up to 7 inputs, loads batched
+            uint4 x[7];
 #pragma unroll
-            for (int l = 0; l < 4; ++l)
-                acc[l] = (MODE == MODE_OR) ? (acc[l] | lane_of(x, l)) : (acc[l] & lane_of(x, l));
+            for (int k = 0; k < 7; ++k)
+                x[k] = (i + k < n) ? ld_input<FULL>(tab[i + k], w, FULL ? 0 : __ldg(a.lens + i + k))
+                                   : (MODE == MODE_OR ? make_uint4(0u, 0u, 0u, 0u)
+                                                      : make_uint4(~0u, ~0u, ~0u, ~0u));
+#pragma unroll
+            for (int k = 0; k < 7; ++k)
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    acc[l] = (MODE == MODE_OR) ? (acc[l] | lane_of(x[k], l)) : (acc[l] & lane_of(x[k], l));
         }
 #pragma unroll
         for (int l = 0; l < 4; ++l) res[l] = acc[l];
@@ -187,10 +195,18 @@ __device__ __forceinline__ void column(const CountArgs &a, const uint64_t *const
                 }
             }
         }
-        for (; i < n; ++i) {
-            uint4 x = ld_input<FULL>(tab[i], w, FULL ? 0 : __ldg(a.lens + i));
+        for (; i < n; i += 8) {  // remaining < 16 inputs (all of them when N < 16): loads batched by 8
+            uint4 x[8];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) ripple_add<M>(c[l], lane_of(x, l), 0);
+            for (int k = 0; k < 8; ++k)
+                x[k] = (i + k < n) ? ld_input<FULL>(tab[i + k], w, FULL ? 0 : __ldg(a.lens + i + k))
+                                   : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (i + k < n) {
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) ripple_add<M>(c[l], lane_of(x[k], l), 0);
+                }
         }
 #pragma unroll
         for (int l = 0; l < 4; ++l) res[l] = epilogue<M, MODE>(c[l], a, slut);
@@ -203,19 +219,20 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__
     const uint64_t **stab = reinterpret_cast<const uint64_t **>(smem);
     uint32_t *slut = reinterpret_cast<uint32_t *>(smem + (SMEM_TABLE ? (size_t)a.n * 8 : 0));
     if (SMEM_TABLE)
-        for (int i = threadIdx.x; i < a.n; i += kThreads) stab[i] = a.ptrs[i];
+        for (int i = threadIdx.x; i < a.n; i += blockDim.x) stab[i] = a.ptrs[i];
     if (MODE == MODE_LUT) {
         const int lut_words = ((1 << M) + 31) / 32;
-        for (int i = threadIdx.x; i < lut_words; i += kThreads) slut[i] = a.lut[i];
+        for (int i = threadIdx.x; i < lut_words; i += blockDim.x) slut[i] = a.lut[i];
     }
     __syncthreads();
     const uint64_t *const *tab = SMEM_TABLE ? stab : a.ptrs;
 
     unsigned long long pc = 0, lnz = 0;
-    const uint64_t ntiles = (a.nwords + kTileWords - 1) / kTileWords;
+    const uint64_t tile_words = 2ull * blockDim.x;  // kTileWords, or less for small inputs
+    const uint64_t ntiles = (a.nwords + tile_words - 1) / tile_words;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t w = tile * kTileWords + 2 * threadIdx.x;
-        const bool full = (tile + 1) * kTileWords <= a.full_words;  // CTA-uniform
+        const uint64_t w = tile * tile_words + 2 * threadIdx.x;
+        const bool full = (tile + 1) * tile_words <= a.full_words;  // CTA-uniform
         if (w >= a.nwords) continue;
         uint32_t res[4];
         if (full)
@@ -320,10 +337,13 @@ int launch_count(const CountArgs &a, int m, int mode, cudaStream_t stream) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(count_kernel)");
     }
-    const uint64_t ntiles = (a.nwords + kTileWords - 1) / kTileWords;
-    uint64_t grid = (uint64_t)sm_count() * (uint64_t)blocks_per_sm(fn, smem);
+    // small inputs: narrower CTAs so at least ~2 CTAs per SM get work (C1 is 16k words)
+    int threads = kThreads;
+    while (threads > 64 && (a.nwords + 2ull * threads - 1) / (2ull * threads) < 2ull * (uint64_t)sm_count()) threads >>= 1;
+    const uint64_t ntiles = (a.nwords + 2ull * threads - 1) / (2ull * threads);
+    uint64_t grid = (uint64_t)sm_count() * (uint64_t)blocks_per_sm(fn, smem) * (kThreads / threads);
     if (grid > ntiles) grid = ntiles;
-    fn<<<(unsigned)grid, kThreads, smem, stream>>>(a);
+    fn<<<(unsigned)grid, threads, smem, stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "count_kernel launch");
     return BQ_OK;
