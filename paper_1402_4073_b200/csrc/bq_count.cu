@@ -38,7 +38,6 @@
 namespace bq {
 
 constexpr int kThreads = 256;
-constexpr int kTileWords = kThreads * 2;
 
 __device__ __forceinline__ uint4 ld_stream(const uint64_t *p) {
     uint4 r;
