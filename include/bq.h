@@ -158,6 +158,14 @@ BQ_API int bq_rle_query_symmetric(bq_rle_query *q, const uint8_t *h_accept, uint
 BQ_API int bq_rle_encode_host(const uint64_t *h_words, uint64_t n_words, uint64_t r_bits,
                               uint64_t *h_out, uint64_t cap, uint64_t *out_len);
 
+/* The same canonical encoding computed on the device (csrc/bq_encode.cu):
+ * d_words (n_words valid words of a ceil(r/64)-word bitmap) -> d_out.  The
+ * encoding never exceeds ceil(r/64) + 1 words.  Synchronous on `stream`;
+ * *out_len receives the encoded length (also when cap is too small:
+ * BQ_ERESOURCE).  Requires ceil(r/64) < 2^31. */
+BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_words, uint64_t r_bits, uint64_t *d_out,
+                                uint64_t cap, uint64_t *out_len, void *stream);
+
 /* ---- benchmark input generation (K5, csrc/bq_gen.h) ---------------------- */
 
 /* Words [w0, w0 + nw) of bitmap `bitmap` under `seed`, each bit Bernoulli(q16 / 65536).

@@ -117,6 +117,20 @@ def compress_words(words, bit_length: int) -> list:
     return out[: n_out.value].tolist()
 
 
+def encode_device(words: torch.Tensor, bit_length: int) -> np.ndarray:
+    """Canonical RLE encoding (RleBuilder, bitmaps.py:351-414) of device words,
+    computed on the GPU (bq_rle_encode_device); returns the host stream."""
+    lib = _lib.load()
+    nw = word_count(bit_length)
+    cap = nw + 2
+    dout = torch.empty(max(cap, 2), dtype=torch.int64, device=words.device)
+    n_out = ctypes.c_uint64(0)
+    _lib.check(lib.bq_rle_encode_device(words.data_ptr() if words.numel() else None, min(words.numel(), nw),
+                                        bit_length, dout.data_ptr(), cap, ctypes.byref(n_out),
+                                        torch.cuda.current_stream(words.device).cuda_stream), "bq_rle_encode_device")
+    return dout[: n_out.value].cpu().numpy().view(np.uint64)
+
+
 def _finish(bitmaps, out: torch.Tensor, nwords: int, r: int, popcnt: torch.Tensor, last_nz: torch.Tensor):
     """Wrap a device result like the reference would (type of bitmaps[0])."""
     proto = bitmaps[0]
@@ -125,12 +139,11 @@ def _finish(bitmaps, out: torch.Tensor, nwords: int, r: int, popcnt: torch.Tenso
         return DeviceBitmap(out[:nwords] if nwords else out[:0], r, nwords)
     if k == "dr":
         return DeviceBitmap(out[:nwords] if nwords else out[:0], r, nwords)
-    used = int(last_nz.item())
-    words = out[:used].cpu().numpy().view(np.uint64)
     if k == "u":
-        res = type(proto)(words.tolist(), r)
-    else:
-        res = type(proto)(compress_words(words, r), r)
+        used = int(last_nz.item())
+        res = type(proto)(out[:used].cpu().numpy().view(np.uint64).tolist(), r)
+    else:  # RLE in -> canonical RLE out, encoded on the device; only the stream crosses PCIe
+        res = type(proto)(encode_device(out[:nwords], r).tolist(), r)
     card = int(popcnt.item())
     if hasattr(res, "_card"):
         try:
@@ -165,10 +178,6 @@ def _run(bitmaps, r, t=None, accept=None):
         else:
             q.symmetric(accept, out, popcnt)
         q.close()
-        # trim point for host results
-        if kind_of(bitmaps[0]) == "r":
-            nz = torch.nonzero(out[:nw]).flatten()
-            last_nz.fill_(int(nz[-1].item()) + 1 if nz.numel() else 0)
     return _finish(bitmaps, out, nw, r, popcnt, last_nz)
 
 

@@ -178,3 +178,36 @@ def test_rle_errors(bq):
         q.threshold(3)
     with pytest.raises(bq.InputError):
         q.symmetric([True, False])
+
+
+@pytest.mark.parametrize("case", [c for c in CODEC if c.meta["kind"] == "compress"] + RLE[::3], ids=lambda c: c.id)
+def test_device_encoder_matches_reference(bq, case):
+    """bq_rle_encode_device == the reference's canonical compress (bitmaps.py:407-414)."""
+    from paper_1402_4073_b200.api import encode_device
+
+    if case.meta["kind"] == "compress":
+        words, expect = case.inputs[0], case.out
+    else:
+        words, expect = np.array(case.meta["uncompressed"], dtype=np.uint64), case.out
+    t = torch.from_numpy(np.ascontiguousarray(words, dtype=np.uint64).view(np.int64)).cuda() if words.size \
+        else torch.zeros(0, dtype=torch.int64, device="cuda")
+    assert np.array_equal(encode_device(t, case.r), expect)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_device_encoder_random(bq, seed):
+    from paper_1402_4073_b200.api import compress_words, encode_device
+
+    rng = np.random.default_rng(seed)
+    nw = int(rng.integers(1, 20000))
+    r = 64 * nw - int(rng.integers(0, 64))
+    kinds = rng.integers(0, 3, size=nw)
+    words = np.where(kinds == 0, 0, np.where(kinds == 1, np.uint64(2**64 - 1),
+                                             rng.integers(1, 2**63, size=nw, dtype=np.uint64))).astype(np.uint64)
+    # runs: repeat classes to create long fills
+    words = np.repeat(words, rng.integers(1, 6, size=nw))[:nw]
+    if r % 64:
+        words[-1] &= np.uint64((1 << (r % 64)) - 1)
+    cut = int(rng.integers(0, nw + 1))
+    t = torch.from_numpy(words[:cut].view(np.int64).copy()).cuda()
+    assert encode_device(t, r).tolist() == compress_words(words[:cut], r)
