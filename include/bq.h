@@ -166,6 +166,28 @@ BQ_API int bq_rle_encode_host(const uint64_t *h_words, uint64_t n_words, uint64_
 BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_words, uint64_t r_bits, uint64_t *d_out,
                                 uint64_t cap, uint64_t *out_len, void *stream);
 
+/* ---- straight-line BitPrograms (circuits/programs.py) --------------------- */
+
+/* A reference BitProgram (programs.py:56-72) JIT-compiled for sm_100a with
+ * NVRTC: one thread per output word, every slot a register.  instr holds
+ * n_instr (opcode, dst, a, b) quadruples with the reference opcodes
+ * (programs.py:21-28: 0 zero, 1 one, 2 and, 3 or, 4 xor, 5 andnot, 6 not,
+ * 7 reclaim).  BQ_EFORMAT for an unknown opcode or slot out of range;
+ * BQ_ECUDA if NVRTC / the driver is unavailable.  Opaque. */
+typedef struct bq_program bq_program;
+BQ_API int bq_program_compile(const int32_t *instr, int n_instr, int arity, int n_slots, int result_slot,
+                              bq_program **out);
+BQ_API void bq_program_destroy(bq_program *p);
+/* The generated CUDA source (NUL-terminated; *len includes the NUL): the GPU
+ * counterpart of emit_source (programs.py:332-352). */
+BQ_API int bq_program_source(const bq_program *p, char *buf, uint64_t cap, uint64_t *len);
+/* Run the program over the inputs of a prepared query (its arity must equal
+ * the query's n, programs.py:240-242), like execute / execute_horizontal
+ * (programs.py:163-237).  Output and popcount / last-nonzero conventions are
+ * those of bq_query_threshold.  Asynchronous on stream. */
+BQ_API int bq_program_execute(bq_program *p, bq_query *q, uint64_t *d_out, unsigned long long *d_popcnt,
+                              unsigned long long *d_last_nz, void *stream);
+
 /* ---- benchmark input generation (K5, csrc/bq_gen.h) ---------------------- */
 
 /* Words [w0, w0 + nw) of bitmap `bitmap` under `seed`, each bit Bernoulli(q16 / 65536).

@@ -14,6 +14,10 @@ word-range multi-GPU partitioner in :mod:`.shard`; the C ABI underneath is
 from .api import (
     DEFAULT_BUDGET_BYTES,
     CircuitLibrary,
+    CompiledProgram,
+    compile_program,
+    execute,
+    execute_horizontal,
     cdom_symmetric,
     cdom_threshold,
     compress,

@@ -51,6 +51,10 @@ SIGNATURES = {
     "bq_rle_query_symmetric": (_I, [_P, _P, _P, _P, _P]),
     "bq_rle_encode_host": (_I, [_P, _U64, _U64, _P, _U64, _P]),
     "bq_rle_encode_device": (_I, [_P, _U64, _U64, _P, _U64, _P, _P]),
+    "bq_program_compile": (_I, [_P, _I, _I, _I, _I, _P]),
+    "bq_program_destroy": (None, [_P]),
+    "bq_program_source": (_I, [_P, _P, _U64, _P]),
+    "bq_program_execute": (_I, [_P, _P, _P, _P, _P, _P]),
     "bq_gen_bernoulli": (_I, [_U64, _U32, _U32, _U64, _U64, _P, _I, _P]),
     "bq_gen_bernoulli_rows": (_I, [_U64, _U32, _I, _P, _U64, _U64, _P, _U64, _P]),
     "bq_gen_density_q16": (_U32, [_U64, _U32, _U32, _U32]),

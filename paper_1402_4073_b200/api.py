@@ -356,3 +356,101 @@ def _cardinality(b) -> int:
     if hasattr(b, "cardinality"):
         return int(b.cardinality())
     return 0
+
+
+# ---------------------------------------------------------------------------
+# straight-line BitPrograms (circuits/programs.py), JIT-compiled for the GPU
+
+class CompiledProgram:
+    """A reference BitProgram (programs.py:56-72) compiled to an sm_100a kernel
+    with NVRTC (bq_program_compile).  Duck-typed: anything with ``arity``,
+    ``n_slots``, ``result_slot`` and ``instructions`` [(op, dst, a, b)]."""
+
+    def __init__(self, program):
+        self._lib = _lib.load()
+        self.arity = int(program.arity)
+        self.n_slots = int(program.n_slots)
+        self.result_slot = int(program.result_slot)
+        ins = np.asarray([tuple(i) for i in program.instructions], dtype=np.int32).reshape(-1, 4)
+        self._ins = np.ascontiguousarray(ins)
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.bq_program_compile(self._ins.ctypes.data if ins.size else None, len(ins), self.arity,
+                                                self.n_slots, self.result_slot, ctypes.byref(h)),
+                   "bq_program_compile")
+        self._h = h
+
+    def source(self) -> str:
+        """Generated CUDA source (the GPU analogue of emit_source, programs.py:332-352)."""
+        n = ctypes.c_uint64(0)
+        _lib.check(self._lib.bq_program_source(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _lib.check(self._lib.bq_program_source(self._h, buf, n.value, ctypes.byref(n)))
+        return buf.value.decode()
+
+    def run(self, query: ThresholdQuery, out, popcnt, last_nz, stream=None):
+        from .engine import stream_handle
+        _lib.check(self._lib.bq_program_execute(self._h, query._h, out.data_ptr(), popcnt.data_ptr(),
+                                                last_nz.data_ptr() if last_nz is not None else None,
+                                                stream_handle(stream, query.device)), "bq_program_execute")
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                self._lib.bq_program_destroy(self._h)
+        except Exception:
+            pass
+
+
+_PROGRAM_CACHE: dict = {}
+
+
+def compile_program(program) -> CompiledProgram:
+    """Compile (once per distinct program) and cache."""
+    key = (int(program.arity), int(program.n_slots), int(program.result_slot),
+           tuple(tuple(int(x) for x in i) for i in program.instructions))
+    got = _PROGRAM_CACHE.get(key)
+    if got is None:
+        got = _PROGRAM_CACHE[key] = CompiledProgram(program)
+    return got
+
+
+def _check_program_inputs(program, inputs):
+    if len(inputs) != program.arity:  # programs.py:240-242
+        raise InputError(f"program expects {program.arity} inputs, got {len(inputs)}")
+    if len({type(b) for b in inputs}) > 1:  # programs.py:243-245
+        raise InputError("program inputs must share one representation")
+
+
+def execute(program, inputs: Sequence):
+    """circuits.execute (programs.py:163-193) on the GPU: any straight-line
+    program over either representation; result of type(inputs[0])."""
+    _check_program_inputs(program, inputs)
+    r = max(b.bit_length for b in inputs)
+    device = _device_for(inputs)
+    dev = _dev_inputs(inputs, device)
+    if kind_of(inputs[0]) in ("r", "dr"):  # decode RLE inputs on the device first
+        decoded = []
+        for d in dev:
+            q = RleQuery([d], r, device=device)
+            words, _ = q.threshold(1)
+            q.close()
+            decoded.append(DeviceBitmap(words[: word_count(r)], r, word_count(r)))
+        dev = decoded
+    nw = word_count(r)
+    out = torch.empty(max(nw, 2), dtype=torch.int64, device=device)
+    popcnt = torch.zeros(1, dtype=torch.int64, device=device)
+    last_nz = torch.zeros(1, dtype=torch.int64, device=device)
+    q = ThresholdQuery(dev, r, device=device)
+    compile_program(program).run(q, out, popcnt, last_nz)
+    q.close()
+    return _finish(inputs, out, nw, r, popcnt, last_nz)
+
+
+def execute_horizontal(program, inputs: Sequence, batch_words: int = 256):
+    """circuits.execute_horizontal (programs.py:196-237): uncompressed inputs
+    only.  The GPU evaluates every word column in parallel, so ``batch_words``
+    (the reference's CPU tile) does not change the result and is ignored."""
+    _check_program_inputs(program, inputs)
+    if kind_of(inputs[0]) not in ("u", "du"):
+        raise InputError("horizontal execution requires uncompressed bitmaps")
+    return execute(program, inputs)

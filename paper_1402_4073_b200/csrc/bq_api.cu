@@ -204,6 +204,25 @@ BQ_API void bq_query_destroy(bq_query *q) {
 
 BQ_API uint64_t bq_query_out_words(const bq_query *q) { return q ? q->nwords : 0; }
 
+}  // extern "C"
+
+namespace bq {
+int query_view(const bq_query *q, const uint64_t *const **ptrs, const uint64_t **lens, int *n, uint64_t *nwords,
+               uint64_t *full_words, uint64_t *last_mask, int *device) {
+    if (!q) return set_error(BQ_EINPUT, "query is NULL");
+    *ptrs = q->d_ptrs;
+    *lens = q->d_lens;
+    *n = q->n;
+    *nwords = q->nwords;
+    *full_words = q->full_words;
+    *last_mask = q->last_mask;
+    *device = q->device;
+    return BQ_OK;
+}
+}  // namespace bq
+
+extern "C" {
+
 static int base_args(bq_query *q, uint64_t *d_out, unsigned long long *d_popcnt,
                      unsigned long long *d_last_nz, CountArgs &a) {
     if (!q) return set_error(BQ_EINPUT, "query is NULL");

@@ -36,6 +36,9 @@ from bitquorum import counters, oracle, runmerge  # noqa: E402
 from bitquorum.circuits import (  # noqa: E402
     CircuitLibrary,
     build_sideways_sum,
+    build_sop,
+    build_sorter,
+    build_symmetric,
     build_tree_adder,
     compile_circuit,
     csv_threshold,
@@ -301,6 +304,38 @@ def codec_cases(rng):
     wr.save()
 
 
+def program_cases(rng):
+    """Reference BitPrograms (TreeAdd / SSum / SrtCkt / SoP / build_symmetric),
+    optimized + compiled by the reference, with the reference's execute()
+    result on uncompressed and RLE inputs."""
+    wr = Writer("programs")
+    specs = [("tree", 5, 2), ("sideways", 5, 2), ("sorter", 8, 3), ("sop", 4, 2), ("sideways", 33, 17),
+             ("tree", 64, 32), ("sorter", 16, 9), ("sideways", 64, 1), ("tree", 7, 7), ("sorter", 12, 12)]
+    builders = {"tree": build_tree_adder, "sideways": build_sideways_sum, "sorter": build_sorter, "sop": build_sop}
+    progs = []
+    for name, n, t in specs:
+        progs.append((f"{name}({n},{t})", n, compile_circuit(optimize(builders[name](n, t)))))
+    for n, spec in [(8, oracle.SymmetricSpec.interval(8, 2, 5)), (9, oracle.SymmetricSpec.parity(9)),
+                    (12, oracle.SymmetricSpec.delta(12, 0)), (10, oracle.SymmetricSpec((True,) + (False,) * 5 + (True,) * 5))]:
+        for strategy in ("sorter", "adder"):
+            progs.append((f"symmetric-{strategy}({n})", n, compile_circuit(optimize(build_symmetric(spec, strategy)))))
+    for label, n, prog in progs:
+        r = rng.choice([64 * 40, 64 * 100 + 17, 3000])
+        inputs = make_inputs(rng, n, r)
+        got = execute(prog, inputs)
+        assert execute_horizontal(prog, inputs) == got
+        comp = [bm.compress(b) for b in inputs]
+        got_rle = execute(prog, comp)
+        assert bm.decompress(got_rle) == got
+        ins = np.array(prog.instructions, dtype=np.int64).reshape(-1, 4)
+        wr.add([b.words for b in inputs], [b.bit_length for b in inputs], got.words,
+               {"label": label, "r": max(b.bit_length for b in inputs), "arity": prog.arity,
+                "n_slots": prog.n_slots, "result_slot": prog.result_slot, "peak_slots": prog.peak_slots,
+                "instructions": ins.tolist(), "rle_out": [str(w) for w in got_rle.words],
+                "card": got.cardinality()})
+    wr.save()
+
+
 def generator_cases():
     out = {"seed": 1402, "cases": []}
     for (i, w, q) in [(0, 0, 6554), (0, 1, 6554), (3, 12345, 6554), (7, 0, 32768), (1, 99, 3277),
@@ -347,4 +382,5 @@ if __name__ == "__main__":
     symmetric_cases(rng)
     rle_cases(rng)
     codec_cases(rng)
+    program_cases(rng)
     kat()

@@ -165,3 +165,16 @@ def test_registry_plugs_into_reference():
     for name in names:
         assert name in competitions.ALGORITHMS
     assert competitions.ALGORITHMS["gpu_cdom"].reprs == frozenset({"ewah"})
+
+
+def test_program_compile_validates_before_jit(lib):
+    """Malformed programs are rejected (FormatError) before NVRTC is touched."""
+    import paper_1402_4073_b200 as bq
+    import types
+
+    bad_op = types.SimpleNamespace(arity=2, n_slots=3, result_slot=2, instructions=[(9, 2, 0, 1)])
+    with pytest.raises(bq.FormatError):
+        bq.CompiledProgram(bad_op)
+    bad_slot = types.SimpleNamespace(arity=2, n_slots=3, result_slot=2, instructions=[(2, 2, 0, 7)])
+    with pytest.raises(bq.FormatError):
+        bq.CompiledProgram(bad_slot)
