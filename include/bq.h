@@ -166,6 +166,15 @@ BQ_API int bq_rle_encode_host(const uint64_t *h_words, uint64_t n_words, uint64_
 BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_words, uint64_t r_bits, uint64_t *d_out,
                                 uint64_t cap, uint64_t *out_len, void *stream);
 
+/* ---- whole-bitmap set algebra (bitmaps.py:438-476, :598-644) -------------
+ * kind: 0 and, 1 or, 2 xor, 3 andnot (a & ~b), 4 not (~a within r_bits; b unused).
+ * Operands of na / nb words (missing words zero); output ceil(r/64) words with
+ * bits >= r cleared, popcount ADDED to d_popcnt, max(index+1) of nonzero words
+ * to d_last_nz (both optional).  Asynchronous on stream. */
+BQ_API int bq_binary_op(int kind, const uint64_t *d_a, uint64_t na, const uint64_t *d_b, uint64_t nb,
+                        uint64_t r_bits, uint64_t *d_out, unsigned long long *d_popcnt,
+                        unsigned long long *d_last_nz, void *stream);
+
 /* ---- straight-line BitPrograms (circuits/programs.py) --------------------- */
 
 /* A reference BitProgram (programs.py:56-72) JIT-compiled for sm_100a with

@@ -15,6 +15,12 @@ from .api import (
     DEFAULT_BUDGET_BYTES,
     CircuitLibrary,
     CompiledProgram,
+    and_,
+    andnot,
+    binary_op,
+    not_,
+    or_,
+    xor,
     compile_program,
     execute,
     execute_horizontal,

@@ -454,3 +454,79 @@ def execute_horizontal(program, inputs: Sequence, batch_words: int = 256):
     if kind_of(inputs[0]) not in ("u", "du"):
         raise InputError("horizontal execution requires uncompressed bitmaps")
     return execute(program, inputs)
+
+
+# ---------------------------------------------------------------------------
+# whole-bitmap set algebra on the device (bitmaps.py:438-677)
+
+_OPS = {"and": 0, "or": 1, "xor": 2, "andnot": 3}
+
+
+def _operand_words(b, r, device):
+    """Device words of an operand: uncompressed as is, RLE decoded on the device."""
+    k = kind_of(b)
+    if k == "du":
+        return b.data, b.n_words
+    if k == "u":
+        t = UPLOADS.get(b, device)
+        return t, t.numel()
+    d = b if k == "dr" else DeviceRleBitmap(UPLOADS.get(b, device), b.bit_length)
+    q = RleQuery([d], r, device=device)
+    words, _ = q.threshold(1)
+    q.close()
+    return words, word_count(r)
+
+
+def _set_op(kind: int, a, b, r: int):
+    device = _device_for([a] if b is None else [a, b])
+    ta, na = _operand_words(a, r, device)
+    tb, nb = (None, 0) if b is None else _operand_words(b, r, device)
+    nw = word_count(r)
+    out = torch.empty(max(nw, 2), dtype=torch.int64, device=device)
+    popcnt = torch.zeros(1, dtype=torch.int64, device=device)
+    last_nz = torch.zeros(1, dtype=torch.int64, device=device)
+    from .engine import stream_handle
+    lib = _lib.load()
+    _lib.check(lib.bq_binary_op(kind, ta.data_ptr() if na else None, na,
+                                (tb.data_ptr() if nb else None) if tb is not None else None, nb, r,
+                                out.data_ptr(), popcnt.data_ptr(), last_nz.data_ptr(),
+                                stream_handle(None, device)), "bq_binary_op")
+    return _finish([a], out, nw, r, popcnt, last_nz)
+
+
+def _check_same_type(a, b):
+    if type(a) is not type(b):  # bitmaps.py:591-595
+        raise InputError("mixed bitmap representations; convert explicitly with compress/decompress")
+
+
+def binary_op(kind: str, a, b):
+    """bitmaps.binary_op (bitmaps.py:629-635) on the device."""
+    try:
+        code = _OPS[kind.lower()]
+    except KeyError:
+        raise InputError(f"unknown operation {kind!r}") from None
+    _check_same_type(a, b)
+    return _set_op(code, a, b, max(a.bit_length, b.bit_length))
+
+
+def and_(a, b):
+    return binary_op("and", a, b)
+
+
+def or_(a, b):
+    return binary_op("or", a, b)
+
+
+def xor(a, b):
+    return binary_op("xor", a, b)
+
+
+def andnot(a, b):
+    return binary_op("andnot", a, b)
+
+
+def not_(a, bit_length: int):
+    """bitmaps.not_ (bitmaps.py:638-644): complement within [0, bit_length)."""
+    if bit_length < a.bit_length:
+        raise InputError("complement universe smaller than the bitmap")
+    return _set_op(4, a, None, bit_length)

@@ -349,3 +349,63 @@ int launch_count(const CountArgs &a, int m, int mode, cudaStream_t stream) {
 }
 
 }  // namespace bq
+
+// ---------------------------------------------------------------------------
+// Whole-bitmap set algebra (bitmaps.py:438-476, 598-644) with fused popcount.
+namespace bq {
+
+__global__ void __launch_bounds__(256) binop_kernel(int kind, const uint64_t *__restrict__ a, uint64_t na,
+                                                   const uint64_t *__restrict__ b, uint64_t nb, uint64_t nwords,
+                                                   uint64_t last_mask, uint64_t *__restrict__ out,
+                                                   unsigned long long *popcnt, unsigned long long *last_nz) {
+    unsigned long long pc = 0, lnz = 0;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = w < na ? __ldg(a + w) : 0ull;
+        const uint64_t y = w < nb ? __ldg(b + w) : 0ull;
+        uint64_t r;
+        switch (kind) {
+            case 0: r = x & y; break;   // _u_and: zero beyond the shorter operand
+            case 1: r = x | y; break;   // _u_or: longer tail copied
+            case 2: r = x ^ y; break;   // _u_xor
+            case 3: r = x & ~y; break;  // _u_andnot: a's tail copied
+            default: r = ~x; break;     // _u_not: complement within r
+        }
+        if (w == nwords - 1) r &= last_mask;
+        out[w] = r;
+        pc += __popcll(r);
+        if (r) lnz = w + 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        pc += __shfl_down_sync(0xffffffffu, pc, o);
+        unsigned long long t = __shfl_down_sync(0xffffffffu, lnz, o);
+        lnz = t > lnz ? t : lnz;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (popcnt && pc) atomicAdd(popcnt, pc);
+        if (last_nz && lnz) atomicMax(last_nz, lnz);
+    }
+}
+
+}  // namespace bq
+
+extern "C" BQ_API int bq_binary_op(int kind, const uint64_t *d_a, uint64_t na, const uint64_t *d_b, uint64_t nb,
+                                   uint64_t r_bits, uint64_t *d_out, unsigned long long *d_popcnt,
+                                   unsigned long long *d_last_nz, void *stream) {
+    using namespace bq;
+    if (kind < 0 || kind > 4) return set_error(BQ_EINPUT, "unknown operation %d", kind);
+    const uint64_t nwords = word_count(r_bits);
+    if (na > nwords || (kind != 4 && nb > nwords)) return set_error(BQ_EINPUT, "more words than bit_length allows");
+    if ((na && !d_a) || (kind != 4 && nb && !d_b)) return set_error(BQ_EINPUT, "NULL operand");
+    if (nwords && !d_out) return set_error(BQ_EINPUT, "d_out is NULL");
+    if (!nwords) return BQ_OK;
+    const uint64_t last_mask = (r_bits % W) ? ((1ull << (r_bits % W)) - 1) : ~0ull;
+    uint64_t grid = (nwords + 255) / 256;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    binop_kernel<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        kind, d_a, na, kind == 4 ? nullptr : d_b, kind == 4 ? 0 : nb, nwords, last_mask, d_out, d_popcnt, d_last_nz);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "binop_kernel launch");
+    return BQ_OK;
+}

@@ -336,6 +336,32 @@ def program_cases(rng):
     wr.save()
 
 
+def setop_cases(rng):
+    """bitmaps.and_/or_/xor/andnot/not_ on both representations (bitmaps.py:438-644)."""
+    wr = Writer("setops")
+    for k in range(24):
+        ra, rb = rng.choice([0, 1, 64, 130, 64 * 20, 3001]), rng.choice([0, 64, 200, 64 * 20 + 5, 3001])
+        kind_a = rng.choice(["sparse", "dense", "runs", "zero", "one", "uniform"])
+        kind_b = rng.choice(["sparse", "dense", "runs", "zero", "one", "uniform"])
+        a = bm.UncompressedBitmap(rand_bitmap(rng, ra, kind_a), ra)
+        b = bm.UncompressedBitmap(rand_bitmap(rng, rb, kind_b), rb)
+        ca, cb = bm.compress(a), bm.compress(b)
+        for op in ("and", "or", "xor", "andnot"):
+            u = bm.binary_op(op, a, b)
+            c = bm.binary_op(op, ca, cb)
+            assert bm.decompress(c) == u
+            wr.add([a.words, b.words], [ra, rb], u.words,
+                   {"op": op, "r": u.bit_length, "rle_a": [str(w) for w in ca.words],
+                    "rle_b": [str(w) for w in cb.words], "rle_out": [str(w) for w in c.words]})
+        rn = max(ra, rng.choice([ra, ra + 1, ra + 64, ra + 100]))
+        u = bm.not_(a, rn)
+        c = bm.not_(ca, rn)
+        assert bm.decompress(c) == u
+        wr.add([a.words], [ra], u.words, {"op": "not", "r": rn, "rle_a": [str(w) for w in ca.words],
+                                           "rle_out": [str(w) for w in c.words]})
+    wr.save()
+
+
 def generator_cases():
     out = {"seed": 1402, "cases": []}
     for (i, w, q) in [(0, 0, 6554), (0, 1, 6554), (3, 12345, 6554), (7, 0, 32768), (1, 99, 3277),
@@ -383,4 +409,5 @@ if __name__ == "__main__":
     rle_cases(rng)
     codec_cases(rng)
     program_cases(rng)
+    setop_cases(rng)
     kat()

@@ -211,3 +211,22 @@ def test_device_encoder_random(bq, seed):
     cut = int(rng.integers(0, nw + 1))
     t = torch.from_numpy(words[:cut].view(np.int64).copy()).cuda()
     assert encode_device(t, r).tolist() == compress_words(words[:cut], r)
+
+
+SETOPS = load_golden("setops")
+
+
+@pytest.mark.parametrize("case", SETOPS, ids=lambda c: c.id + "-" + c.meta["op"])
+def test_set_algebra_matches_reference(bq, case):
+    """and_/or_/xor/andnot/not_ on the device, both representations (bitmaps.py:438-644)."""
+    op = case.meta["op"]
+    ua = bq.UncompressedBitmap(case.inputs[0].tolist(), case.bits[0])
+    ra = bq.RleBitmap([int(w) for w in case.meta["rle_a"]], case.bits[0])
+    if op == "not":
+        got_u, got_r = bq.not_(ua, case.r), bq.not_(ra, case.r)
+    else:
+        ub = bq.UncompressedBitmap(case.inputs[1].tolist(), case.bits[1])
+        rb = bq.RleBitmap([int(w) for w in case.meta["rle_b"]], case.bits[1])
+        got_u, got_r = bq.binary_op(op, ua, ub), bq.binary_op(op, ra, rb)
+    assert got_u.words == case.out.tolist() and got_u.bit_length == case.r
+    assert [str(w) for w in got_r.words] == case.meta["rle_out"] and got_r.bit_length == case.r
