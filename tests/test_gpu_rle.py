@@ -230,3 +230,30 @@ def test_set_algebra_matches_reference(bq, case):
         got_u, got_r = bq.binary_op(op, ua, ub), bq.binary_op(op, ra, rb)
     assert got_u.words == case.out.tolist() and got_u.bit_length == case.r
     assert [str(w) for w in got_r.words] == case.meta["rle_out"] and got_r.bit_length == case.r
+
+
+def test_all_literal_streams_overflow_pools(bq):
+    """Uniform random words: every word is a literal, so each tile segment
+    (~1025 words per stream) overflows the warp pool (walked from HBM) and every
+    output word is undecided (phase C runs in several slot batches)."""
+    from oracle import oracle as Or
+
+    rng = np.random.default_rng(11)
+    n, r = 40, 64 * 5000 - 9
+    nw = (r + 63) // 64
+    streams = []
+    for i in range(n):
+        w = rng.integers(1, 2**63, size=nw, dtype=np.uint64) | np.uint64(1 << 63) if i % 2 else \
+            rng.integers(0, 2**64 - 1, size=nw, dtype=np.uint64)
+        w[-1] &= np.uint64((1 << (r % 64)) - 1)
+        streams.append(Or.rle_compress(Or.trim(w), r))
+    q = bq.RleQuery(dev(streams), r)
+    for t in (1, 5, 20, 39, 40):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+    acc = [k % 3 == 0 for k in range(n + 1)]
+    out, pc = q.symmetric(acc)
+    exp = O.cdom_symmetric(streams, r, acc)
+    assert np.array_equal(host(out, nw), exp)

@@ -228,3 +228,28 @@ def test_errors(bq):
         bq.scan_count([bq.UncompressedBitmap([1], 64), bq.RleBitmap([], 64)], 1)  # mixed representations
     with pytest.raises(bq.ResourceError):
         bq.scan_count([bq.UncompressedBitmap([1], 1 << 40)], 1, budget_bytes=1 << 20)
+
+
+@pytest.mark.parametrize("n", [8200, 20000])
+def test_large_n_global_pointer_table(bq, n):
+    """N > 8192: the kernel reads the pointer table from global memory; M = 14/16-bit counters."""
+    lib = bq._lib.load()
+    nw = 96
+    r = 64 * nw - 3
+    arrs = []
+    for i in range(n):
+        a = gen(lib, 21, i, 32768 if i % 3 else 65000, nw)
+        a[-1] &= np.uint64((1 << 61) - 1)
+        arrs.append(a[: nw - (i % 7)])
+    q = bq.ThresholdQuery(dev(arrs), r)
+    for t in (1, n // 2, n - 3, n):
+        out, pc = q.threshold(t)
+        exp = O.threshold_port(arrs, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+    rng = np.random.default_rng(n)
+    acc = [bool(rng.random() < 0.5) for _ in range(n + 1)]  # many breakpoints -> LUT epilogue
+    out, pc = q.symmetric(acc)
+    exp = O.scan_count_symmetric(arrs, r, acc)
+    assert np.array_equal(host(out, nw), exp)
+    assert int(pc.item()) == popcount(exp)
