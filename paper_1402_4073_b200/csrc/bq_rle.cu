@@ -195,47 +195,49 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
     auto load = [src](uint32_t k) { return GLOBAL ? __ldg(src + k) : src[k]; };
     if (lim == 0) return;
     const uint32_t Wu = (uint32_t)W;
+    const uint32_t dummy = Wu + 1 + (threadIdx.x & 31);  // this lane's slot for empty contributions
     // first marker: its fill starts at or before the tile (64-bit positions)
     uint64_t mk = load(0);
     uint32_t dirty = (uint32_t)(mk >> 33);
+    uint32_t carry;  // -dirty pending at the next marker's start (where this marker's literals end)
+    uint32_t rel;
     {
         const int64_t fs64 = (int64_t)pos - (int64_t)ts;
         const int64_t fe64 = fs64 + (int64_t)(uint32_t)(mk >> 1);
         const int64_t de64 = fe64 + dirty;
         auto cl = [W](int64_t v) { return (uint32_t)(v < 0 ? 0 : (v > W ? W : v)); };
         const uint32_t fs = cl(fs64), fe = cl(fe64), de = cl(de64);
-        if ((mk & 1) && fe > fs) {
-            atomicAdd(&cnt[fs], 1u);
-            atomicAdd(&cnt[fe], 0xFFFFFFFFu);
-        }
-        if (de > fe) {
-            atomicAdd(&cnt[fe], 0x10000u);
-            atomicAdd(&cnt[de], 0xFFFF0000u);
-        }
+        const uint32_t ones = ((mk & 1) && fe > fs) ? 1u : 0u;
+        const bool lit = de > fe;
+        atomicAdd(&cnt[ones ? fs : dummy], ones);
+        const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
+        atomicAdd(&cnt[at_fe ? fe : dummy], at_fe);
         if (de64 >= W) return;
-        pos = (uint32_t)de64;  // reused as the tile-relative start of the next marker
+        carry = lit ? 0xFFFF0000u : 0u;
+        rel = (uint32_t)de64;
     }
-    uint32_t rel = pos;
     uint32_t i = 1 + dirty;
-    const uint32_t dummy = Wu + 1 + (threadIdx.x & 31);
     while (i < lim) {
         mk = load(i);
         dirty = (uint32_t)(mk >> 33);
         const uint32_t run = min((uint32_t)(mk >> 1), Wu);
         const uint32_t ones = (uint32_t)(mk & 1) & (run != 0u);
-        const uint32_t fe_raw = rel + run;           // <= 2W
-        const uint32_t de_raw = fe_raw + dirty;      // < 2^32: dirty < 2^31
-        const uint32_t fe = min(fe_raw, Wu), de = min(de_raw, Wu);
+        const uint32_t fe_raw = rel + run;       // <= 2W
+        const uint32_t de_raw = fe_raw + dirty;  // < 2^32: dirty < 2^31
+        const uint32_t fe = min(fe_raw, Wu);
         const bool lit = (dirty != 0u) & (fe < Wu);
-        // branchless: an empty contribution goes to this lane's dummy slot past the tile
+        // two reductions per marker: (previous literals end | this one-fill starts) at rel,
+        // (this one-fill ends | this marker's literals start) at fe
+        const uint32_t at_rel = carry + ones;
         const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
-        atomicAdd(&cnt[ones ? rel : dummy], 1u);
+        atomicAdd(&cnt[at_rel ? rel : dummy], at_rel);
         atomicAdd(&cnt[at_fe ? fe : dummy], at_fe);
-        atomicAdd(&cnt[lit ? de : dummy], 0xFFFF0000u);
-        if (de_raw >= Wu) break;
+        carry = lit ? 0xFFFF0000u : 0u;
+        if (de_raw >= Wu) return;  // the pending literal end lies past the tile
         rel = de_raw;
         i += 1 + dirty;
     }
+    if (carry) atomicAdd(&cnt[rel], carry);  // stream ended inside the tile
 }
 
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
