@@ -120,6 +120,9 @@ BQ_API int bq_sweep_host(const uint64_t *const *h_inputs, const uint64_t *n_word
                          uint64_t *const *h_outs, unsigned long long *h_popcnts, int device,
                          uint64_t chunk_words);
 
+/* Free the device workspace and streams bq_sweep_host keeps cached per device. */
+BQ_API void bq_release_workspace(void);
+
 /* ---- run-length-compressed inputs (EWAH-style, bitmaps.py:27-40) ---------- */
 
 /* One compressed input stream on the device. */

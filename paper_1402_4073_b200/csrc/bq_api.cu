@@ -495,6 +495,23 @@ BQ_API int bq_sweep_host(const uint64_t *const *h_inputs, const uint64_t *n_word
     return BQ_OK;
 }
 
+BQ_API void bq_release_workspace(void) {
+    for (auto &ws : g_sweep) {
+        std::lock_guard<std::mutex> guard(ws.mu);
+        if (ws.dev) {
+            cudaFree(ws.dev);
+            ws.dev = nullptr;
+            ws.dev_bytes = 0;
+        }
+        if (ws.s_in) {
+            cudaStreamDestroy(ws.s_in);
+            cudaStreamDestroy(ws.s_comp);
+            cudaStreamDestroy(ws.s_out);
+            ws.s_in = ws.s_comp = ws.s_out = nullptr;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // canonical RLE encoder (RleBuilder, bitmaps.py:351-414)
 

@@ -123,12 +123,12 @@ extern "C" BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_w
         enc_flags_kernel<<<grid, threads, 0, s>>>(d_words, n_words, total, flags);
         size_t t = a_tmp;
         if ((e = cub::DeviceSelect::Flagged(tmp, t, it, flags, cp, n_cp, (int)total, s)) != cudaSuccess) break;
-        enc_sizes_kernel<<<grid, threads, 0, s>>>(d_words, n_words, total, cp, n_cp, sizes);
-        t = a_tmp;
-        if ((e = cub::DeviceScan::ExclusiveSum(tmp, t, sizes, offs, (int)total, s)) != cudaSuccess) break;
-        // encoded length = offs[n_cp - 1] + sizes[n_cp - 1]
         if ((e = cudaMemcpyAsync(&h_ncp, n_cp, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+        enc_sizes_kernel<<<grid, threads, 0, s>>>(d_words, n_words, total, cp, n_cp, sizes);
+        t = a_tmp;  // exclusive scan over exactly the n_cp change points
+        if ((e = cub::DeviceScan::ExclusiveSum(tmp, t, sizes, offs, (int)h_ncp, s)) != cudaSuccess) break;
+        // encoded length = offs[n_cp - 1] + sizes[n_cp - 1]
         uint32_t last_size = 0;
         if ((e = cudaMemcpyAsync(&h_last[0], offs + (h_ncp - 1), 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
         if ((e = cudaMemcpyAsync(&last_size, sizes + (h_ncp - 1), 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
