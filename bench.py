@@ -317,13 +317,14 @@ def run_ours(args):
         host_out = torch.empty((len(C2_TS), nw), dtype=torch.int64, pin_memory=True)
         h_out = [host_out[k].numpy().view(np.uint64) for k in range(len(C2_TS))]
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        chunk_words = (args.e2e_chunk_mib << 20) // (8 * n) if args.e2e_chunk_mib else 0
         for _ in range(max(1, min(args.warmup, 2))):
-            bq.sweep_host(h_in, r_local, list(C2_TS), outs=h_out, device=local)
+            bq.sweep_host(h_in, r_local, list(C2_TS), outs=h_out, device=local, chunk_words=chunk_words)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            _, pops = bq.sweep_host(h_in, r_local, list(C2_TS), outs=h_out, device=local)
+            _, pops = bq.sweep_host(h_in, r_local, list(C2_TS), outs=h_out, device=local, chunk_words=chunk_words)
             if world > 1:
                 pt = torch.tensor(pops, dtype=torch.int64, device=dev)
                 dist.all_reduce(pt)
@@ -630,6 +631,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--pad-words", type=int, default=256, help="row pitch padding (words) between bitmaps")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-chunk-mib", type=int, default=0, help="host streaming chunk (MiB of input; 0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
