@@ -178,6 +178,15 @@ BQ_API int bq_binary_op(int kind, const uint64_t *d_a, uint64_t na, const uint64
                         uint64_t r_bits, uint64_t *d_out, unsigned long long *d_popcnt,
                         unsigned long long *d_last_nz, void *stream);
 
+/* ---- similarity-query front end (bench/similarity.py:26-58) ---------------
+ * h_out[i * nr + j] = bit h_rids[j] of bitmap i (UncompressedBitmap.get /
+ * RleBitmap.get, bitmaps.py:107-113, :314-325); positions past a bitmap's
+ * words read 0.  The RLE form walks each stream once and needs ascending rids.
+ * Synchronous. */
+BQ_API int bq_membership(const bq_span *bitmaps, int m, const uint64_t *h_rids, int nr, uint8_t *h_out, int device);
+BQ_API int bq_rle_membership(const bq_rle_span *streams, int m, const uint64_t *h_rids, int nr, uint8_t *h_out,
+                             int device);
+
 /* ---- straight-line BitPrograms (circuits/programs.py) --------------------- */
 
 /* A reference BitProgram (programs.py:56-72) JIT-compiled for sm_100a with

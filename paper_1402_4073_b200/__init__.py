@@ -55,6 +55,7 @@ from .errors import (
     NoCoveringCircuit,
     ResourceError,
 )
+from .similarity import SimilarityQuery, make_similarity
 from .spec import SymmetricSpec
 
 __version__ = "0.1.0"

@@ -53,6 +53,8 @@ SIGNATURES = {
     "bq_rle_encode_host": (_I, [_P, _U64, _U64, _P, _U64, _P]),
     "bq_rle_encode_device": (_I, [_P, _U64, _U64, _P, _U64, _P, _P]),
     "bq_binary_op": (_I, [_I, _P, _U64, _P, _U64, _U64, _P, _P, _P, _P]),
+    "bq_membership": (_I, [_P, _I, _P, _I, _P, _I]),
+    "bq_rle_membership": (_I, [_P, _I, _P, _I, _P, _I]),
     "bq_program_compile": (_I, [_P, _I, _I, _I, _I, _P]),
     "bq_program_destroy": (None, [_P]),
     "bq_program_source": (_I, [_P, _P, _U64, _P]),

@@ -362,6 +362,26 @@ def setop_cases(rng):
     wr.save()
 
 
+def similarity_cases():
+    """bench.similarity.make_similarity on reference synthetic datasets, plus the
+    threshold answer over the resolved (replicated) inputs."""
+    from bitquorum.bench.datagen import SyntheticSpec, gen_synthetic
+    from bitquorum.bench.similarity import make_similarity
+
+    wr = Writer("similarity")
+    for process, seed, card, universe, count in [("uniform", 3, 40, 2000, 30), ("clustered", 5, 300, 4000, 40),
+                                                 ("uniform", 9, 5, 5000, 12)]:
+        ds = gen_synthetic(SyntheticSpec(process, seed, card, universe, count))
+        for rid_count, n, qseed, t in [(1, 8, 0, 2), (3, 16, 1, 3), (2, 64, 7, 5), (1, 5, 11, 1)]:
+            q = make_similarity(ds, rid_count, n, qseed)
+            exp = counters.scan_count(q.bitmaps, t)
+            wr.add([b.words for b in ds.bitmaps], [b.bit_length for b in ds.bitmaps], exp.words,
+                   {"name": ds.name, "universe": ds.universe, "rid_count": rid_count, "n": n, "seed": qseed,
+                    "t": t, "rids": q.rids, "chosen": q.source_indices, "mult": q.multiplicities,
+                    "r": max(b.bit_length for b in q.bitmaps)})
+    wr.save()
+
+
 def generator_cases():
     out = {"seed": 1402, "cases": []}
     for (i, w, q) in [(0, 0, 6554), (0, 1, 6554), (3, 12345, 6554), (7, 0, 32768), (1, 99, 3277),
@@ -410,4 +430,5 @@ if __name__ == "__main__":
     codec_cases(rng)
     program_cases(rng)
     setop_cases(rng)
+    similarity_cases()
     kat()

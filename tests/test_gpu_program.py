@@ -78,3 +78,26 @@ def test_large_program_vs_counting_kernel(bq):
     got = bq.execute(prog, dev)
     exp = O.threshold_port(arrs, 64 * nw, 32)
     assert np.array_equal(got.to_numpy(), exp)
+
+
+SIM = load_golden("similarity")
+
+
+@pytest.mark.parametrize("case", SIM, ids=lambda c: c.id)
+def test_similarity_front_end_matches_reference(bq, case):
+    """make_similarity (bench/similarity.py:26-58) with device membership, both
+    representations, then the threshold over the replicated inputs."""
+    from paper_1402_4073_b200.similarity import make_similarity
+
+    m = case.meta
+    for rle in (False, True):
+        if rle:
+            bms = [bq.compress(bq.UncompressedBitmap(a.tolist(), b)) for a, b in zip(case.inputs, case.bits)]
+        else:
+            bms = [bq.UncompressedBitmap(a.tolist(), b) for a, b in zip(case.inputs, case.bits)]
+        ds = types.SimpleNamespace(name=m["name"], universe=m["universe"], bitmaps=bms)
+        q = make_similarity(ds, m["rid_count"], m["n"], m["seed"])
+        assert q.rids == m["rids"] and q.source_indices == m["chosen"] and q.multiplicities == m["mult"]
+        got = bq.scan_count(q.bitmaps, m["t"])
+        words = bq.decompress(got).words if rle else got.words
+        assert words == case.out.tolist()
