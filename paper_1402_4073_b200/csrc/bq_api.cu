@@ -126,6 +126,7 @@ struct bq_query {
     uint64_t r_bits, w_begin, w_end, nwords, full_words, last_mask;
     const uint64_t **d_ptrs;
     uint64_t *d_lens;
+    std::vector<const uint64_t *> h_ptrs;  // host copy (small N: passed by value to the kernel)
 };
 
 extern "C" {
@@ -191,6 +192,7 @@ BQ_API int bq_query_create(const bq_span *inputs, int n, uint64_t r_bits, uint64
         delete q;
         return cuda_error(e, "cudaMemcpy(query table)");
     }
+    q->h_ptrs = ptrs;
     *out = q;
     return BQ_OK;
 }
@@ -232,6 +234,8 @@ static int base_args(bq_query *q, uint64_t *d_out, unsigned long long *d_popcnt,
     a.ptrs = q->d_ptrs;
     a.lens = q->d_lens;
     a.n = q->n;
+    if (q->n <= kSmallN)
+        for (int i = 0; i < q->n; ++i) a.small_ptrs[i] = q->h_ptrs[i];
     a.nwords = q->nwords;
     a.full_words = q->full_words;
     a.last_mask = q->last_mask;
@@ -471,6 +475,8 @@ BQ_API int bq_sweep_host(const uint64_t *const *h_inputs, const uint64_t *n_word
             memset(&a, 0, sizeof a);
             a.ptrs = d_ptrs[b];
             a.lens = d_lens + c * n;
+            if (n <= kSmallN)
+                for (int i = 0; i < n; ++i) a.small_ptrs[i] = hp[(size_t)b * n + i];
             a.n = n;
             a.nwords = cw;
             a.full_words = full[c];

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const __grid_constant__
     const uint64_t **stab = reinterpret_cast<const uint64_t **>(smem);
     uint32_t *slut = reinterpret_cast<uint32_t *>(smem + (SMEM_TABLE ? (size_t)a.n * 8 : 0));
     if (SMEM_TABLE)
-        for (int i = threadIdx.x; i < a.n; i += blockDim.x) stab[i] = a.ptrs[i];
+            for (int i = threadIdx.x; i < a.n; i += blockDim.x) stab[i] = (a.n <= kSmallN) ? a.small_ptrs[i] : a.ptrs[i];
     if (MODE == MODE_LUT) {
         const int lut_words = ((1 << M) + 31) / 32;
         for (int i = threadIdx.x; i < lut_words; i += blockDim.x) slut[i] = a.lut[i];

@@ -32,6 +32,7 @@ int sm_count();              // SMs of the current device
 constexpr int kMaxBreaks = 32;
 constexpr int kMaxCounterBits = 16;
 constexpr int kSmemTableMax = 8192;  // pointer tables up to this N live in shared memory
+constexpr int kSmallN = 16;          // pointer tables up to this N also travel in the kernel parameters
 
 enum CountMode { MODE_OR = 0, MODE_AND = 1, MODE_BREAK = 2, MODE_LUT = 3 };
 
@@ -49,6 +50,7 @@ struct CountArgs {
     int nbreak;
     uint32_t breaks[kMaxBreaks];  // output flips at each count >= breaks[b]
     const uint32_t *lut;          // MODE_LUT: bit-packed accept table, 2^m bits
+    const uint64_t *small_ptrs[kSmallN];  // n <= kSmallN: the pointer table by value (no dependent DRAM load)
 };
 
 // Launch the counting kernel for counter width m (1..16) and mode.
