@@ -91,15 +91,52 @@ def _device_for(bitmaps):
 def _dev_inputs(bitmaps, device):
     out = []
     for b in bitmaps:
-        if isinstance(b, (DeviceBitmap, DeviceRleBitmap)):
+        k = kind_of(b)
+        if k in ("du", "dr"):
             out.append(b)
-        elif isinstance(b, (UncompressedBitmap,)) or type(b).__name__ == "UncompressedBitmap":
-            t = UPLOADS.get(b, device)
-            out.append(DeviceBitmap(t, b.bit_length, t.numel()))
         else:
             t = UPLOADS.get(b, device)
-            out.append(DeviceRleBitmap(t, b.bit_length, t.numel()))
+            out.append(DeviceBitmap(t, b.bit_length, t.numel()) if k == "u" else
+                       DeviceRleBitmap(t, b.bit_length, t.numel()))
     return out
+
+
+class _QueryCache:
+    """Prepared queries (device pointer table; for RLE inputs also the K3 tile
+    directory) keyed by the identities of their input objects.  Bitmaps are
+    immutable after construction (reference bitmaps.py:12-13), so a query stays
+    valid as long as its inputs live; entries hold strong references to them so
+    ids cannot be reused.  LRU-bounded."""
+
+    def __init__(self, maxsize: int = 32):
+        from collections import OrderedDict
+        import threading
+
+        self.maxsize = maxsize
+        self._d = OrderedDict()
+        self._lock = threading.Lock()
+
+    def get(self, kind: str, bitmaps, r: int, device):
+        key = (kind, tuple(id(b) for b in bitmaps), r, device.index)
+        with self._lock:
+            hit = self._d.get(key)
+            if hit is not None and all(x is y for x, y in zip(hit[0], bitmaps)):
+                self._d.move_to_end(key)
+                return hit[1]
+        dev = _dev_inputs(bitmaps, device)
+        q = ThresholdQuery(dev, r, device=device) if kind == "u" else RleQuery(dev, r, device=device)
+        with self._lock:
+            self._d[key] = (list(bitmaps), q)
+            while len(self._d) > self.maxsize:
+                self._d.popitem(last=False)
+        return q
+
+    def clear(self):
+        with self._lock:
+            self._d.clear()
+
+
+QUERIES = _QueryCache()
 
 
 def compress_words(words, bit_length: int) -> list:
@@ -159,25 +196,21 @@ def _run(bitmaps, r, t=None, accept=None):
     if r is None:
         r = max(b.bit_length for b in bitmaps)
     device = _device_for(bitmaps)
-    dev = _dev_inputs(bitmaps, device)
+    q = QUERIES.get(kind, bitmaps, r, device)
     nw = word_count(r)
     out = torch.empty(max(nw, 2), dtype=torch.int64, device=device)
     popcnt = torch.zeros(1, dtype=torch.int64, device=device)
     last_nz = torch.zeros(1, dtype=torch.int64, device=device)
     if kind == "u":
-        q = ThresholdQuery(dev, r, device=device)
         if accept is None:
             q.threshold(t, out, popcnt, last_nz)
         else:
             q.symmetric(accept, out, popcnt, last_nz)
-        q.close()
     else:
-        q = RleQuery(dev, r, device=device)
         if accept is None:
             q.threshold(t, out, popcnt)
         else:
             q.symmetric(accept, out, popcnt)
-        q.close()
     return _finish(bitmaps, out, nw, r, popcnt, last_nz)
 
 
@@ -427,22 +460,21 @@ def execute(program, inputs: Sequence):
     _check_program_inputs(program, inputs)
     r = max(b.bit_length for b in inputs)
     device = _device_for(inputs)
-    dev = _dev_inputs(inputs, device)
-    if kind_of(inputs[0]) in ("r", "dr"):  # decode RLE inputs on the device first
-        decoded = []
-        for d in dev:
-            q = RleQuery([d], r, device=device)
-            words, _ = q.threshold(1)
-            q.close()
-            decoded.append(DeviceBitmap(words[: word_count(r)], r, word_count(r)))
-        dev = decoded
     nw = word_count(r)
     out = torch.empty(max(nw, 2), dtype=torch.int64, device=device)
     popcnt = torch.zeros(1, dtype=torch.int64, device=device)
     last_nz = torch.zeros(1, dtype=torch.int64, device=device)
-    q = ThresholdQuery(dev, r, device=device)
+    if kind_of(inputs[0]) in ("r", "dr"):  # decode RLE inputs on the device first
+        decoded = []
+        for d in _dev_inputs(inputs, device):
+            rq = RleQuery([d], r, device=device)
+            words, _ = rq.threshold(1)
+            rq.close()
+            decoded.append(DeviceBitmap(words[:nw], r, nw))
+        q = ThresholdQuery(decoded, r, device=device)
+    else:
+        q = QUERIES.get("u", inputs, r, device)
     compile_program(program).run(q, out, popcnt, last_nz)
-    q.close()
     return _finish(inputs, out, nw, r, popcnt, last_nz)
 
 

@@ -257,3 +257,18 @@ def test_all_literal_streams_overflow_pools(bq):
     out, pc = q.symmetric(acc)
     exp = O.cdom_symmetric(streams, r, acc)
     assert np.array_equal(host(out, nw), exp)
+
+
+def test_repeated_dropin_calls_reuse_the_prepared_query(bq):
+    """Immutable inputs: the second cdom call on the same objects reuses the
+    query (and its K3 directory) and returns the identical result."""
+    from paper_1402_4073_b200.api import QUERIES
+
+    case = RLE[0]
+    ins = [bq.RleBitmap(a.tolist(), b) for a, b in zip(case.inputs, case.bits)]
+    QUERIES.clear()
+    first = bq.cdom_threshold(ins, 1)
+    n_cached = len(QUERIES._d)
+    second = bq.cdom_threshold(ins, 1)
+    assert first.words == second.words
+    assert len(QUERIES._d) == n_cached == 1
