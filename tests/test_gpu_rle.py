@@ -29,6 +29,14 @@ def bq():
     return bq
 
 
+@pytest.fixture(autouse=True, params=["0", "1"], ids=["per_stream", "tile_major"])
+def rle_layout(request, monkeypatch):
+    """Run every case on both K4 layouts: the per-stream walk (BQ_RLE_TILED=0) and the
+    tile-major copy built at the first evaluation (BQ_RLE_TILED=1)."""
+    monkeypatch.setenv("BQ_RLE_TILED", request.param)
+    return request.param
+
+
 def dev(arrs):
     out = []
     for a in arrs:
@@ -272,3 +280,23 @@ def test_repeated_dropin_calls_reuse_the_prepared_query(bq):
     second = bq.cdom_threshold(ins, 1)
     assert first.words == second.words
     assert len(QUERIES._d) == n_cached == 1
+
+
+def test_tile_major_copy_is_built_at_the_second_evaluation(bq, monkeypatch):
+    """Default policy: the first evaluation walks the per-stream layout, the second
+    builds the tile-major copy (directory_bytes grows) and both agree with the oracle."""
+    monkeypatch.delenv("BQ_RLE_TILED", raising=False)
+    lib = bq._lib.load()
+    n, r = 96, 1 << 20
+    streams = [markov(lib, 77, i, r, 64.0, 900.0) for i in range(n)]
+    q = bq.RleQuery(dev(streams), r)
+    nw = r // 64
+    before = q.directory_bytes
+    for k, t in enumerate((3, 3, 7, 50)):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), (k, t)
+        assert int(pc.item()) == popcount(exp)
+        if k == 0:
+            assert q.directory_bytes == before
+    assert q.directory_bytes > before + sum(s.size for s in streams) * 8
