@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(kStagedThreads, 4) rle_tiled_kernel(const __gr
             const uintptr_t a0 = reinterpret_cast<uintptr_t>(tblock + b_lo) & ~(uintptr_t)15;
             const uintptr_t a1 = (reinterpret_cast<uintptr_t>(tblock + b_hi) + 15) & ~(uintptr_t)15;
             const uint32_t cap = (uint32_t)kPoolWords * 8;
-            const uint32_t span = (uint32_t)(a1 - a0);
+            const uint32_t span = b_hi > b_lo ? (uint32_t)(a1 - a0) : 0u;
             const uint32_t bytes = span < cap ? span : cap;
             // staged iff the segment lies inside the copied prefix of the batch range
             sg.staged = sg.len && a.debug < 2 &&
@@ -699,19 +699,18 @@ __global__ void __launch_bounds__(kStagedThreads, 4) rle_tiled_kernel(const __gr
             }
         };
         const int nk = (n + NT - 1) / NT;
-        Seg cur, nxt;
-        nxt.len = 0;
-        nxt.staged = false;
-        Pre q0, q1;
-        fetch(0, q0);
-        fetch(1, q1);
-        plan(q0, 0, cur);
-        for (int k = 0; k < nk; ++k) {
-            if (k + 1 < nk) {
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                plan(q1, k + 1, nxt);
-                fetch(k + 2, q1);
-            }
+        // Two-batch unrolled pipeline: metadata of batch k + 2 lands in `q` while batch k
+        // is walked, and the segment plans alternate between sa / sb, so no register
+        // rotation forces an early wait on the metadata loads.
+        Seg sa, sb;
+        Pre q;
+        fetch(0, q);
+        plan(q, 0, sa);
+        fetch(1, q);
+        auto step = [&](int k, Seg &cur, Seg &nxt) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            plan(q, k + 1, nxt);  // k + 1 == nk: an empty batch, arrive only
+            fetch(k + 2, q);
             wait_batch(k);
             if (cur.len && !a.debug) {
                 if (cur.staged)
@@ -720,8 +719,11 @@ __global__ void __launch_bounds__(kStagedThreads, 4) rle_tiled_kernel(const __gr
                 else
                     sweep_stream<true>(tblock + cur.off, cur.len, cur.pos, ts, width, cnt);
             }
-            __syncwarp();
-            cur = nxt;
+            __syncwarp();  // batch k's pool half may be refilled for batch k + 2
+        };
+        for (int k = 0; k < nk; k += 2) {
+            step(k, sa, sb);
+            if (k + 1 < nk) step(k + 1, sb, sa);
         }
     }
     __syncthreads();
