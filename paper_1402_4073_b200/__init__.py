@@ -55,6 +55,7 @@ from .errors import (
     NoCoveringCircuit,
     ResourceError,
 )
+from .serial import dumps_bitmap, loads_bitmap_device, read_bitmap_device, write_bitmap
 from .similarity import SimilarityQuery, make_similarity
 from .spec import SymmetricSpec
 

@@ -394,6 +394,61 @@ def generator_cases():
     return out
 
 
+def serial_cases():
+    """BQBM serialization (bitmaps.py:689-732): bytes the reference writes, and what
+    its reader does with valid and malformed payloads."""
+    import struct
+
+    rng = random.Random(1402)
+    out = {"valid": [], "invalid": []}
+    bitmaps = [bm.UncompressedBitmap.empty(0), bm.UncompressedBitmap.empty(1000),
+               bm.UncompressedBitmap.from_positions([0, 63, 64, 999], 1000),
+               bm.UncompressedBitmap([rng.getrandbits(64) for _ in range(40)], 64 * 40),
+               bm.RleBitmap.empty(0), bm.RleBitmap.empty(5000),
+               bm.compress(bm.UncompressedBitmap.from_positions(sorted(rng.sample(range(70000), 900)), 70001)),
+               bm.compress(bm.UncompressedBitmap.ones(12345))]
+    for b in bitmaps:
+        data = bm.dumps_bitmap(b)
+        back = bm.loads_bitmap(data)
+        assert back == b
+        out["valid"].append({"kind": "U" if isinstance(b, bm.UncompressedBitmap) else "R", "r": b.bit_length,
+                             "words": [str(w) for w in b.words], "hex": data.hex()})
+    hdr = struct.Struct("<4scQQ")
+    mk = lambda bit, run, dirty: bit | (run << 1) | (dirty << 33)  # noqa: E731
+
+    def raw(tag, r, words, magic=b"BQBM", count=None):
+        count = len(words) if count is None else count
+        return hdr.pack(magic, tag, r, count) + struct.pack(f"<{len(words)}Q", *words)
+
+    cases = {
+        "truncated_header": raw(b"U", 64, [])[:20],
+        "bad_magic": raw(b"U", 64, [1], magic=b"BQBX"),
+        "truncated_payload": raw(b"U", 640, [1, 2, 3], count=4),
+        "unknown_tag": raw(b"X", 64, [1]),
+        "u_bits_beyond_r": raw(b"U", 70, [1, 1 << 10]),
+        "u_too_many_words": raw(b"U", 64, [1, 2]),
+        "u_trailing_zero_words": raw(b"U", 64, [5, 0, 0]),
+        "r_truncated_literals": raw(b"R", 640, [mk(0, 1, 3), 7]),
+        "r_beyond_r": raw(b"R", 128, [mk(1, 3, 0)]),
+        "r_valid_with_trailing_literal": raw(b"R", 200, [mk(0, 1, 1), 9]),
+        "r_literal_bits_beyond_r": raw(b"R", 70, [mk(0, 1, 1), 1 << 10]),
+        "r_empty_stream": raw(b"R", 300, []),
+    }
+    for name, data in cases.items():
+        try:
+            b = bm.loads_bitmap(data)
+            out["invalid"].append({"name": name, "hex": data.hex(), "error": None,
+                                   "kind": "U" if isinstance(b, bm.UncompressedBitmap) else "R",
+                                   "r": b.bit_length, "words": [str(w) for w in b.words]})
+        except Exception as exc:  # noqa: BLE001 -- record exactly what the reference raises
+            out["invalid"].append({"name": name, "hex": data.hex(), "error": type(exc).__name__,
+                                   "message": str(exc)})
+    path = os.path.join(HERE, "serial.json")
+    with open(path, "w") as fp:
+        json.dump(out, fp, indent=1)
+    print(path)
+
+
 def kat():
     """Known-answer tests quoted in SPEC.md / PAPER.md, evaluated by the reference."""
     res = {}
@@ -431,4 +486,5 @@ if __name__ == "__main__":
     program_cases(rng)
     setop_cases(rng)
     similarity_cases()
+    serial_cases()
     kat()
