@@ -56,6 +56,50 @@ struct CountArgs {
 // Launch the counting kernel for counter width m (1..16) and mode.
 int launch_count(const CountArgs &a, int m, int mode, cudaStream_t stream);
 
+// ---- K4 over the tile-sliced RLE layout (bq_rle_sliced.cu) -------------------
+constexpr int kRleTile = 1024;        // output words per K4 tile (and directory granularity)
+constexpr uint16_t kNoSlot = 0xFFFF;  // phase C: word has no bit-counter slot
+
+#ifdef __CUDACC__
+__device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { return (bits[c >> 5] >> (c & 31)) & 1u; }
+#endif
+
+// Tile-sliced layout of n RLE streams, derived once per query from the inputs and
+// the K3 directory.  Every (tile, stream) slice -- the stream's words
+// [1024 t, 1024 t + 1024) -- is re-encoded as self-contained markers covering
+// exactly 1024 words (clipped fills, clipped literal groups, a zero fill after
+// the stream's end), stored as 32-bit markers (bit | run << 1 | dirty << 12) in
+// one array and their literal words in another, both tile-major.  Marker arrays
+// of a tile are padded to a multiple of kSliceChunk; one checkpoint per chunk
+// (word position within its slice, pending literal end, literal index) lets any
+// warp decode any chunk.
+constexpr int kSliceChunk = 128;
+struct SlicedLayout {
+    void *mem = nullptr;
+    const uint32_t *markers = nullptr;    // [sum of padded tile marker counts]
+    const uint64_t *literals = nullptr;   // [sum of tile literal counts]
+    const uint64_t *tile_mbase = nullptr; // [ntiles + 1] marker offset of each tile (multiple of kSliceChunk)
+    const uint64_t *tile_lbase = nullptr; // [ntiles + 1] literal offset of each tile
+    const uint64_t *chunk_meta = nullptr; // [markers / kSliceChunk]: rel | carry << 11 | literal index << 32
+    uint64_t bytes = 0;
+    uint64_t n_markers = 0, n_literals = 0;
+};
+int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t ntiles,
+                 SlicedLayout *out);
+void free_sliced(SlicedLayout *l);
+struct SlicedEval {
+    int n;
+    uint64_t total_words;
+    uint32_t ntiles;
+    uint64_t last_mask;
+    const uint32_t *accept_bits;
+    const uint32_t *const_until;
+    uint64_t *out;
+    unsigned long long *popcnt;
+    int debug;
+};
+int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t stream);
+
 // ---- K5 generator kernels --------------------------------------------------
 int launch_gen_rows(uint64_t seed, uint32_t first, int count, const uint32_t *d_q16s, uint64_t w0,
                     uint64_t nw, uint64_t *d_out, uint64_t pitch, cudaStream_t stream);

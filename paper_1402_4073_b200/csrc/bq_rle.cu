@@ -45,10 +45,8 @@
 
 namespace bq {
 
-constexpr int kRleTile = 1024;        // output words per K4 tile (and directory granularity)
 constexpr int kRleThreads = 256;
 constexpr int kSlotsPerBatch = 256;   // undecided words resolved per phase-C pass
-constexpr uint16_t kNoSlot = 0xFFFF;
 constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
 constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
@@ -156,7 +154,6 @@ struct RleCountArgs {
     int debug;  // experiment knob (BQ_RLE_DEBUG): 1 = skip marker walks, 2 = also skip copies
 };
 
-__device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { return (bits[c >> 5] >> (c & 31)) & 1u; }
 
 // Walk stream `st` across tile [ts, te) from its directory entry; Visit(fs, fe, bit, ds, de, lit)
 // is called for each marker whose runs intersect the tile (fill [fs,fe), dirty [ds,de) with the
@@ -847,6 +844,7 @@ struct bq_rle_query {
     uint64_t tiled_bytes = 0;
     int evals = 0;
     bool tiled_tried = false;
+    SlicedLayout sliced;  // tile-sliced layout (K4s), the default derived layout
 };
 
 // Build the tile-major copy of the streams (see tiled_len_kernel).  Failure to
@@ -1021,10 +1019,11 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     if (q->device >= 0) cudaSetDevice(q->device);
     cudaFree(q->mem);
     if (q->tiled_mem) cudaFree(q->tiled_mem);
+    free_sliced(&q->sliced);
     delete q;
 }
 
-BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) { return q ? q->dir_bytes + q->tiled_bytes : 0; }
+BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) { return q ? q->dir_bytes + q->tiled_bytes + q->sliced.bytes : 0; }
 
 static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *d_out, unsigned long long *d_popcnt,
                     void *stream) {
@@ -1080,13 +1079,32 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
             cudaFreeAsync(d_tab, s);
             return cuda_error(e, "cudaStreamSynchronize");
         }
-        rc = build_tiled(q);
+        // BQ_RLE_LAYOUT=tiled selects the tile-major stream copy instead of the slices (A/B)
+        const char *lenv = getenv("BQ_RLE_LAYOUT");
+        if (lenv && lenv[0] == 't')
+            rc = build_tiled(q);
+        else
+            rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, &q->sliced);
         if (rc) {
             cudaFreeAsync(d_tab, s);
             return rc;
         }
     }
-    if (q->tiled_mem && staged && tiled_mode) {
+    if (q->sliced.mem && staged && tiled_mode) {
+        SlicedEval se;
+        se.n = n;
+        se.total_words = q->total_words;
+        se.ntiles = q->ntiles;
+        se.last_mask = a.last_mask;
+        se.accept_bits = a.accept_bits;
+        se.const_until = a.const_until;
+        se.out = d_out;
+        se.popcnt = d_popcnt;
+        se.debug = a.debug;
+        rc = launch_sliced(q->sliced, se, s);
+        cudaFreeAsync(d_tab, s);
+        return rc;
+    } else if (q->tiled_mem && staged && tiled_mode) {
         RleTiledArgs b;
         b.block = q->d_block;
         b.tile_base = q->d_tile_base;

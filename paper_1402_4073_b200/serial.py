@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import io
 import os
+import re
 import struct
 
 import numpy as np
@@ -112,8 +113,7 @@ def read_bitmap_device(fp, device=None):
     try:
         RleQuery([bm], bit_length)  # K3 walks the markers: the reference's decompress() validation
     except FormatError as exc:
-        msg = str(exc)
-        raise FormatError(msg.split(": ", 1)[1] if msg.startswith("stream ") and ": " in msg else msg) from None
+        raise FormatError(re.sub(r"^.*?stream \d+: ", "", str(exc))) from None  # the reference's bare message
     return bm
 
 
