@@ -142,11 +142,11 @@ typedef struct bq_rle_query bq_rle_query;
 BQ_API int bq_rle_query_create(const bq_rle_span *streams, int n, uint64_t r_bits, int device,
                                bq_rle_query **out);
 BQ_API void bq_rle_query_destroy(bq_rle_query *q);
-/* Device bytes the query owns: the directory plus, once built, the tile-major
- * copy of the streams (the segments every 1024-word tile reads, stored
- * contiguously per tile).  That copy is made at the second evaluation of a
- * query (BQ_RLE_TILED: 0 never, 1 at the first evaluation); it trades about
- * the compressed input size in HBM for one bulk copy per 32 streams. */
+/* Device bytes the query owns: the directory plus, once built, the tile-sliced
+ * layout (every 1024-word slice of every stream re-encoded as 32-bit markers
+ * covering exactly that slice, literal words apart, tile-major; K4s decodes it
+ * with warp prefix sums).  The layout is built at the second evaluation of a
+ * query (BQ_RLE_SLICED: 0 never, 1 at the first evaluation). */
 BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q);
 
 /* Threshold / symmetric function over the compressed inputs, output

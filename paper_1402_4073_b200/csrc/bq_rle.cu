@@ -39,8 +39,6 @@
 #include <algorithm>
 #include <vector>
 
-#include <cub/device/device_scan.cuh>
-
 #include "bq_internal.h"
 
 namespace bq {
@@ -508,320 +506,6 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
     if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
 }
 
-// ===========================================================================
-// Tile-major layout (built once per query object, like the directory).
-//
-// For every 1024-word tile t the segments of all N streams -- from the
-// directory marker to the marker covering the next tile boundary, exactly
-// what K4 reads for that tile -- are stored back to back in one HBM block:
-//   block[tile_base[t] + seg_off[t][s] ...]   (seg_off[t][n] = block length)
-// so the 32 segments a warp walks are one contiguous range: ONE TMA bulk copy
-// per warp-batch instead of one per stream, no per-lane prefix sums, and
-// strictly sequential DRAM traffic.  Consecutive segments of a stream share
-// one marker word, so the block is the compressed input plus ~1 word per
-// (stream, tile).
-
-__global__ void tiled_len_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
-                                 uint32_t ntiles, uint64_t *len_out, uint32_t *pos_out) {
-    const uint64_t total = (uint64_t)ntiles * (n + 1);
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = (uint32_t)(k / (n + 1));
-        const int s = (int)(k % (n + 1));
-        uint64_t len = 0;
-        uint32_t pos = 0;
-        if (s < n) {
-            const uint64_t L = lens[s];
-            const uint2 e = dir[(size_t)t * n + s];
-            if (e.x < L) {
-                uint64_t end = L;
-                if (t + 1 < ntiles) {
-                    // through the marker covering the next tile boundary, plus those of its
-                    // literals that still lie inside this tile (phase C reads them)
-                    const uint2 f = dir[(size_t)(t + 1) * n + s];
-                    if (f.x < L) {
-                        const uint64_t mk = __ldg(ptrs[s] + f.x);
-                        const uint64_t ds = (uint64_t)f.y + ((mk >> 1) & 0xFFFFFFFFull);
-                        const uint64_t te = (uint64_t)(t + 1) * kRleTile;
-                        const uint64_t lits = ds < te ? min(te - ds, mk >> 33) : 0;
-                        end = min((uint64_t)f.x + 1 + lits, L);
-                    }
-                }
-                len = end - e.x;
-                pos = e.y;
-            }
-        }
-        len_out[k] = len;
-        pos_out[k] = pos;
-    }
-}
-
-// offs: exclusive scan of the lengths (global word offsets); one warp per segment copies it.
-__global__ void tiled_copy_kernel(const uint64_t *const *ptrs, const uint2 *dir, int n, uint32_t ntiles,
-                                  const uint64_t *offs, uint64_t *block, uint64_t *tile_base, uint32_t *seg_off) {
-    const uint64_t total = (uint64_t)ntiles * (n + 1);
-    const int lane = threadIdx.x & 31;
-    for (uint64_t k = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < total;
-         k += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t t = (uint32_t)(k / (n + 1));
-        const int s = (int)(k % (n + 1));
-        const uint64_t base = offs[(uint64_t)t * (n + 1)];
-        if (lane == 0) {
-            seg_off[k] = (uint32_t)(offs[k] - base);
-            if (s == 0) tile_base[t] = base;
-        }
-        if (s == n) continue;
-        const uint64_t len = offs[k + 1] - offs[k];
-        if (!len) continue;
-        const uint64_t *src = ptrs[s] + dir[(size_t)t * n + s].x;
-        uint64_t *dst = block + offs[k];
-        for (uint64_t j = lane; j < len; j += 32) dst[j] = __ldg(src + j);
-    }
-}
-
-struct RleTiledArgs {
-    const uint64_t *block;      // tile-major segments (16 bytes of padding either side)
-    const uint64_t *tile_base;  // [ntiles]
-    const uint32_t *seg_off;    // [ntiles][n + 1] word offsets within the tile block
-    const uint32_t *seg_pos;    // [ntiles][n + 1] word position where the segment's first marker's fill starts
-    int n;
-    uint64_t total_words;
-    uint32_t ntiles;
-    uint64_t last_mask;
-    const uint32_t *accept_bits;
-    const uint32_t *const_until;
-    uint64_t *out;
-    unsigned long long *popcnt;
-    int debug;
-};
-
-// K4 over the tile-major layout: one CTA (4 warps) per 1024-word tile; a warp-batch
-// is 32 consecutive streams whose segments are contiguous in the block.
-__global__ void __launch_bounds__(kStagedThreads, 4) rle_tiled_kernel(const __grid_constant__ RleTiledArgs a) {
-    constexpr int NT = kStagedThreads;
-    constexpr int kSlots = kSlotsPerBatch;
-    extern __shared__ __align__(16) uint8_t rle_smem[];
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);
-    uint8_t *region = rle_smem + kCntBytes;
-    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);
-    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + kSlots * 128);
-    uint16_t *undecided = slot_of + kRleTile;
-    uint16_t *slot_word = undecided + kRleTile;
-    __shared__ uint32_t n_undecided;
-    __shared__ uint32_t warp_sums[NT / 32];
-
-    const uint32_t tile = blockIdx.x;
-    const uint64_t ts = (uint64_t)tile * kRleTile;
-    const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
-    const int width = (int)(te - ts);
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int n = a.n;
-    const uint32_t *toff = a.seg_off + (size_t)tile * (n + 1);
-    const uint32_t *tpos = a.seg_pos + (size_t)tile * (n + 1);
-    const uint64_t *tblock = a.block + a.tile_base[tile];
-
-    for (int k = tid; k <= kRleTile; k += NT) cnt[k] = 0u;
-    if (tid == 0) n_undecided = 0;
-    __syncthreads();
-
-    // ---- A: one bulk copy per warp-batch, then a marker walk per lane ----------
-    {
-        uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * 2 * kPoolWords;
-        uint64_t *bars = reinterpret_cast<uint64_t *>(cnt + kRleTile + 36) + warp * 2;
-        const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
-        if (lane == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        }
-        __syncwarp();
-        struct Pre {
-            uint32_t off, pos, end;  // this lane's segment [off, end) in the tile block; end of the batch in lane 31
-        };
-        auto fetch = [&](int k, Pre &q) {
-            const int s = k * NT + warp * 32 + lane;
-            const int sc = min(s, n);
-            q.off = toff[sc];
-            q.pos = tpos[sc];
-            q.end = (lane == 31) ? toff[min(s + 1, n)] : 0u;
-        };
-        struct Seg {
-            uint32_t off, len, pos;
-            bool staged;
-        };
-        auto plan = [&](const Pre &q, int k, Seg &sg) {
-            const uint32_t nxt = __shfl_down_sync(0xffffffffu, q.off, 1);
-            const uint32_t end = (lane == 31) ? q.end : nxt;
-            sg.off = q.off;
-            sg.len = end - q.off;
-            sg.pos = q.pos;
-            const uint32_t b_lo = __shfl_sync(0xffffffffu, q.off, 0), b_hi = __shfl_sync(0xffffffffu, q.end, 31);
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(tblock + b_lo) & ~(uintptr_t)15;
-            const uintptr_t a1 = (reinterpret_cast<uintptr_t>(tblock + b_hi) + 15) & ~(uintptr_t)15;
-            const uint32_t cap = (uint32_t)kPoolWords * 8;
-            const uint32_t span = b_hi > b_lo ? (uint32_t)(a1 - a0) : 0u;
-            const uint32_t bytes = span < cap ? span : cap;
-            // staged iff the segment lies inside the copied prefix of the batch range
-            sg.staged = sg.len && a.debug < 2 &&
-                        reinterpret_cast<uintptr_t>(tblock + end) <= a0 + bytes;
-            sg.off = (uint32_t)((reinterpret_cast<uintptr_t>(tblock + q.off) - a0) / 8);  // pool index if staged
-            if (!sg.staged) sg.off = q.off;                                                // block index otherwise
-            if (lane == 0) {
-                const uint32_t bar = bar0 + 8 * (k & 1);
-                if (bytes && a.debug < 2) {
-                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pool + (size_t)(k & 1) * kPoolWords);
-                    asm volatile(
-                        "{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
-                        "r"(bytes)
-                        : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-                        "l"(a0), "r"(bytes), "r"(bar)
-                        : "memory");
-                } else {
-                    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
-                }
-            }
-        };
-        auto wait_batch = [&](int k) {
-            const uint32_t bar = bar0 + 8 * (k & 1);
-            const uint32_t parity = (uint32_t)((k >> 1) & 1);
-            uint32_t done = 0;
-            while (!done) {
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-                    : "=r"(done)
-                    : "r"(bar), "r"(parity)
-                    : "memory");
-            }
-        };
-        const int nk = (n + NT - 1) / NT;
-        // Two-batch unrolled pipeline: metadata of batch k + 2 lands in `q` while batch k
-        // is walked, and the segment plans alternate between sa / sb, so no register
-        // rotation forces an early wait on the metadata loads.
-        Seg sa, sb;
-        Pre q;
-        fetch(0, q);
-        plan(q, 0, sa);
-        fetch(1, q);
-        auto step = [&](int k, Seg &cur, Seg &nxt) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            plan(q, k + 1, nxt);  // k + 1 == nk: an empty batch, arrive only
-            fetch(k + 2, q);
-            wait_batch(k);
-            if (cur.len && !a.debug) {
-                if (cur.staged)
-                    sweep_stream<false>(pool + (size_t)(k & 1) * kPoolWords + cur.off, cur.len, cur.pos, ts, width,
-                                        cnt);
-                else
-                    sweep_stream<true>(tblock + cur.off, cur.len, cur.pos, ts, width, cnt);
-            }
-            __syncwarp();  // batch k's pool half may be refilled for batch k + 2
-        };
-        for (int k = 0; k < nk; k += 2) {
-            step(k, sa, sb);
-            if (k + 1 < nk) step(k + 1, sb, sa);
-        }
-    }
-    __syncthreads();
-
-    // ---- inclusive prefix scan of cnt[0..kRleTile) ------------------------------
-    constexpr int kPer = kRleTile / NT;
-    uint32_t local[kPer];
-    uint32_t run_sum = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        run_sum += cnt[tid * kPer + k];
-        local[k] = run_sum;
-    }
-    uint32_t incl = run_sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) warp_sums[warp] = incl;
-    __syncthreads();
-    uint32_t warp_off = 0;
-    for (int w = 0; w < warp; ++w) warp_off += warp_sums[w];
-    const uint32_t excl = warp_off + incl - run_sum;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) cnt[tid * kPer + k] = local[k] + excl;
-    for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
-    __syncthreads();
-
-    // ---- B: decide from (k, d) ----------------------------------------------
-    unsigned long long pc = 0;
-    for (int k = tid; k < width; k += NT) {
-        const uint32_t c = cnt[k];
-        const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
-        if (ones + dirty <= __ldg(a.const_until + ones)) {
-            uint64_t w = accept_at(a.accept_bits, ones) ? ~0ull : 0ull;
-            if (ts + k == a.total_words - 1) w &= a.last_mask;
-            a.out[ts + k] = w;
-            pc += __popcll(w);
-        } else {
-            undecided[atomicAdd(&n_undecided, 1u)] = (uint16_t)k;
-        }
-    }
-    __syncthreads();
-    const uint32_t nu = n_undecided;
-
-    // ---- C: literals of undecided words, read from the tile block ---------------
-    for (uint32_t base = 0; base < nu; base += kSlots) {
-        const uint32_t nb = min((uint32_t)kSlots, nu - base);
-        for (uint32_t u = tid; u < nb; u += NT) {
-            const uint16_t wk = undecided[base + u];
-            slot_word[u] = wk;
-            slot_of[wk] = (uint16_t)u;
-        }
-        for (int k = tid; k < kSlots * 32; k += NT) (&bitcnt[0][0])[k] = 0u;
-        __syncthreads();
-        for (int st = tid; st < n; st += NT) {
-            const uint64_t *src = tblock + toff[st];
-            const uint64_t lim = toff[st + 1] - toff[st];
-            uint64_t i = 0, pos = tpos[st];
-            while (i < lim && pos < te) {
-                const uint64_t mk = __ldg(src + i);
-                const uint64_t run = (mk >> 1) & 0xFFFFFFFFull, dirty = mk >> 33;
-                const uint64_t ds = pos + run, de = ds + dirty;
-                const uint64_t lo = max(ds, ts), hi = min(de, te);
-                for (uint64_t p = lo; p < hi; ++p) {
-                    const uint16_t u = slot_of[p - ts];
-                    if (u == kNoSlot || i + 1 + (p - ds) >= lim) continue;
-                    uint64_t x = __ldg(src + i + 1 + (p - ds));
-                    while (x) {
-                        const int b = __ffsll((long long)x) - 1;
-                        atomicAdd(&bitcnt[u][b & 31], (b < 32) ? 1u : 0x10000u);
-                        x &= x - 1;
-                    }
-                }
-                pos = de;
-                i += 1 + dirty;
-            }
-        }
-        __syncthreads();
-        for (uint32_t u = tid; u < nb; u += NT) {
-            const uint16_t wk = slot_word[u];
-            const uint32_t ones = cnt[wk] & 0xFFFFu;
-            uint64_t w = 0;
-            for (int b = 0; b < 64; ++b) {
-                const uint32_t cb = (bitcnt[u][b & 31] >> ((b >> 5) * 16)) & 0xFFFFu;
-                if (accept_at(a.accept_bits, ones + cb)) w |= 1ull << b;
-            }
-            if (ts + wk == a.total_words - 1) w &= a.last_mask;
-            a.out[ts + wk] = w;
-            pc += __popcll(w);
-            slot_of[wk] = kNoSlot;
-        }
-        __syncthreads();
-    }
-
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
-    if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
-}
-
 }  // namespace bq
 
 using namespace bq;
@@ -836,91 +520,10 @@ struct bq_rle_query {
     uint64_t *d_lens;
     uint2 *d_dir;
     uint64_t dir_bytes;
-    // tile-major layout (null when disabled or when it did not fit in HBM)
-    void *tiled_mem = nullptr;
-    const uint64_t *d_block = nullptr;
-    const uint64_t *d_tile_base = nullptr;
-    const uint32_t *d_seg_off = nullptr, *d_seg_pos = nullptr;
-    uint64_t tiled_bytes = 0;
     int evals = 0;
-    bool tiled_tried = false;
+    bool sliced_tried = false;
     SlicedLayout sliced;  // tile-sliced layout (K4s), the default derived layout
 };
-
-// Build the tile-major copy of the streams (see tiled_len_kernel).  Failure to
-// allocate leaves the query on the per-stream layout; other errors are reported.
-static int build_tiled(bq_rle_query *q) {
-    const int n = q->n;
-    const uint64_t cells = (uint64_t)q->ntiles * (n + 1);
-    uint64_t *d_len = nullptr, *d_offs = nullptr;
-    void *d_tmp = nullptr;
-    size_t tmp_bytes = 0;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                                  (int64_t)(cells + 1));
-    if (e != cudaSuccess) return cuda_error(e, "DeviceScan sizing");
-    const size_t meta = (size_t)cells * 8 * 2 + 16 + tmp_bytes + 256;
-    char *scratch = nullptr;
-    e = cudaMalloc(&scratch, meta);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return BQ_OK;
-    }
-    d_len = reinterpret_cast<uint64_t *>(scratch);
-    d_offs = d_len + cells + 1;
-    d_tmp = reinterpret_cast<char *>(d_offs + cells + 1);
-    // seg_pos is produced by the length pass; keep it in the final allocation's place later
-    uint32_t *d_pos_tmp = nullptr;
-    e = cudaMalloc(&d_pos_tmp, (size_t)cells * 4);
-    const unsigned grid = (unsigned)std::min<uint64_t>((cells + 255) / 256, (uint64_t)sm_count() * 16);
-    if (e == cudaSuccess) {
-        tiled_len_kernel<<<grid, 256>>>(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, d_len, d_pos_tmp);
-        e = cudaMemset(d_len + cells, 0, 8);
-    }
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_len, d_offs, (int64_t)(cells + 1));
-    uint64_t total = 0;
-    if (e == cudaSuccess) e = cudaMemcpy(&total, d_offs + cells, 8, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) {
-        cudaFree(scratch);
-        cudaFree(d_pos_tmp);
-        return cuda_error(e, "tiled layout lengths");
-    }
-    // block (16 bytes of padding either side) | tile_base | seg_off | seg_pos
-    const size_t bb = (size_t)total * 8 + 64;
-    const size_t bytes = bb + (size_t)q->ntiles * 8 + (size_t)cells * 8 + 64;
-    char *m = nullptr;
-    e = cudaMalloc(&m, bytes);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(scratch);
-        cudaFree(d_pos_tmp);
-        return BQ_OK;
-    }
-    uint64_t *block = reinterpret_cast<uint64_t *>(m + 16);
-    uint64_t *tile_base = reinterpret_cast<uint64_t *>(m + bb);
-    uint32_t *seg_off = reinterpret_cast<uint32_t *>(tile_base + q->ntiles);
-    uint32_t *seg_pos = seg_off + cells;
-    e = cudaMemsetAsync(m, 0, bb);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(seg_pos, d_pos_tmp, (size_t)cells * 4, cudaMemcpyDeviceToDevice);
-    if (e == cudaSuccess) {
-        const unsigned g2 = (unsigned)std::min<uint64_t>((cells + 7) / 8, (uint64_t)sm_count() * 32);
-        tiled_copy_kernel<<<g2, 256>>>(q->d_ptrs, q->d_dir, n, q->ntiles, d_offs, block, tile_base, seg_off);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    cudaFree(scratch);
-    cudaFree(d_pos_tmp);
-    if (e != cudaSuccess) {
-        cudaFree(m);
-        return cuda_error(e, "tiled layout copy");
-    }
-    q->tiled_mem = m;
-    q->d_block = block;
-    q->d_tile_base = tile_base;
-    q->d_seg_off = seg_off;
-    q->d_seg_pos = seg_pos;
-    q->tiled_bytes = bytes;
-    return BQ_OK;
-}
 
 extern "C" {
 
@@ -1018,12 +621,11 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     if (!q) return;
     if (q->device >= 0) cudaSetDevice(q->device);
     cudaFree(q->mem);
-    if (q->tiled_mem) cudaFree(q->tiled_mem);
     free_sliced(&q->sliced);
     delete q;
 }
 
-BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) { return q ? q->dir_bytes + q->tiled_bytes + q->sliced.bytes : 0; }
+BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) { return q ? q->dir_bytes + q->sliced.bytes : 0; }
 
 static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *d_out, unsigned long long *d_popcnt,
                     void *stream) {
@@ -1066,31 +668,26 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     const size_t smem = rle_smem_bytes(staged, n);
     static const char *dbg = getenv("BQ_RLE_DEBUG");
     a.debug = dbg ? atoi(dbg) : 0;
-    // Tile-major layout policy (BQ_RLE_TILED): "0" never; "1" build at the first
+    // Tile-sliced layout policy (BQ_RLE_SLICED): "0" never; "1" build at the first
     // evaluation; default: build at the second one, so a one-shot query does not pay
-    // the copy and a reused query (cache hit, several thresholds) gets the fast kernel.
-    const char *tenv = getenv("BQ_RLE_TILED");
-    const int tiled_mode = tenv ? atoi(tenv) : 2;
+    // the re-encoding and a reused query (cache hit, several thresholds) gets K4s.
+    const char *tenv = getenv("BQ_RLE_SLICED");
+    const int sliced_mode = tenv ? atoi(tenv) : 2;
     ++q->evals;
-    if (staged && tiled_mode && !q->tiled_tried && q->evals >= tiled_mode) {
-        q->tiled_tried = true;
+    if (staged && sliced_mode && !q->sliced_tried && q->evals >= sliced_mode) {
+        q->sliced_tried = true;
         e = cudaStreamSynchronize(s);  // the build runs on the legacy stream
         if (e != cudaSuccess) {
             cudaFreeAsync(d_tab, s);
             return cuda_error(e, "cudaStreamSynchronize");
         }
-        // BQ_RLE_LAYOUT=tiled selects the tile-major stream copy instead of the slices (A/B)
-        const char *lenv = getenv("BQ_RLE_LAYOUT");
-        if (lenv && lenv[0] == 't')
-            rc = build_tiled(q);
-        else
-            rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, &q->sliced);
+        rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, &q->sliced);
         if (rc) {
             cudaFreeAsync(d_tab, s);
             return rc;
         }
     }
-    if (q->sliced.mem && staged && tiled_mode) {
+    if (q->sliced.mem && staged && sliced_mode) {
         SlicedEval se;
         se.n = n;
         se.total_words = q->total_words;
@@ -1104,23 +701,6 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         rc = launch_sliced(q->sliced, se, s);
         cudaFreeAsync(d_tab, s);
         return rc;
-    } else if (q->tiled_mem && staged && tiled_mode) {
-        RleTiledArgs b;
-        b.block = q->d_block;
-        b.tile_base = q->d_tile_base;
-        b.seg_off = q->d_seg_off;
-        b.seg_pos = q->d_seg_pos;
-        b.n = n;
-        b.total_words = q->total_words;
-        b.ntiles = q->ntiles;
-        b.last_mask = a.last_mask;
-        b.accept_bits = a.accept_bits;
-        b.const_until = a.const_until;
-        b.out = d_out;
-        b.popcnt = d_popcnt;
-        b.debug = a.debug;
-        e = cudaFuncSetAttribute(rle_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) rle_tiled_kernel<<<q->ntiles, kStagedThreads, smem, s>>>(b);
     } else if (staged) {
         e = cudaFuncSetAttribute(rle_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) rle_count_kernel<true><<<q->ntiles, kStagedThreads, smem, s>>>(a);

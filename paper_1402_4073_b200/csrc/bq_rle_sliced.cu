@@ -29,10 +29,17 @@ namespace bq {
 
 namespace {
 
-constexpr int kSlNT = 128;                                 // K4s threads per CTA (4 warps)
+#ifndef BQ_SL_NT
+#define BQ_SL_NT 128
+#define BQ_SL_MINB 5
+#endif
+#ifndef BQ_SL_SLOTS
+#define BQ_SL_SLOTS 256
+#endif
+constexpr int kSlNT = BQ_SL_NT;                            // K4s threads per CTA (4 warps)
 constexpr int kPieceChunks = 32;                           // chunks per staged piece
 constexpr int kPieceMarkers = kPieceChunks * kSliceChunk;  // 4096 markers = 16 KB
-constexpr int kSlSlots = 256;                              // undecided words per phase-C pass
+constexpr int kSlSlots = BQ_SL_SLOTS;                      // undecided words per phase-C pass
 constexpr size_t kSlCntBytes = (size_t)(kRleTile + 36) * 4;  // + sentinel + 32 per-lane dummies (+ pad)
 constexpr size_t kSlBufBytes = 2 * (size_t)kPieceMarkers * 4;
 constexpr size_t kSlPhaseC = (size_t)kSlSlots * 128 + (size_t)kRleTile * 4 + (size_t)kSlSlots * 2;
@@ -203,7 +210,7 @@ __device__ __forceinline__ void decode_chunk(const uint4 v, uint32_t cm, int lan
     }
 }
 
-__global__ void __launch_bounds__(kSlNT, 5) rle_sliced_kernel(const __grid_constant__ SlArgs a) {
+__global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __grid_constant__ SlArgs a) {
     constexpr int NT = kSlNT;
     extern __shared__ __align__(128) uint8_t sl_smem[];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(sl_smem);
@@ -216,6 +223,7 @@ __global__ void __launch_bounds__(kSlNT, 5) rle_sliced_kernel(const __grid_const
     uint16_t *slot_word = undecided + kRleTile;
     __shared__ uint32_t n_undecided;
     __shared__ uint32_t warp_sums[NT / 32];
+    __shared__ uint32_t warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
     const uint32_t tile = blockIdx.x;
@@ -310,13 +318,27 @@ __global__ void __launch_bounds__(kSlNT, 5) rle_sliced_kernel(const __grid_const
     uint32_t warp_off = 0;
     for (int w = 0; w < warp; ++w) warp_off += warp_sums[w];
     const uint32_t excl = warp_off + incl - run_sum;
+    uint32_t reach = 0;  // max over this thread's words of ones + dirty (the largest count they can reach)
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) cnt[tid * kPer + k] = local[k] + excl;
-    for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
+    for (int k = 0; k < kPer; ++k) {
+        const uint32_t c = local[k] + excl;
+        cnt[tid * kPer + k] = c;
+        reach = max(reach, (c & 0xFFFFu) + (c >> 16));
+    }
+    reach = __reduce_max_sync(0xffffffffu, reach);
+    if (lane == 0) warp_reach[warp] = reach;
     __syncthreads();
+    for (int w = 0; w < NT / 32; ++w) reach = max(reach, warp_reach[w]);
 
     // ---- B: decide from (ones, dirty) ------------------------------------------
     unsigned long long pc = 0;
+    if (reach <= __ldg(E.const_until) && width == kRleTile && ts + kRleTile < E.total_words) {
+        // no word can leave the accept value of count 0: the tile is constant
+        const uint64_t w = accept_at(E.accept_bits, 0u) ? ~0ull : 0ull;
+        ulonglong2 *o = reinterpret_cast<ulonglong2 *>(E.out + ts);
+        for (int k = tid; k < kRleTile / 2; k += NT) o[k] = make_ulonglong2(w, w);
+        pc = w ? (unsigned long long)(kRleTile / NT) * 64 : 0ull;
+    } else {
     for (int k = tid; k < width; k += NT) {
         const uint32_t c = cnt[k];
         const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
@@ -329,8 +351,13 @@ __global__ void __launch_bounds__(kSlNT, 5) rle_sliced_kernel(const __grid_const
             undecided[atomicAdd(&n_undecided, 1u)] = (uint16_t)k;
         }
     }
+    }
     __syncthreads();
     const uint32_t nu = n_undecided;
+    if (nu) {
+        for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
+        __syncthreads();
+    }
 
     // ---- C: literal bits of undecided words ----------------------------------------
     for (uint32_t base = 0; base < nu; base += kSlSlots) {

@@ -31,9 +31,9 @@ def bq():
 
 @pytest.fixture(autouse=True, params=["0", "1"], ids=["per_stream", "sliced"])
 def rle_layout(request, monkeypatch):
-    """Run every case on both K4 paths: the per-stream walk (BQ_RLE_TILED=0) and the
-    tile-sliced layout built at the first evaluation (BQ_RLE_TILED=1)."""
-    monkeypatch.setenv("BQ_RLE_TILED", request.param)
+    """Run every case on both K4 paths: the per-stream walk (BQ_RLE_SLICED=0) and the
+    tile-sliced layout built at the first evaluation (BQ_RLE_SLICED=1)."""
+    monkeypatch.setenv("BQ_RLE_SLICED", request.param)
     return request.param
 
 
@@ -285,7 +285,7 @@ def test_repeated_dropin_calls_reuse_the_prepared_query(bq):
 def test_sliced_layout_is_built_at_the_second_evaluation(bq, monkeypatch):
     """Default policy: the first evaluation walks the per-stream layout, the second
     builds the tile-sliced layout (directory_bytes grows) and both agree with the oracle."""
-    monkeypatch.delenv("BQ_RLE_TILED", raising=False)
+    monkeypatch.delenv("BQ_RLE_SLICED", raising=False)
     lib = bq._lib.load()
     n, r = 96, 1 << 20
     streams = [markov(lib, 77, i, r, 64.0, 900.0) for i in range(n)]
@@ -300,3 +300,21 @@ def test_sliced_layout_is_built_at_the_second_evaluation(bq, monkeypatch):
         if k == 0:
             assert q.directory_bytes == before
     assert q.directory_bytes > before
+
+
+@pytest.mark.parametrize("acc_kind", ["zero_accepted", "zero_rejected"])
+def test_constant_tiles_of_sparse_streams(bq, acc_kind):
+    """Sparse streams leave whole tiles with no word able to change the count-0
+    answer (the constant-tile path of phase B); with count 0 accepted those tiles
+    are all ones.  Ragged r so the last, partial tile takes the general path."""
+    lib = bq._lib.load()
+    n, r = 24, (1 << 21) + 77
+    streams = [markov(lib, 5, i, r, 40.0, 60000.0) for i in range(n)]
+    acc = [(k == 0 or k >= 3) if acc_kind == "zero_accepted" else (k in (2, 5)) for k in range(n + 1)]
+    q = bq.RleQuery(dev(streams), r)
+    nw = (r + 63) // 64
+    for _ in range(2):  # per-stream path, then the sliced layout
+        out, pc = q.symmetric(acc)
+        exp = O.cdom_symmetric(streams, r, acc)
+        assert np.array_equal(host(out, nw), exp)
+        assert int(pc.item()) == popcount(exp)
