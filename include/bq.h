@@ -148,6 +148,10 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q);
  * with warp prefix sums).  The layout is built at the second evaluation of a
  * query (BQ_RLE_SLICED: 0 never, 1 at the first evaluation). */
 BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q);
+/* Size of the tile-sliced layout once built (0, 0 before): 32-bit markers and
+ * 64-bit literal words.  K4s reads every marker once per evaluation and
+ * literals only at undecided words (bench.py's roofline uses these). */
+BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals);
 
 /* Threshold / symmetric function over the compressed inputs, output
  * uncompressed (ceil(r/64) words).  Replaces runmerge.cdom_threshold

@@ -627,6 +627,13 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
 
 BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) { return q ? q->dir_bytes + q->sliced.bytes : 0; }
 
+BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals) {
+    if (!q || !n_markers || !n_literals) return set_error(BQ_EINPUT, "NULL argument");
+    *n_markers = q->sliced.n_markers;
+    *n_literals = q->sliced.n_literals;
+    return BQ_OK;
+}
+
 static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *d_out, unsigned long long *d_popcnt,
                     void *stream) {
     if (!q) return set_error(BQ_EINPUT, "query is NULL");

@@ -210,6 +210,14 @@ class RleQuery:
     def directory_bytes(self) -> int:
         return int(self._lib.bq_rle_query_directory_bytes(self._h))
 
+    @property
+    def layout_stats(self) -> tuple:
+        """(markers, literal words) of the tile-sliced layout; (0, 0) until it is built."""
+        m, l = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _lib.check(self._lib.bq_rle_query_layout_stats(self._h, ctypes.byref(m), ctypes.byref(l)),
+                   "bq_rle_query_layout_stats")
+        return int(m.value), int(l.value)
+
     def _outs(self, out, popcnt):
         if out is None:
             out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)
