@@ -418,6 +418,8 @@ def _line(workload, value, per_launch_ms, algo_bytes, steps, warmup, config, ext
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": ncu_traffic(traffic_key or workload),
                          "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": round(mean_ms, 5),
+                         "median_launch_ms": round(statistics.median(per_launch_ms), 5),
+                         "min_launch_ms": round(min(per_launch_ms), 5),
                          "peak_source": peak_src},
             "gpu_launches": len(per_launch_ms)}
     if extra:

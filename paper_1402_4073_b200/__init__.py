@@ -27,6 +27,7 @@ from .api import (
     cdom_symmetric,
     cdom_threshold,
     compress,
+    compress_device,
     compress_words,
     counter_width,
     csv_op_count,
@@ -56,7 +57,7 @@ from .errors import (
     ResourceError,
 )
 from .serial import dumps_bitmap, loads_bitmap_device, read_bitmap_device, write_bitmap
-from .similarity import SimilarityQuery, make_similarity
+from .similarity import DeviceDataset, SimilarityQuery, make_similarity
 from .spec import SymmetricSpec
 
 __version__ = "0.1.0"

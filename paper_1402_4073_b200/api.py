@@ -154,9 +154,8 @@ def compress_words(words, bit_length: int) -> list:
     return out[: n_out.value].tolist()
 
 
-def encode_device(words: torch.Tensor, bit_length: int) -> np.ndarray:
-    """Canonical RLE encoding (RleBuilder, bitmaps.py:351-414) of device words,
-    computed on the GPU (bq_rle_encode_device); returns the host stream."""
+def _encode_on_device(words: torch.Tensor, bit_length: int):
+    """K7 (bq_rle_encode_device): canonical stream of device words -> (device buffer, length)."""
     lib = _lib.load()
     nw = word_count(bit_length)
     cap = nw + 2
@@ -165,7 +164,27 @@ def encode_device(words: torch.Tensor, bit_length: int) -> np.ndarray:
     _lib.check(lib.bq_rle_encode_device(words.data_ptr() if words.numel() else None, min(words.numel(), nw),
                                         bit_length, dout.data_ptr(), cap, ctypes.byref(n_out),
                                         torch.cuda.current_stream(words.device).cuda_stream), "bq_rle_encode_device")
-    return dout[: n_out.value].cpu().numpy().view(np.uint64)
+    return dout, int(n_out.value)
+
+
+def encode_device(words: torch.Tensor, bit_length: int) -> np.ndarray:
+    """Canonical RLE encoding (RleBuilder, bitmaps.py:351-414) of device words,
+    computed on the GPU (bq_rle_encode_device); returns the host stream."""
+    dout, n = _encode_on_device(words, bit_length)
+    return dout[:n].cpu().numpy().view(np.uint64)
+
+
+def compress_device(bitmap, device=None) -> DeviceRleBitmap:
+    """bitmaps.compress (bitmaps.py:407-414) with the result kept in HBM: the
+    canonical stream of an uncompressed bitmap, encoded on the device (K7)."""
+    k = kind_of(bitmap)
+    if k == "dr":
+        return bitmap
+    if k == "r":
+        return to_device(bitmap, device)
+    b = to_device(bitmap, device)
+    dout, n = _encode_on_device(b.data[: b.n_words], b.bit_length)
+    return DeviceRleBitmap(dout[: max(n, 1)], b.bit_length, n)
 
 
 def _finish(bitmaps, out: torch.Tensor, nwords: int, r: int, popcnt: torch.Tensor, last_nz: torch.Tensor):

@@ -14,15 +14,58 @@ from __future__ import annotations
 
 import ctypes
 import random
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
-from .api import _device_for
+from .api import _device_for, compress_device, decompress, to_device
 from .bitmaps import DeviceBitmap, DeviceRleBitmap, kind_of
 from .engine import UPLOADS
 from .errors import InputError
+
+
+@dataclass
+class DeviceDataset:
+    """``bench.datagen.Dataset`` (datagen.py:29-56) with its bitmaps in HBM: a named
+    collection over a shared universe of row ids.  ``make_similarity`` accepts it
+    like the reference's dataset; representation changes run on the device
+    (K7 encoder for ``ewah``, the K4 decoder for ``uncompressed``)."""
+
+    name: str
+    universe: int
+    bitmaps: list
+    labels: list = field(default_factory=list)
+
+    def __post_init__(self):
+        if not self.labels:
+            self.labels = [str(i) for i in range(len(self.bitmaps))]
+
+    @classmethod
+    def from_dataset(cls, dataset, kind: str | None = None, device=None) -> "DeviceDataset":
+        """Upload a (reference or host) dataset; each distinct bitmap object is copied once."""
+        seen = {}
+        bms = []
+        for b in dataset.bitmaps:
+            if id(b) not in seen:
+                seen[id(b)] = to_device(b, device)
+            bms.append(seen[id(b)])
+        out = cls(dataset.name, dataset.universe, bms, list(getattr(dataset, "labels", []) or []))
+        return out.to_repr(kind) if kind else out
+
+    def to_repr(self, kind: str) -> "DeviceDataset":
+        """Dataset.to_repr (datagen.py:42-52) on the device."""
+        if kind in ("ewah", "rle", "compressed"):
+            conv = [compress_device(b) for b in self.bitmaps]
+        elif kind in ("uncompressed", "bitset"):
+            conv = [b if isinstance(b, DeviceBitmap) else decompress(b) for b in self.bitmaps]
+        else:
+            raise InputError(f"unknown representation {kind!r}")
+        return DeviceDataset(self.name, self.universe, conv, list(self.labels))
+
+    def compressed_words(self) -> int:
+        """Dataset.compressed_words (datagen.py:54-56)."""
+        return sum(b.n_words if isinstance(b, DeviceRleBitmap) else compress_device(b).n_words for b in self.bitmaps)
 
 
 @dataclass

@@ -101,3 +101,32 @@ def test_similarity_front_end_matches_reference(bq, case):
         got = bq.scan_count(q.bitmaps, m["t"])
         words = bq.decompress(got).words if rle else got.words
         assert words == case.out.tolist()
+
+
+@pytest.mark.parametrize("case", SIM[:4], ids=lambda c: c.id)
+def test_device_dataset_matches_reference_selection(bq, case):
+    """DeviceDataset (datagen.Dataset in HBM): both representations produced on the
+    device give the reference's selection and threshold answer."""
+    from oracle import oracle as O
+    from paper_1402_4073_b200.similarity import DeviceDataset, make_similarity
+
+    m = case.meta
+    host = [bq.UncompressedBitmap(a.tolist(), b) for a, b in zip(case.inputs, case.bits)]
+    ds = types.SimpleNamespace(name=m["name"], universe=m["universe"], bitmaps=host)
+    for kind in ("uncompressed", "ewah"):
+        dd = DeviceDataset.from_dataset(ds, kind)
+        assert len(dd.labels) == len(host)
+        if kind == "ewah":
+            for b, h in zip(dd.bitmaps, host):
+                exp = O.rle_compress(np.array(h.words, dtype=np.uint64), h.bit_length)
+                assert b.data[: b.n_words].cpu().numpy().view(np.uint64).tolist() == list(exp)
+        q = make_similarity(dd, m["rid_count"], m["n"], m["seed"])
+        assert q.rids == m["rids"] and q.source_indices == m["chosen"] and q.multiplicities == m["mult"]
+        got = bq.scan_count(q.bitmaps, m["t"])  # device inputs of either kind: uncompressed device result
+        assert isinstance(got, bq.DeviceBitmap)
+        words = got.to_numpy()
+        nz = np.flatnonzero(words)
+        assert words[: nz[-1] + 1 if nz.size else 0].tolist() == case.out.tolist()
+    assert dd.compressed_words() == sum(len(bq.compress(h).words) for h in host)
+    with pytest.raises(bq.InputError):
+        dd.to_repr("roaring")
