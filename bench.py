@@ -549,6 +549,18 @@ def run_c4(args, torch, bq, lib, dev, stream):
         first_evals_s.append(round(time.perf_counter() - t_e, 4))
     ms = _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), args.steps, args.warmup, stream,
                          flush=lambda: _l2_flush(scratch))
+    # the same query through the in-kernel EWAH decoder (K4, per-stream marker walks over the
+    # original streams: what a query's first evaluation runs), timed the same way
+    prev = os.environ.get("BQ_RLE_SLICED")
+    os.environ["BQ_RLE_SLICED"] = "0"
+    try:
+        ms_k4 = _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), max(10, args.steps // 5),
+                                args.warmup, stream, flush=lambda: _l2_flush(scratch))
+    finally:
+        if prev is None:
+            os.environ.pop("BQ_RLE_SLICED", None)
+        else:
+            os.environ["BQ_RLE_SLICED"] = prev
     pc.zero_()
     q.threshold(t, out, pc, stream=stream)
     comp_bytes = comp_words * 8
@@ -576,6 +588,9 @@ def run_c4(args, torch, bq, lib, dev, stream):
                  {"value_uncompressed_equivalent_gbs": round(n * nw * 8 / (statistics.mean(ms) / 1e3) / 1e9, 1),
                   "popcount": int(pc.item()), "directory_build_s": round(t_dir, 4),
                   "directory_bytes": q.directory_bytes, "host_generation_s": round(t_gen, 2),
+                  "direct_ewah_k4": {"mean_launch_ms": round(statistics.mean(ms_k4), 5),
+                                     "value_gbs": round(comp_bytes / (statistics.mean(ms_k4) / 1e3) / 1e9, 1),
+                                     "note": "per-stream K4 on the original EWAH streams (a query's first evaluation)"},
                   "sliced_layout": {"markers": n_mk, "literal_words": n_lit,
                                     "note": "value = EWAH input bytes / kernel time; roofline = bytes K4s moves "
                                             "(32-bit markers + checkpoints + output)"},

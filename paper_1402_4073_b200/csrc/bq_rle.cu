@@ -40,6 +40,7 @@
 #include <vector>
 
 #include "bq_internal.h"
+#include "bq_rle_tile.cuh"
 
 namespace bq {
 
@@ -260,13 +261,9 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
     constexpr int kSlots = STAGED ? kSlotsPerBatch : kSlotsUnstaged;
     extern __shared__ __align__(16) uint8_t rle_smem[];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);  // [kRleTile + 4] packed (ones | dirty << 16)
-    uint8_t *region = rle_smem + kCntBytes;                  // phase A: warp pools; phase C: bit counters
-    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);       // [kSlots][32]
-    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + kSlots * 128);   // [kRleTile]
-    uint16_t *undecided = slot_of + kRleTile;                                    // [kRleTile]
-    uint16_t *slot_word = undecided + kRleTile;                                  // [kSlots]
+    uint8_t *region = rle_smem + kCntBytes;                  // phase A: warp pools; phases B/C: tile_resolve
     __shared__ uint32_t n_undecided;
-    __shared__ uint32_t warp_sums[NT / 32];
+    __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const uint32_t tile = blockIdx.x;
     const uint64_t ts = (uint64_t)tile * kRleTile;
@@ -390,19 +387,18 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
         };
         const int nk = (n + NT - 1) / NT;
         const int my = warp * 32 + lane;
-        Seg cur, nxt;
-        nxt.lim = 0;
-        nxt.staged = false;
-        Pre q0, q1;
-        fetch(my, q0);
-        fetch(NT + my, q1);
-        plan(q0, 0, cur);
-        for (int k = 0; k < nk; ++k) {
-            if (k + 1 < nk) {
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
-                plan(q1, k + 1, nxt);
-                fetch((k + 2) * NT + my, q1);
-            }
+        // two-batch unrolled pipeline: batch k + 2's metadata lands in q while batch k is
+        // walked, and the segment plans alternate between sa / sb (no register rotation
+        // that would wait on the metadata loads right after issuing them)
+        Seg sa, sb;
+        Pre q;
+        fetch(my, q);
+        plan(q, 0, sa);
+        fetch(NT + my, q);
+        auto step = [&](int k, Seg &cur, Seg &nxt) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
+            plan(q, k + 1, nxt);  // k + 1 == nk: nothing to copy, arrive only
+            fetch((k + 2) * NT + my, q);
             wait_batch(k);  // every lane's bulk copy for batch k has landed
             if (cur.lim && !a.debug) {
                 if (cur.staged)
@@ -411,95 +407,34 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
                     sweep_stream<true>(cur.g, cur.lim, cur.pos, ts, width, cnt);
             }
             __syncwarp();  // batch k's pool half may be refilled for batch k + 2
-            cur = nxt;
+        };
+        for (int k = 0; k < nk; k += 2) {
+            step(k, sa, sb);
+            if (k + 1 < nk) step(k + 1, sb, sa);
         }
     }
     __syncthreads();
 
-    // ---- inclusive prefix scan of cnt[0..kRleTile) (kPer words per thread) -----
-    constexpr int kPer = kRleTile / NT;
-    uint32_t local[kPer];
-    uint32_t run_sum = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        run_sum += cnt[tid * kPer + k];
-        local[k] = run_sum;
-    }
-    uint32_t incl = run_sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) warp_sums[warp] = incl;
+    // ---- B: prefix sum, then decide every word the fills decide ------------------
+    const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
+    TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out};
+    uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlots>());
+    unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
-    uint32_t warp_off = 0;
-    for (int w = 0; w < warp; ++w) warp_off += warp_sums[w];
-    const uint32_t excl = warp_off + incl - run_sum;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) cnt[tid * kPer + k] = local[k] + excl;
-    for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
-    __syncthreads();
-
-    // ---- B: decide from (k, d) ----------------------------------------------
-    unsigned long long pc = 0;
-    for (int k = tid; k < width; k += NT) {
-        const uint32_t c = cnt[k];
-        const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
-        if (ones + dirty <= __ldg(a.const_until + ones)) {
-            uint64_t w = accept_at(a.accept_bits, ones) ? ~0ull : 0ull;
-            if (ts + k == a.total_words - 1) w &= a.last_mask;
-            a.out[ts + k] = w;
-            pc += __popcll(w);
-        } else {
-            undecided[atomicAdd(&n_undecided, 1u)] = (uint16_t)k;
-        }
-    }
-    __syncthreads();
-    const uint32_t nu = n_undecided;
 
     // ---- C: read dirty literals only where the fills leave the outcome open ----
-    for (uint32_t base = 0; base < nu; base += kSlots) {
-        const uint32_t nb = min((uint32_t)kSlots, nu - base);
-        for (uint32_t u = tid; u < nb; u += NT) {
-            const uint16_t wk = undecided[base + u];
-            slot_word[u] = wk;
-            slot_of[wk] = (uint16_t)u;
-        }
-        for (int k = tid; k < kSlots * 32; k += NT) (&bitcnt[0][0])[k] = 0u;
-        __syncthreads();
+    pc += tile_resolve<NT, kSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &add_bits) {
         for (int st = tid; st < a.n; st += NT) {
             walk_tile(a, st, tile, ts, te,
                       [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit, const uint64_t *s) {
                           const uint64_t lo = max(ds, ts), hi = min(de, te);
                           for (uint64_t p = lo; p < hi; ++p) {
                               const uint16_t u = slot_of[p - ts];
-                              if (u == kNoSlot) continue;
-                              uint64_t x = __ldg(s + lit + (p - ds));
-                              while (x) {
-                                  const int b = __ffsll((long long)x) - 1;
-                                  atomicAdd(&bitcnt[u][b & 31], (b < 32) ? 1u : 0x10000u);
-                                  x &= x - 1;
-                              }
+                              if (u != kNoSlot) add_bits(u, __ldg(s + lit + (p - ds)));
                           }
                       });
         }
-        __syncthreads();
-        for (uint32_t u = tid; u < nb; u += NT) {
-            const uint16_t wk = slot_word[u];
-            const uint32_t ones = cnt[wk] & 0xFFFFu;
-            uint64_t w = 0;
-            for (int b = 0; b < 64; ++b) {
-                const uint32_t cb = (bitcnt[u][b & 31] >> ((b >> 5) * 16)) & 0xFFFFu;
-                if (accept_at(a.accept_bits, ones + cb)) w |= 1ull << b;
-            }
-            if (ts + wk == a.total_words - 1) w &= a.last_mask;
-            a.out[ts + wk] = w;
-            pc += __popcll(w);
-            slot_of[wk] = kNoSlot;
-        }
-        __syncthreads();
-    }
+    });
 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);

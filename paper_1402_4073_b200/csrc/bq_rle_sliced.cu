@@ -24,6 +24,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "bq_internal.h"
+#include "bq_rle_tile.cuh"
 
 namespace bq {
 
@@ -42,7 +43,7 @@ constexpr int kPieceMarkers = kPieceChunks * kSliceChunk;  // 4096 markers = 16 
 constexpr int kSlSlots = BQ_SL_SLOTS;                      // undecided words per phase-C pass
 constexpr size_t kSlCntBytes = (size_t)(kRleTile + 36) * 4;  // + sentinel + 32 per-lane dummies (+ pad)
 constexpr size_t kSlBufBytes = 2 * (size_t)kPieceMarkers * 4;
-constexpr size_t kSlPhaseC = (size_t)kSlSlots * 128 + (size_t)kRleTile * 4 + (size_t)kSlSlots * 2;
+constexpr size_t kSlPhaseC = tile_resolve_bytes<kSlSlots>() + (size_t)kRleTile * 2;  // + undecided list
 constexpr size_t kSlRegion = kSlBufBytes > kSlPhaseC ? kSlBufBytes : kSlPhaseC;
 constexpr size_t kSlSmem = kSlCntBytes + 16 + kSlRegion;  // cnt | 2 mbarriers | region
 
@@ -217,13 +218,8 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     uint64_t *bars = reinterpret_cast<uint64_t *>(sl_smem + kSlCntBytes);
     uint8_t *region = sl_smem + kSlCntBytes + 16;
     uint32_t *buf = reinterpret_cast<uint32_t *>(region);  // [2][kPieceMarkers]
-    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);
-    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + kSlSlots * 128);
-    uint16_t *undecided = slot_of + kRleTile;
-    uint16_t *slot_word = undecided + kRleTile;
     __shared__ uint32_t n_undecided;
-    __shared__ uint32_t warp_sums[NT / 32];
-    __shared__ uint32_t warp_reach[NT / 32];
+    __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
     const uint32_t tile = blockIdx.x;
@@ -303,72 +299,16 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     }
     __syncthreads();
 
-    // ---- inclusive prefix scan of cnt[0..kRleTile) ------------------------------
-    constexpr int kPer = kRleTile / NT;
-    uint32_t local[kPer];
-    uint32_t run_sum = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        run_sum += cnt[tid * kPer + k];
-        local[k] = run_sum;
-    }
-    const uint32_t incl = warp_incl_scan(run_sum, lane);
-    if (lane == 31) warp_sums[warp] = incl;
+    // ---- B: prefix sum, then decide every word the fills decide ------------------
+    const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
+    TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out};
+    uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlSlots>());
+    unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
-    uint32_t warp_off = 0;
-    for (int w = 0; w < warp; ++w) warp_off += warp_sums[w];
-    const uint32_t excl = warp_off + incl - run_sum;
-    uint32_t reach = 0;  // max over this thread's words of ones + dirty (the largest count they can reach)
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        const uint32_t c = local[k] + excl;
-        cnt[tid * kPer + k] = c;
-        reach = max(reach, (c & 0xFFFFu) + (c >> 16));
-    }
-    reach = __reduce_max_sync(0xffffffffu, reach);
-    if (lane == 0) warp_reach[warp] = reach;
-    __syncthreads();
-    for (int w = 0; w < NT / 32; ++w) reach = max(reach, warp_reach[w]);
 
-    // ---- B: decide from (ones, dirty) ------------------------------------------
-    unsigned long long pc = 0;
-    if (reach <= __ldg(E.const_until) && width == kRleTile && ts + kRleTile < E.total_words) {
-        // no word can leave the accept value of count 0: the tile is constant
-        const uint64_t w = accept_at(E.accept_bits, 0u) ? ~0ull : 0ull;
-        ulonglong2 *o = reinterpret_cast<ulonglong2 *>(E.out + ts);
-        for (int k = tid; k < kRleTile / 2; k += NT) o[k] = make_ulonglong2(w, w);
-        pc = w ? (unsigned long long)(kRleTile / NT) * 64 : 0ull;
-    } else {
-    for (int k = tid; k < width; k += NT) {
-        const uint32_t c = cnt[k];
-        const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
-        if (ones + dirty <= __ldg(E.const_until + ones)) {
-            uint64_t w = accept_at(E.accept_bits, ones) ? ~0ull : 0ull;
-            if (ts + k == E.total_words - 1) w &= E.last_mask;
-            E.out[ts + k] = w;
-            pc += __popcll(w);
-        } else {
-            undecided[atomicAdd(&n_undecided, 1u)] = (uint16_t)k;
-        }
-    }
-    }
-    __syncthreads();
-    const uint32_t nu = n_undecided;
-    if (nu) {
-        for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
-        __syncthreads();
-    }
-
-    // ---- C: literal bits of undecided words ----------------------------------------
-    for (uint32_t base = 0; base < nu; base += kSlSlots) {
-        const uint32_t nb = min((uint32_t)kSlSlots, nu - base);
-        for (uint32_t u = tid; u < nb; u += NT) {
-            const uint16_t wk = undecided[base + u];
-            slot_word[u] = wk;
-            slot_of[wk] = (uint16_t)u;
-        }
-        for (int k = tid; k < kSlSlots * 32; k += NT) (&bitcnt[0][0])[k] = 0u;
-        __syncthreads();
+    // ---- C: literal bits of undecided words (chunks decoded again, literals from HBM) --
+    pc += tile_resolve<NT, kSlSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of,
+                                                                                 auto &add_bits) {
         for (uint32_t c = warp; c < nchunks; c += NT / 32) {
             const uint64_t cm = __ldg(meta + c);
             const uint4 v = __ldg(reinterpret_cast<const uint4 *>(tmk) + c * 32 + lane);
@@ -389,34 +329,13 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
                 const uint32_t fe = rel + run;
                 for (uint32_t q = 0; q < dirty; ++q) {
                     const uint16_t u = slot_of[fe + q];
-                    if (u == kNoSlot) continue;
-                    uint64_t x = __ldg(tlit + lit + q);
-                    while (x) {
-                        const int b = __ffsll((long long)x) - 1;
-                        atomicAdd(&bitcnt[u][b & 31], (b < 32) ? 1u : 0x10000u);
-                        x &= x - 1;
-                    }
+                    if (u != kNoSlot) add_bits(u, __ldg(tlit + lit + q));
                 }
                 lit += dirty;
                 rel = (fe + dirty) & (kRleTile - 1);
             }
         }
-        __syncthreads();
-        for (uint32_t u = tid; u < nb; u += NT) {
-            const uint16_t wk = slot_word[u];
-            const uint32_t ones = cnt[wk] & 0xFFFFu;
-            uint64_t w = 0;
-            for (int b = 0; b < 64; ++b) {
-                const uint32_t cb = (bitcnt[u][b & 31] >> ((b >> 5) * 16)) & 0xFFFFu;
-                if (accept_at(E.accept_bits, ones + cb)) w |= 1ull << b;
-            }
-            if (ts + wk == E.total_words - 1) w &= E.last_mask;
-            E.out[ts + wk] = w;
-            pc += __popcll(w);
-            slot_of[wk] = kNoSlot;
-        }
-        __syncthreads();
-    }
+    });
 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
