@@ -68,7 +68,7 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 // the K3 directory.  Every (tile, stream) slice -- the stream's words
 // [1024 t, 1024 t + 1024) -- is re-encoded as self-contained markers covering
 // exactly 1024 words (clipped fills, clipped literal groups, a zero fill after
-// the stream's end), stored as 32-bit markers (bit | run << 1 | dirty << 12) in
+// the stream's end), stored as 32-bit markers (run | bit << 11 | dirty << 16) in
 // one array and their literal words in another, both tile-major.  Marker arrays
 // of a tile are padded to a multiple of kSliceChunk; one checkpoint per chunk
 // (word position within its slice, pending literal end, literal index) lets any

@@ -47,9 +47,11 @@ constexpr size_t kSlPhaseC = tile_resolve_bytes<kSlSlots>() + (size_t)kRleTile *
 constexpr size_t kSlRegion = kSlBufBytes > kSlPhaseC ? kSlBufBytes : kSlPhaseC;
 constexpr size_t kSlSmem = kSlCntBytes + 16 + kSlRegion;  // cnt | 2 mbarriers | region
 
-__device__ __forceinline__ uint32_t mk_bit(uint32_t m) { return m & 1u; }
-__device__ __forceinline__ uint32_t mk_run(uint32_t m) { return (m >> 1) & 0x7FFu; }
-__device__ __forceinline__ uint32_t mk_dirty(uint32_t m) { return (m >> 12) & 0x7FFu; }
+// 32-bit slice marker: run (bits 0-10) | fill bit (bit 11) | dirty (bits 16-26); run, dirty <= 1024
+__device__ __forceinline__ uint32_t mk_bit(uint32_t m) { return (m >> 11) & 1u; }
+__device__ __forceinline__ uint32_t mk_run(uint32_t m) { return m & 0x7FFu; }
+__device__ __forceinline__ uint32_t mk_dirty(uint32_t m) { return m >> 16; }
+__device__ __forceinline__ uint32_t mk_pack(uint32_t bit, uint32_t run, uint32_t dirty) { return run | (bit << 11) | (dirty << 16); }
 
 // ---------------------------------------------------------------------------
 // Layout build.  Thread k handles slice (tile k % ntiles, stream k / ntiles):
@@ -73,7 +75,7 @@ __device__ uint2 slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint64_t t
     auto emit = [&](uint32_t bit, uint32_t run, uint32_t dirty) {
         if (EMIT) {
             const uint32_t j = sink.mk0 + n_mk;
-            sink.mk[j] = bit | (run << 1) | (dirty << 12);
+            sink.mk[j] = mk_pack(bit, run, dirty);
             if (j % kSliceChunk == 0)
                 sink.meta[j / kSliceChunk] = (uint64_t)rel | ((uint64_t)(rel != 0 && prev_dirty) << 11) |
                                              ((uint64_t)(sink.lit0 + n_lit) << 32);
