@@ -78,35 +78,78 @@ __device__ __forceinline__ void rle_fail(const RleDirArgs &a, int code, int stre
     if (atomicCAS(a.err, 0, code) == 0) atomicExch(a.err_stream, (unsigned long long)stream);
 }
 
+// K3: one warp per stream.  The stream is read in 32-word windows aligned to its
+// start, so window loads do not wait for the marker chain: the next window is
+// loaded while the current one is decoded (a dirty group reaching past the next
+// window jumps straight to the window of the next marker, skipping literals
+// unread).  Inside a window the markers reachable from the entry marker are found
+// by pointer doubling (each lane's successor j + 1 + dirty, squared five times,
+// with a warp OR-reduction per level), their word positions by a warp prefix sum.
+constexpr int kDirAhead = 6;  // windows in flight ahead of the one being decoded
+constexpr int kDirRing = 8;   // ring slots per warp (> kDirAhead: consumed slots are reused late)
+
 __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constant__ RleDirArgs a) {
+    __shared__ uint64_t ring_all[4][kDirRing][32];
     const int lane = threadIdx.x & 31;
     const int stream = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (stream >= a.n) return;
+    uint64_t(*ring)[32] = ring_all[threadIdx.x >> 5];
     const uint64_t *s = a.ptrs[stream];
     const uint64_t L = a.lens[stream];
     uint2 *dir = a.dir + stream;  // stride n between tiles
-    uint64_t i = 0;     // stream index of the next marker
-    uint64_t pos = 0;   // word position where that marker's fill run starts
-    while (i < L) {
-        const uint64_t idx = i + lane;
-        const uint64_t w = idx < L ? __ldg(s + idx) : 0ull;
+    // Window q (words [32q, 32q + 32)) is copied into ring slot q % kDirRing by
+    // per-lane 8-byte cp.async, kDirAhead windows ahead of the decode; each lane
+    // reads back only the word it copied, so its own wait_group suffices.
+    auto issue = [&](uint64_t q) {
+        const uint64_t idx = q * 32 + lane;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ring[q % kDirRing][lane]);
+        const uint64_t *src = s + (idx < L ? idx : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(idx < L ? 8u : 0u)
+                     : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    uint64_t k = 0;     // window being decoded
+    uint64_t next = 0;  // stream index of the next marker
+    uint64_t pos = 0;   // word position where its fill run starts
+    for (int q = 0; q < kDirAhead; ++q) issue(q);
+    for (uint32_t step = 0; next < L; ++step) {
+        const uint64_t kk = next / 32;
+        if (kk >= k + kDirAhead) {  // a long literal group: restart the pipeline at the next marker
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            k = kk;
+            for (int q = 0; q < kDirAhead; ++q) issue(k + q);
+        } else {
+            for (; k < kk; ++k) issue(k + kDirAhead);  // windows of literals only
+        }
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDirAhead - 1) : "memory");
+        const uint64_t w = ring[k % kDirRing][lane];
+        const uint64_t bc = k * 32;
+        const uint64_t idx = bc + lane;
         const uint64_t run = (w >> 1) & 0xFFFFFFFFull;
         const uint64_t dirty = w >> 33;
-        const uint64_t nxt = (uint64_t)lane + 1 + dirty;
-        // follow the chain from lane 0 (a marker) through the window
-        uint32_t mask = 0;
-        uint64_t cur = 0;
-        while (cur < 32 && i + cur < L) {
-            mask |= 1u << cur;
-            cur = __shfl_sync(0xffffffffu, nxt, (int)cur);
+        // markers reachable from the entry marker: each lane's successor if it were a
+        // marker (window-relative, 32 = outside), squared five times by pointer doubling
+        // with one warp OR-reduction per level
+        uint32_t j = dirty < 32 ? min((uint32_t)lane + 1 + (uint32_t)dirty, 32u) : 32u;
+        uint32_t reach = 1u << (uint32_t)(next - bc);
+#pragma unroll
+        for (int level = 0; level < 5; ++level) {
+            const bool in = ((reach >> lane) & 1u) && j < 32u;
+            reach |= __reduce_or_sync(0xffffffffu, in ? (1u << j) : 0u);
+            if (level < 4) {
+                const uint32_t jj = __shfl_sync(0xffffffffu, j, j < 32u ? (int)j : lane);
+                j = j < 32u ? jj : 32u;
+            }
         }
-        const bool is_m = (mask >> lane) & 1u;
+        reach &= (L - bc >= 32) ? 0xffffffffu : ((1u << (uint32_t)(L - bc)) - 1u);
+        next = __shfl_sync(0xffffffffu, idx + 1 + dirty, 31 - __clz(reach));
+        const bool is_m = (reach >> lane) & 1u;
         const uint64_t span = is_m ? run + dirty : 0ull;
         // exclusive prefix sum of spans over marker lanes
         uint64_t incl = span;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
         const uint64_t start = pos + incl - span;
@@ -128,11 +171,10 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
             for (; b < end && b < a.total_words; b += kRleTile)
                 dir[(b / kRleTile) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
         }
-        const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
-        pos += total;
-        i += cur;
-        if (*((volatile int *)a.err)) break;
+        pos += __shfl_sync(0xffffffffu, incl, 31);
+        if ((step & 63) == 63 && *((volatile int *)a.err)) break;
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // tiles past the encoded coverage: stream exhausted, implicit zero tail
     uint64_t b = (pos + kRleTile - 1) / kRleTile * kRleTile;
     for (uint64_t t = b / kRleTile + lane; t < a.ntiles; t += 32) dir[t * a.n] = make_uint2((uint32_t)L, (uint32_t)pos);
