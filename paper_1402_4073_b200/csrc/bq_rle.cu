@@ -37,6 +37,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "bq_internal.h"
@@ -500,6 +501,7 @@ struct bq_rle_query {
     int evals = 0;
     bool sliced_tried = false;
     SlicedLayout sliced;  // tile-sliced layout (K4s), the default derived layout
+    mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced
 };
 
 extern "C" {
@@ -602,10 +604,15 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     delete q;
 }
 
-BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) { return q ? q->dir_bytes + q->sliced.bytes : 0; }
+BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) {
+    if (!q) return 0;
+    std::lock_guard<std::mutex> guard(q->build_mu);
+    return q->dir_bytes + q->sliced.bytes;
+}
 
 BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals) {
     if (!q || !n_markers || !n_literals) return set_error(BQ_EINPUT, "NULL argument");
+    std::lock_guard<std::mutex> guard(q->build_mu);
     *n_markers = q->sliced.n_markers;
     *n_literals = q->sliced.n_literals;
     return BQ_OK;
@@ -657,21 +664,28 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     // the re-encoding and a reused query (cache hit, several thresholds) gets K4s.
     const char *tenv = getenv("BQ_RLE_SLICED");
     const int sliced_mode = tenv ? atoi(tenv) : 2;
-    ++q->evals;
-    if (staged && sliced_mode && !q->sliced_tried && q->evals >= sliced_mode) {
-        q->sliced_tried = true;
-        e = cudaStreamSynchronize(s);  // the build runs on the legacy stream
-        if (e != cudaSuccess) {
-            cudaFreeAsync(d_tab, s);
-            return cuda_error(e, "cudaStreamSynchronize");
+    SlicedLayout sliced;
+    {
+        // evaluations of one query may come from several host threads (inputs are shared,
+        // SPEC.md:269-270): the layout is built once, under the query's lock
+        std::lock_guard<std::mutex> guard(q->build_mu);
+        ++q->evals;
+        if (staged && sliced_mode && !q->sliced_tried && q->evals >= sliced_mode) {
+            q->sliced_tried = true;
+            e = cudaStreamSynchronize(s);  // the build runs on the legacy stream
+            if (e != cudaSuccess) {
+                cudaFreeAsync(d_tab, s);
+                return cuda_error(e, "cudaStreamSynchronize");
+            }
+            rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, &q->sliced);
+            if (rc) {
+                cudaFreeAsync(d_tab, s);
+                return rc;
+            }
         }
-        rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, &q->sliced);
-        if (rc) {
-            cudaFreeAsync(d_tab, s);
-            return rc;
-        }
+        sliced = q->sliced;
     }
-    if (q->sliced.mem && staged && sliced_mode) {
+    if (sliced.mem && staged && sliced_mode) {
         SlicedEval se;
         se.n = n;
         se.total_words = q->total_words;
@@ -682,7 +696,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         se.out = d_out;
         se.popcnt = d_popcnt;
         se.debug = a.debug;
-        rc = launch_sliced(q->sliced, se, s);
+        rc = launch_sliced(sliced, se, s);
         cudaFreeAsync(d_tab, s);
         return rc;
     } else if (staged) {

@@ -318,3 +318,41 @@ def test_constant_tiles_of_sparse_streams(bq, acc_kind):
         exp = O.cdom_symmetric(streams, r, acc)
         assert np.array_equal(host(out, nw), exp)
         assert int(pc.item()) == popcount(exp)
+
+
+def test_concurrent_evaluations_share_one_query(bq, monkeypatch):
+    """Several host threads evaluate one query (the reference allows concurrent
+    invocations on shared inputs); the layout is built once and
+    every answer matches the oracle."""
+    import threading
+
+    monkeypatch.delenv("BQ_RLE_SLICED", raising=False)
+    lib = bq._lib.load()
+    n, r = 64, 1 << 20
+    streams = [markov(lib, 31, i, r, 64.0, 700.0) for i in range(n)]
+    q = bq.RleQuery(dev(streams), r)
+    nw = r // 64
+    ts = [1, 3, 7, 20, 64]
+    exp = {t: O.cdom_threshold(streams, r, t) for t in ts}
+    errors = []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    t = ts[(k + rep) % len(ts)]
+                    out, pc = q.threshold(t)
+                    s.synchronize()
+                    if not np.array_equal(host(out, nw), exp[t]):
+                        errors.append((k, t))
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors
+    assert q.layout_stats[0] > 0
