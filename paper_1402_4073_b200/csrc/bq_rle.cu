@@ -194,6 +194,7 @@ struct RleCountArgs {
     uint64_t *out;
     unsigned long long *popcnt;
     int debug;  // experiment knob (BQ_RLE_DEBUG): 1 = skip marker walks, 2 = also skip copies
+    uint32_t four;  // 4 as a runtime value (see sweep_stream)
 };
 
 
@@ -232,7 +233,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // fill ends and the literals begin, -dirty where the literals end.
 template <bool GLOBAL>
 __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, uint32_t pos, uint64_t ts, int W,
-                                             uint32_t *cnt) {
+                                             uint32_t *cnt, uint32_t four) {
     auto load = [src](uint32_t k) { return GLOBAL ? __ldg(src + k) : src[k]; };
     if (lim == 0) return;
     const uint32_t Wu = (uint32_t)W;
@@ -271,8 +272,9 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
         // (this one-fill ends | this marker's literals start) at fe
         const uint32_t at_rel = carry + ones;
         const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
-        atomicAdd(&cnt[at_rel ? rel : dummy], at_rel);
-        atomicAdd(&cnt[at_fe ? fe : dummy], at_fe);
+        // byte offsets as index * four (runtime 4): IMAD on the FMA pipe instead of an ALU LEA
+        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_rel ? rel : dummy) * four), at_rel);
+        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_fe ? fe : dummy) * four), at_fe);
         carry = lit ? 0xFFFF0000u : 0u;
         if (de_raw >= Wu) return;  // the pending literal end lies past the tile
         rel = de_raw;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             if (st + NT < n) prefetch(st + NT);
             const uint2 e = a.dir[(size_t)tile * a.n + st];
             const uint64_t L = a.lens[st];
-            if (e.x < L) sweep_stream<true>(a.ptrs[st] + e.x, (uint32_t)(L - e.x), e.y, ts, width, cnt);
+            if (e.x < L) sweep_stream<true>(a.ptrs[st] + e.x, (uint32_t)(L - e.x), e.y, ts, width, cnt, a.four);
         }
     } else {
         // directory metadata of a lane's stream in batch k (tile-major rows: coalesced),
@@ -445,9 +447,10 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             wait_batch(k);  // every lane's bulk copy for batch k has landed
             if (cur.lim && !a.debug) {
                 if (cur.staged)
-                    sweep_stream<false>(pool + (size_t)(k & 1) * kPoolWords + cur.off, cur.lim, cur.pos, ts, width, cnt);
+                    sweep_stream<false>(pool + (size_t)(k & 1) * kPoolWords + cur.off, cur.lim, cur.pos, ts, width, cnt,
+                                        a.four);
                 else
-                    sweep_stream<true>(cur.g, cur.lim, cur.pos, ts, width, cnt);
+                    sweep_stream<true>(cur.g, cur.lim, cur.pos, ts, width, cnt, a.four);
             }
             __syncwarp();  // batch k's pool half may be refilled for batch k + 2
         };
@@ -653,6 +656,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.const_until = static_cast<const uint32_t *>(d_tab) + nbits_words;
     a.out = d_out;
     a.popcnt = d_popcnt;
+    a.four = 4;
     // BQ_RLE_STAGED=0 selects the unstaged phase A (A/B measurement)
     static const char *env = getenv("BQ_RLE_STAGED");
     const bool staged = !(env && env[0] == '0');

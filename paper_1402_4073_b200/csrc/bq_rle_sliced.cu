@@ -169,10 +169,18 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
 // ---------------------------------------------------------------------------
 // K4s: one CTA per tile.
 
+// K4s decode is bound by the ALU pipe (shifts, masks, selects, LEA); the shared-memory
+// byte offsets are formed as index * four with four a runtime value, so they go to
+// the FMA pipe (IMAD) instead of an ALU LEA.
+struct MulC {
+    uint32_t four;  // 4
+};
+
 struct SlArgs {
     const uint32_t *markers;
     const uint64_t *literals;
     const uint64_t *tile_mbase, *tile_lbase, *chunk_meta;
+    MulC mc;
     SlicedEval e;
 };
 
@@ -190,7 +198,9 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 // (run + dirty), modulo 1024 (slices cover exactly 1024 words).  Two updates per
 // marker: (+one-fill start, -pending literal end) at its start, (-one-fill end,
 // +literal start) where its fill ends.
-__device__ __forceinline__ void decode_chunk(const uint4 v, uint32_t cm, int lane, uint32_t *cnt) {
+
+__device__ __forceinline__ void decode_chunk(const uint4 v, uint32_t cm, int lane, uint32_t *cnt, const MulC &c) {
+    const uint32_t four = c.four;
     const uint32_t dummy = kRleTile + 1 + lane;  // per-lane slot for zero updates (no same-address conflicts)
     const uint32_t m[4] = {v.x, v.y, v.z, v.w};
     uint32_t tot = 0;
@@ -206,8 +216,9 @@ __device__ __forceinline__ void decode_chunk(const uint4 v, uint32_t cm, int lan
         const uint32_t fe = rel + run;
         const uint32_t at_rel = bit + ((rel != 0u && pd) ? 0xFFFF0000u : 0u);
         const uint32_t at_fe = (dirty ? 0x10000u : 0u) - bit;
-        atomicAdd(&cnt[at_rel ? rel : dummy], at_rel);
-        atomicAdd(&cnt[at_fe ? fe : dummy], at_fe);
+        // byte offsets through IMAD (runtime stride): keeps address arithmetic off the ALU pipe
+        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_rel ? rel : dummy) * four), at_rel);
+        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_fe ? fe : dummy) * four), at_fe);
         pd = dirty != 0u;
         rel = (fe + dirty) & (kRleTile - 1);
     }
@@ -290,8 +301,8 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
             const uint32_t cm1 = (uint32_t)__shfl_sync(0xffffffffu, pmeta, two ? c2 : c);
             const uint4 v0 = pb[c * 32 + lane];
             const uint4 v1 = two ? pb[c2 * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-            decode_chunk(v0, cm0, lane, cnt);
-            decode_chunk(v1, two ? cm1 : 0u, lane, cnt);
+            decode_chunk(v0, cm0, lane, cnt, a.mc);
+            decode_chunk(v1, two ? cm1 : 0u, lane, cnt, a.mc);
         }
         __syncthreads();  // buf[p & 1] is free
         if (tid == 0 && p + 2 < npieces) {
@@ -439,6 +450,7 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
     a.tile_mbase = l.tile_mbase;
     a.tile_lbase = l.tile_lbase;
     a.chunk_meta = l.chunk_meta;
+    a.mc = MulC{4u};
     a.e = e;
     cudaError_t err = cudaFuncSetAttribute(rle_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlSmem);
     if (err != cudaSuccess) return cuda_error(err, "cudaFuncSetAttribute(rle_sliced_kernel)");
