@@ -184,14 +184,7 @@ struct SlArgs {
     SlicedEval e;
 };
 
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-    }
-    return v;
-}
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) { return warp_incl_scan_u32(v, lane); }
 
 // Decode one chunk (4 markers per lane) into the difference array: the word
 // position of each marker is the chunk checkpoint plus the warp prefix sum of

@@ -23,12 +23,14 @@ struct TileDecide {
     uint64_t *out;
 };
 
-__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, int lane) {
+// Warp inclusive prefix sum.  The shuffle's own in-range predicate guards the add
+// (shfl.sync.up r|p), so no lane compare or select is spent per step.
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, int) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-    }
+    for (int o = 1; o < 32; o <<= 1)
+        asm("{\n\t.reg .u32 r;\n\t.reg .pred p;\n\tshfl.sync.up.b32 r|p, %0, %1, 0, 0xffffffff;\n\t@p add.u32 %0, %0, r;\n\t}\n"
+            : "+r"(v)
+            : "r"(o));
     return v;
 }
 
