@@ -141,7 +141,17 @@ typedef struct bq_rle_query bq_rle_query;
  * immutable, bitmaps.py:12-13). */
 BQ_API int bq_rle_query_create(const bq_rle_span *streams, int n, uint64_t r_bits, int device,
                                bq_rle_query **out);
+/* The same over the output word range [w_begin, w_end) only (multi-GPU word
+ * range shards): the streams are the whole, replicated inputs;
+ * K3 still walks and validates them whole but keeps directory rows for the
+ * range's tiles only, and an evaluation writes words w_begin .. w_end - 1 of the
+ * result to d_out[0 ..].  w_begin must be a multiple of 1024 words, w_end too
+ * unless it is >= ceil(r/64) (clamped to it). */
+BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t r_bits, uint64_t w_begin,
+                                     uint64_t w_end, int device, bq_rle_query **out);
 BQ_API void bq_rle_query_destroy(bq_rle_query *q);
+/* Output words of one evaluation (w_end - w_begin). */
+BQ_API uint64_t bq_rle_query_out_words(const bq_rle_query *q);
 /* Device bytes the query owns: the directory plus, once built, the tile-sliced
  * layout (every 1024-word slice of every stream re-encoded as 32-bit markers
  * covering exactly that slice, literal words apart, tile-major; K4s decodes it

@@ -46,7 +46,9 @@ SIGNATURES = {
     "bq_sweep_host": (_I, [_P, _P, _I, _U64, _P, _P, _I, _P, _P, _I, _U64]),
     "bq_release_workspace": (None, []),
     "bq_rle_query_create": (_I, [_P, _I, _U64, _I, _P]),
+    "bq_rle_query_create_range": (_I, [_P, _I, _U64, _U64, _U64, _I, _P]),
     "bq_rle_query_destroy": (None, [_P]),
+    "bq_rle_query_out_words": (_U64, [_P]),
     "bq_rle_query_directory_bytes": (_U64, [_P]),
     "bq_rle_query_layout_stats": (_I, [_P, _P, _P]),
     "bq_rle_query_threshold": (_I, [_P, _I, _P, _P, _P]),

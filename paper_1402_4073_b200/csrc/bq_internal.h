@@ -84,13 +84,15 @@ struct SlicedLayout {
     uint64_t bytes = 0;
     uint64_t n_markers = 0, n_literals = 0;
 };
-int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t ntiles,
-                 SlicedLayout *out);
+// tiles [tile0, tile0 + ntiles) of the streams; directory rows are relative to tile0
+int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t tile0,
+                 uint32_t ntiles, SlicedLayout *out);
 void free_sliced(SlicedLayout *l);
 struct SlicedEval {
     int n;
     uint64_t total_words;
-    uint32_t ntiles;
+    uint32_t tile0;   // first tile of the query's range (output word 0 is word tile0 * kRleTile)
+    uint32_t ntiles;  // tiles in the range
     uint64_t last_mask;
     const uint32_t *accept_bits;
     const uint32_t *const_until;

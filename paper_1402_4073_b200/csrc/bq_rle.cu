@@ -69,8 +69,9 @@ struct RleDirArgs {
     int n;
     uint64_t total_words;  // ceil(r/64)
     uint64_t tail_mask;    // valid bits of the last word when r % 64 != 0, else 0
-    uint32_t ntiles;
-    uint2 *dir;            // [ntiles][n]: (marker index, run start word); tile-major so a K4 CTA reads one row
+    uint32_t tile0;        // first tile of the query's word range
+    uint32_t nrows;        // directory rows: the range's tiles + 1 (the boundary after its last tile)
+    uint2 *dir;            // [nrows][n]: (marker index, run start word); tile-major so a K4 CTA reads one row
     int *err;              // first error code
     unsigned long long *err_stream;
 };
@@ -167,18 +168,20 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
                     rle_fail(a, RLE_ERR_BEYOND_R, stream);
                 }
             }
-            // record every tile boundary b with start <= b < end
-            uint64_t b = (start + kRleTile - 1) / kRleTile * kRleTile;
-            for (; b < end && b < a.total_words; b += kRleTile)
-                dir[(b / kRleTile) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
+            // record every tile boundary b with start <= b < end that the range's rows cover
+            const uint64_t r0 = (uint64_t)a.tile0 * kRleTile, r1 = (uint64_t)(a.tile0 + a.nrows) * kRleTile;
+            uint64_t b = max((start + kRleTile - 1) / kRleTile * kRleTile, r0);
+            for (; b < end && b < a.total_words && b < r1; b += kRleTile)
+                dir[(b / kRleTile - a.tile0) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
         }
         pos += __shfl_sync(0xffffffffu, incl, 31);
         if ((step & 63) == 63 && *((volatile int *)a.err)) break;
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // tiles past the encoded coverage: stream exhausted, implicit zero tail
-    uint64_t b = (pos + kRleTile - 1) / kRleTile * kRleTile;
-    for (uint64_t t = b / kRleTile + lane; t < a.ntiles; t += 32) dir[t * a.n] = make_uint2((uint32_t)L, (uint32_t)pos);
+    const uint64_t t0 = max((pos + kRleTile - 1) / kRleTile, (uint64_t)a.tile0);
+    for (uint64_t t = t0 + lane; t < (uint64_t)a.tile0 + a.nrows; t += 32)
+        dir[(t - a.tile0) * a.n] = make_uint2((uint32_t)L, (uint32_t)pos);
 }
 
 struct RleCountArgs {
@@ -187,7 +190,7 @@ struct RleCountArgs {
     const uint2 *dir;
     int n;
     uint64_t total_words;
-    uint32_t ntiles;
+    uint32_t tile0;   // first (global) tile of the query's range; blockIdx.x is the tile within it
     uint64_t last_mask;
     const uint32_t *accept_bits;  // (n + 1) bits
     const uint32_t *const_until;  // [n + 1]: largest j >= k with accept[k..j] constant
@@ -310,8 +313,8 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
     __shared__ uint32_t n_undecided;
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
-    const uint32_t tile = blockIdx.x;
-    const uint64_t ts = (uint64_t)tile * kRleTile;
+    const uint32_t tile = blockIdx.x;  // directory row; the tile's words are global
+    const uint64_t ts = (uint64_t)(a.tile0 + tile) * kRleTile;
     const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
     const int width = (int)(te - ts);
     const int tid = threadIdx.x;
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             const uint64_t L = a.lens[st];
             const uint32_t first = a.dir[(size_t)tile * a.n + st].x;
             if (first >= L) return;
-            const uint64_t next = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : L;
+            const uint64_t next = a.dir[(size_t)(tile + 1) * a.n + st].x;  // row tile + 1 always exists
             const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + first) & ~(uintptr_t)127;
             const uintptr_t p1 = reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L));
             for (uintptr_t p = p0; p < p1; p += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
             if (st < n) {
                 q.L = a.lens[st];
                 q.e = a.dir[(size_t)tile * a.n + st];
-                q.nx = (tile + 1 < a.ntiles) ? a.dir[(size_t)(tile + 1) * a.n + st].x : 0xFFFFFFFFu;
+                q.nx = a.dir[(size_t)(tile + 1) * a.n + st].x;
                 q.p = a.ptrs[st];
             }
         };
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
 
     // ---- B: prefix sum, then decide every word the fills decide ------------------
     const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
-    TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out};
+    TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile};
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlots>());
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
@@ -495,7 +498,8 @@ struct bq_rle_query {
     int device;
     int n;
     uint64_t r_bits, total_words;
-    uint32_t ntiles;
+    uint64_t w_begin, w_end;  // output word range (w_begin a multiple of kRleTile)
+    uint32_t tile0, ntiles;   // its tiles [tile0, tile0 + ntiles); the directory has ntiles + 1 rows
     void *mem;  // ptr table | len table | directory | error words
     const uint64_t **d_ptrs;
     uint64_t *d_lens;
@@ -510,6 +514,11 @@ struct bq_rle_query {
 extern "C" {
 
 BQ_API int bq_rle_query_create(const bq_rle_span *streams, int n, uint64_t r_bits, int device, bq_rle_query **out) {
+    return bq_rle_query_create_range(streams, n, r_bits, 0, UINT64_MAX, device, out);
+}
+
+BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t r_bits, uint64_t w_begin,
+                                     uint64_t w_end, int device, bq_rle_query **out) {
     if (!out) return set_error(BQ_EINPUT, "out is NULL");
     *out = nullptr;
     if (n < 1) return set_error(BQ_EINPUT, "need at least one input bitmap");
@@ -524,17 +533,26 @@ BQ_API int bq_rle_query_create(const bq_rle_span *streams, int n, uint64_t r_bit
         if (reinterpret_cast<uintptr_t>(streams[i].words) & 7)
             return set_error(BQ_EINPUT, "stream %d: device words must be 8-byte aligned", i);
     }
+    if (w_end > total) w_end = total;
+    if (w_begin > w_end) return set_error(BQ_EINPUT, "word range [%llu, %llu) is empty or reversed",
+                                          (unsigned long long)w_begin, (unsigned long long)w_end);
+    if (w_begin % kRleTile || (w_end % kRleTile && w_end != total))
+        return set_error(BQ_EINPUT, "RLE word range bounds must be multiples of %d words (or the end)", kRleTile);
     int rc = use_device(device);
     if (rc) return rc;
-    const uint32_t ntiles = (uint32_t)((total + kRleTile - 1) / kRleTile);
+    const uint32_t tile0 = (uint32_t)(w_begin / kRleTile);
+    const uint32_t ntiles = (uint32_t)((w_end - w_begin + kRleTile - 1) / kRleTile);
     const size_t tab = (size_t)n * 16;
-    const size_t dirb = (size_t)n * ntiles * sizeof(uint2);
+    const size_t dirb = (size_t)n * (ntiles + 1) * sizeof(uint2);
     const size_t bytes = tab + dirb + 64;
     bq_rle_query *q = new bq_rle_query();
     q->device = device;
     q->n = n;
     q->r_bits = r_bits;
     q->total_words = total;
+    q->w_begin = w_begin;
+    q->w_end = w_end;
+    q->tile0 = tile0;
     q->ntiles = ntiles;
     q->dir_bytes = dirb;
     cudaError_t e = cudaMalloc(&q->mem, bytes);
@@ -562,14 +580,15 @@ BQ_API int bq_rle_query_create(const bq_rle_span *streams, int n, uint64_t r_bit
         delete q;
         return cuda_error(e, "rle query setup");
     }
-    if (ntiles) {
+    if (total) {  // the directory walk validates every stream whole, whatever the range
         RleDirArgs a;
         a.ptrs = q->d_ptrs;
         a.lens = q->d_lens;
         a.n = n;
         a.total_words = total;
         a.tail_mask = (r_bits % W) ? ((1ull << (r_bits % W)) - 1) : 0ull;
-        a.ntiles = ntiles;
+        a.tile0 = tile0;
+        a.nrows = ntiles + 1;
         a.dir = q->d_dir;
         a.err = d_err;
         a.err_stream = d_err_stream;
@@ -613,6 +632,8 @@ BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q) {
     return q->dir_bytes + q->sliced.bytes;
 }
 
+BQ_API uint64_t bq_rle_query_out_words(const bq_rle_query *q) { return q ? q->w_end - q->w_begin : 0; }
+
 BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals) {
     if (!q || !n_markers || !n_literals) return set_error(BQ_EINPUT, "NULL argument");
     std::lock_guard<std::mutex> guard(q->build_mu);
@@ -624,10 +645,10 @@ BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers,
 static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *d_out, unsigned long long *d_popcnt,
                     void *stream) {
     if (!q) return set_error(BQ_EINPUT, "query is NULL");
-    if (q->total_words && !d_out) return set_error(BQ_EINPUT, "d_out is NULL");
+    if (q->ntiles && !d_out) return set_error(BQ_EINPUT, "d_out is NULL");
     int rc = use_device(q->device);
     if (rc) return rc;
-    if (!q->total_words) return BQ_OK;
+    if (!q->ntiles) return BQ_OK;
     const int n = q->n;
     // accept bits and const_until table (host, O(n))
     const size_t nbits_words = (size_t)(n + 1 + 31) / 32;
@@ -650,7 +671,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.dir = q->d_dir;
     a.n = n;
     a.total_words = q->total_words;
-    a.ntiles = q->ntiles;
+    a.tile0 = q->tile0;
     a.last_mask = (q->r_bits % W) ? ((1ull << (q->r_bits % W)) - 1) : ~0ull;
     a.accept_bits = static_cast<const uint32_t *>(d_tab);
     a.const_until = static_cast<const uint32_t *>(d_tab) + nbits_words;
@@ -681,7 +702,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
                 cudaFreeAsync(d_tab, s);
                 return cuda_error(e, "cudaStreamSynchronize");
             }
-            rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->ntiles, &q->sliced);
+            rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->tile0, q->ntiles, &q->sliced);
             if (rc) {
                 cudaFreeAsync(d_tab, s);
                 return rc;
@@ -693,6 +714,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         SlicedEval se;
         se.n = n;
         se.total_words = q->total_words;
+        se.tile0 = q->tile0;
         se.ntiles = q->ntiles;
         se.last_mask = a.last_mask;
         se.accept_bits = a.accept_bits;

@@ -109,12 +109,13 @@ __device__ uint2 slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint64_t t
 }
 
 __global__ void slice_count_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
-                                   uint32_t ntiles, uint64_t *counts) {
+                                   uint32_t tile0, uint32_t ntiles, uint64_t *counts) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
         const int s = (int)(k / ntiles);
         const uint32_t t = (uint32_t)(k % ntiles);
-        const uint2 c = slice_walk<false>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)t * kRleTile, SliceSink{});
+        const uint2 c =
+            slice_walk<false>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)(tile0 + t) * kRleTile, SliceSink{});
         counts[(size_t)t * n + s] = (uint64_t)c.x | ((uint64_t)c.y << 32);
     }
 }
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, int 
 }
 
 __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
-                                  uint32_t ntiles, const uint64_t *offs, const uint64_t *mbase, const uint64_t *lbase,
+                                  uint32_t tile0, uint32_t ntiles, const uint64_t *offs, const uint64_t *mbase, const uint64_t *lbase,
                                   uint32_t *markers, uint64_t *literals, uint64_t *meta) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
@@ -162,7 +163,7 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
         sink.meta = meta + mbase[t] / kSliceChunk;
         sink.mk0 = (uint32_t)o;
         sink.lit0 = (uint32_t)(o >> 32);
-        slice_walk<true>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)t * kRleTile, sink);
+        slice_walk<true>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)(tile0 + t) * kRleTile, sink);
     }
 }
 
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
-    const uint32_t tile = blockIdx.x;
-    const uint64_t ts = (uint64_t)tile * kRleTile;
+    const uint32_t tile = blockIdx.x;  // tile of the query's range; its words are global
+    const uint64_t ts = (uint64_t)(E.tile0 + tile) * kRleTile;
     const int width = (int)min((uint64_t)kRleTile, E.total_words - ts);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t mbase = a.tile_mbase[tile];
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
 
     // ---- B: prefix sum, then decide every word the fills decide ------------------
     const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
-    TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out};
+    TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out, (uint64_t)E.tile0 * kRleTile};
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlSlots>());
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
@@ -350,8 +351,8 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
 
 }  // namespace
 
-int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t ntiles,
-                 SlicedLayout *out) {
+int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t tile0,
+                 uint32_t ntiles, SlicedLayout *out) {
     *out = SlicedLayout();
     if (!ntiles) return BQ_OK;
     const uint64_t cells = (uint64_t)ntiles * n;
@@ -377,7 +378,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         cudaFree(scratch);
         return cuda_error(err, what);
     };
-    slice_count_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, ntiles, counts);
+    slice_count_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemset(tm + ntiles, 0, 8);
     if (e == cudaSuccess) e = cudaMemset(tl + ntiles, 0, 8);
@@ -410,7 +411,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     if (e == cudaSuccess) e = cudaMemcpy(tmb, mb, ((size_t)ntiles + 1) * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(tlb, lb, ((size_t)ntiles + 1) * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) {
-        slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, ntiles, counts, tmb, tlb, markers, literals, meta);
+        slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, tmb, tlb, markers, literals,
+                                         meta);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();

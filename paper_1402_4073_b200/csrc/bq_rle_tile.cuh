@@ -20,7 +20,8 @@ struct TileDecide {
     uint64_t last_mask;           // valid bits of word total_words - 1
     const uint32_t *accept_bits;  // (n + 1) bits
     const uint32_t *const_until;  // [n + 1]: largest j >= k with accept[k..j] constant
-    uint64_t *out;
+    uint64_t *out;                // word g of the result is out[g - out_first]
+    uint64_t out_first;           // first word of the query's range (a multiple of kRleTile)
 };
 
 // Warp inclusive prefix sum.  The shuffle's own in-range predicate guards the add
@@ -78,7 +79,7 @@ __device__ __forceinline__ unsigned long long tile_decide(const TileDecide &d, c
     unsigned long long pc = 0;
     if (reach <= __ldg(d.const_until) && d.width == kRleTile && d.ts + kRleTile < d.total_words) {
         const uint64_t w = accept_at(d.accept_bits, 0u) ? ~0ull : 0ull;
-        ulonglong2 *o = reinterpret_cast<ulonglong2 *>(d.out + d.ts);
+        ulonglong2 *o = reinterpret_cast<ulonglong2 *>(d.out + (d.ts - d.out_first));
         for (int k = tid; k < kRleTile / 2; k += NT) o[k] = make_ulonglong2(w, w);
         return w ? (unsigned long long)(kRleTile / NT) * 64 : 0ull;
     }
@@ -88,7 +89,7 @@ __device__ __forceinline__ unsigned long long tile_decide(const TileDecide &d, c
         if (ones + dirty <= __ldg(d.const_until + ones)) {
             uint64_t w = accept_at(d.accept_bits, ones) ? ~0ull : 0ull;
             if (d.ts + k == d.total_words - 1) w &= d.last_mask;
-            d.out[d.ts + k] = w;
+            d.out[d.ts - d.out_first + k] = w;
             pc += __popcll(w);
         } else {
             undecided[atomicAdd(n_undecided, 1u)] = (uint16_t)k;
@@ -145,7 +146,7 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
                 if (accept_at(d.accept_bits, ones + cb)) w |= 1ull << b;
             }
             if (d.ts + wk == d.total_words - 1) w &= d.last_mask;
-            d.out[d.ts + wk] = w;
+            d.out[d.ts - d.out_first + wk] = w;
             pc += __popcll(w);
             slot_of[wk] = kNoSlot;
         }

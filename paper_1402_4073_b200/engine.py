@@ -182,9 +182,11 @@ class RleQuery:
     """A prepared query over N device-resident RLE streams (``bq_rle_query``).
 
     Creation decodes every stream's marker chain on the device into a tile
-    directory (K3) and validates the encoding (FormatError)."""
+    directory (K3) and validates the encoding (FormatError).  ``word_range``
+    (begin, end) restricts the output to result words [begin, end) -- one rank's
+    shard (``shard.ShardedQuery``); the streams stay whole (replicated)."""
 
-    def __init__(self, streams: Sequence, r_bits: int, device=None):
+    def __init__(self, streams: Sequence, r_bits: int, device=None, word_range=None):
         self._lib = _lib.load()
         first = streams[0] if streams else None
         d = first.data.device if isinstance(first, DeviceRleBitmap) else getattr(first, "device", None)
@@ -201,10 +203,12 @@ class RleQuery:
             pairs.append((t.data_ptr() if n_words else 0, n_words))
         self._spans = _lib.spans(pairs)
         h = ctypes.c_void_p()
-        _lib.check(self._lib.bq_rle_query_create(self._spans, self.n, self.r_bits, self.device.index,
-                                                 ctypes.byref(h)), "bq_rle_query_create")
+        w0, w1 = word_range if word_range is not None else (0, word_count(self.r_bits))
+        _lib.check(self._lib.bq_rle_query_create_range(self._spans, self.n, self.r_bits, int(w0), int(w1),
+                                                       self.device.index, ctypes.byref(h)), "bq_rle_query_create")
         self._h = h
-        self.out_words = word_count(self.r_bits)
+        self.word_range = (int(w0), int(w0) + int(self._lib.bq_rle_query_out_words(h)))
+        self.out_words = self.word_range[1] - self.word_range[0]
 
     @property
     def directory_bytes(self) -> int:

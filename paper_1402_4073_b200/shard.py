@@ -25,6 +25,7 @@ from .bitmaps import word_count
 from .errors import InputError
 
 TILE_WORDS = 512  # kernel tile; shard boundaries are tile aligned (and even, for 16-byte loads)
+RLE_TILE_WORDS = 1024  # RLE tile (K3 directory granularity): RLE shard boundaries
 
 
 def shard_range(total_words: int, world: int, rank: int, align: int = TILE_WORDS) -> tuple[int, int]:
@@ -59,25 +60,38 @@ class ShardedQuery:
     """This rank's shard of a query over N bitmaps, plus the cross-rank reduction.
 
     ``local_inputs``: per input, a 1-D int64 device tensor holding its words
-    [begin, begin + local_words) (the rank's slice).  ``r_bits`` is the GLOBAL
+    [begin, begin + local_words) (the rank's slice).  With ``rle=True`` they are
+    instead the WHOLE compressed streams, replicated on every rank (SURVEY
+    §8(e): ~2.3 GiB at C4); each rank decodes only its word range, whose bounds
+    are then multiples of the 1024-word RLE tile.  ``r_bits`` is the GLOBAL
     result bit length.  ``evaluate(kind, arg, inputs, r_local) -> (words, popcount)``
     overrides the device evaluation (tests use a CPU oracle with gloo)."""
 
     def __init__(self, local_inputs: Sequence, r_bits: int, world: int | None = None, rank: int | None = None,
-                 group=None, evaluate: Callable | None = None, align: int = TILE_WORDS):
+                 group=None, evaluate: Callable | None = None, align: int = TILE_WORDS, rle: bool = False):
         self.group = group
         self.world = world if world is not None else (dist.get_world_size(group) if dist.is_initialized() else 1)
         self.rank = rank if rank is not None else (dist.get_rank(group) if dist.is_initialized() else 0)
         self.r_bits = int(r_bits)
         self.total_words = word_count(self.r_bits)
+        self.rle = bool(rle)
+        if self.rle:
+            align = max(align, RLE_TILE_WORDS)
+            if align % RLE_TILE_WORDS:
+                raise InputError(f"RLE shard alignment must be a multiple of {RLE_TILE_WORDS} words")
+        self.align = align
         self.begin, self.end = shard_range(self.total_words, self.world, self.rank, align)
         self.r_local = local_bit_length(self.r_bits, self.begin, self.end)
         self.inputs = list(local_inputs)
         self._evaluate = evaluate
         self._q = None
         if evaluate is None:
-            from .engine import ThresholdQuery
-            self._q = ThresholdQuery(self.inputs, self.r_local)
+            if self.rle:
+                from .engine import RleQuery
+                self._q = RleQuery(self.inputs, self.r_bits, word_range=(self.begin, self.end))
+            else:
+                from .engine import ThresholdQuery
+                self._q = ThresholdQuery(self.inputs, self.r_local)
 
     @property
     def n(self) -> int:
@@ -108,7 +122,7 @@ class ShardedQuery:
     def gather_result(self, local_out: torch.Tensor, dst: int | None = 0):
         """Assemble the full result (``dst`` rank, or every rank when dst is None)."""
         return gather_result(local_out[: self.end - self.begin], self.total_words, self.world, self.rank,
-                             self.group, dst)
+                             self.group, dst, self.align)
 
 
 def allreduce_popcount(pc: torch.Tensor, group=None) -> torch.Tensor:
@@ -118,14 +132,15 @@ def allreduce_popcount(pc: torch.Tensor, group=None) -> torch.Tensor:
     return pc
 
 
-def gather_result(local: torch.Tensor, total_words: int, world: int, rank: int, group=None, dst=0):
+def gather_result(local: torch.Tensor, total_words: int, world: int, rank: int, group=None, dst=0,
+                  align: int = TILE_WORDS):
     """Concatenate every rank's result words in rank order.
 
     Shards differ in length by at most one tile, so each is padded to the
     largest before all_gather and the padding is dropped after."""
     if world == 1 or not dist.is_initialized():
         return local
-    sizes = [e - b for b, e in (shard_range(total_words, world, g) for g in range(world))]
+    sizes = [e - b for b, e in (shard_range(total_words, world, g, align) for g in range(world))]
     width = max(sizes)
     buf = torch.zeros(width, dtype=local.dtype, device=local.device)
     buf[: local.numel()] = local

@@ -356,3 +356,41 @@ def test_concurrent_evaluations_share_one_query(bq, monkeypatch):
         x.join()
     assert not errors
     assert q.layout_stats[0] > 0
+
+
+@pytest.mark.parametrize("world", [2, 3, 7])
+def test_word_range_queries_tile_the_result(bq, world):
+    """Replicated streams, one query per 1024-aligned word range (the multi-GPU RLE
+    shard, here all on one GPU): the windows concatenate to the
+    whole result and their popcounts add up; both evaluations (K4, then K4s)."""
+    from paper_1402_4073_b200.shard import shard_range
+
+    lib = bq._lib.load()
+    n, r = 50, 64 * 9000 - 11
+    nw = (r + 63) // 64
+    streams = [markov(lib, 13, i, r, 48.0, 500.0) for i in range(n)]
+    d = dev(streams)
+    qs = [bq.RleQuery(d, r, word_range=shard_range(nw, world, g, 1024)) for g in range(world)]
+    for t in (1, 4, 9):
+        exp = O.cdom_threshold(streams, r, t)
+        for _ in range(2):
+            parts, total = [], 0
+            for q in qs:
+                b, e = q.word_range
+                out, pc = q.threshold(t)
+                parts.append(host(out, e - b) if e > b else np.zeros(0, dtype=np.uint64))
+                total += int(pc.item())
+            assert np.array_equal(np.concatenate(parts), exp), t
+            assert total == popcount(exp)
+
+
+def test_word_range_errors(bq):
+    lib = bq._lib.load()
+    r = 64 * 5000
+    d = dev([markov(lib, 1, 0, r, 8.0, 100.0)])
+    with pytest.raises(bq.InputError):
+        bq.RleQuery(d, r, word_range=(512, 2048))  # not tile aligned
+    with pytest.raises(bq.InputError):
+        bq.RleQuery(d, r, word_range=(1024, 1500))  # interior end not aligned
+    q = bq.RleQuery(d, r, word_range=(4096, 10 ** 9))  # end clamps to ceil(r/64)
+    assert q.word_range == (4096, 5000)

@@ -105,3 +105,51 @@ def test_two_ranks_gloo(tmp_path):
     mp.spawn(_worker, args=(world, _free_port(), path), nprocs=world, join=True)
     for g in range(world):
         assert open(f"{path}.{g}").read() == "ok"
+
+
+def _rle_worker(rank, world, port, result_path):
+    """RLE shards: every rank holds the whole compressed streams and evaluates only
+    its 1024-aligned word window."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(9)
+    n, r = 7, 64 * 5000 - 3
+    nw = (r + 63) // 64
+    streams = []
+    for i in range(n):
+        w = rng.integers(0, 2**64, size=nw, dtype=np.uint64) & rng.integers(0, 2**64, size=nw, dtype=np.uint64)
+        w[rng.integers(0, nw, size=nw // 2)] = 0  # runs of zeros
+        w[-1] &= np.uint64((1 << (r % 64)) - 1)
+        streams.append(O.rle_compress(O.trim(w), r))
+
+    def evaluate(kind, arg, inputs, r_local):
+        # the device query decodes only [begin, end) of the whole streams: the oracle
+        # decodes everything and keeps that window
+        words = O.cdom_threshold(inputs, r, arg)[q.begin:q.end]
+        pc = int(np.unpackbits(words.view(np.uint8)).sum())
+        return torch.from_numpy(words.view(np.int64).copy()), torch.tensor([pc], dtype=torch.int64)
+
+    q = ShardedQuery(streams, r, evaluate=evaluate, rle=True)
+    b, e = shard_range(nw, world, rank, 1024)
+    ok = (q.begin, q.end) == (b, e) and b % 1024 == 0 and q.r_local == local_bit_length(r, b, e)
+    for t in (1, 2, 4, 7):
+        words, pc = q.threshold(t)
+        whole = q.gather_result(words, dst=None)
+        exp = O.cdom_threshold(streams, r, t)
+        ok &= np.array_equal(whole.numpy().view(np.uint64), exp)
+        ok &= int(pc.item()) == int(np.unpackbits(exp.view(np.uint8)).sum())
+    with open(f"{result_path}.{rank}", "w") as fp:
+        fp.write("ok" if ok else "mismatch")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_gloo_rle(tmp_path):
+    world = 2
+    path = str(tmp_path / "res")
+    mp.spawn(_rle_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    for g in range(world):
+        assert open(f"{path}.{g}").read() == "ok"
