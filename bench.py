@@ -427,7 +427,7 @@ def _line(workload, value, per_launch_ms, algo_bytes, steps, warmup, config, ext
     return line
 
 
-def run_c1(args, torch, bq, lib, dev, stream):
+def run_c1(args, torch, bq, lib, dev, stream, ctx):
     """Config 1: N=8, r=2^20, p=0.1, T=3 (1 MiB: L2-resident, launch-bound)."""
     n, nw, t = 8, 1 << 14, 3
     data = torch.empty((n, nw), dtype=torch.int64, device=dev)
@@ -444,20 +444,22 @@ def run_c1(args, torch, bq, lib, dev, stream):
     host = [data[i].cpu().numpy().view(np.uint64) for i in range(n)]
     t0 = time.perf_counter()
     reps = 0
-    while time.perf_counter() - t0 < 2.0:
+    while ctx.cpu and time.perf_counter() - t0 < 2.0:
         O.threshold_port(host, 64 * nw, t, host_threads())
         reps += 1
     cpu_gbs = reps * in_bytes / (time.perf_counter() - t0) / 1e9
     exact = np.array_equal(out.cpu().numpy().view(np.uint64), O.scan_count(host, 64 * nw, t))
-    return _line("c1", in_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, in_bytes + nw * 8, args.steps, args.warmup,
+    line = _line("c1", in_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, in_bytes + nw * 8, args.steps, args.warmup,
                  {"workload": "C1: N=8, r=2^20 bits, p=0.1 (q=6554), T=3; L2 flushed (256 MB read) between launches",
                   "n_bitmaps": n, "r_bits": 64 * nw, "t": t},
                  {"matches_oracle": bool(exact),
                   "cpu_baseline": {"value": round(cpu_gbs, 3), "unit": "GB/s", "cores": host_threads(), "kind": "port",
                                    "sample": "full C1, orc_threshold_port (csv_threshold port), 2 s"}})
+    line["_rank_bytes"] = in_bytes  # replicas at N > 1
+    return line
 
 
-def run_c3(args, torch, bq, lib, dev, stream):
+def run_c3(args, torch, bq, lib, dev, stream, ctx):
     """Config 3: N=256, r=2^26, p=0.05, accept = count in [2, 10] (2 GiB)."""
     n, nw = 256, 1 << 20
     pitch = nw + args.pad_words
@@ -479,16 +481,18 @@ def run_c3(args, torch, bq, lib, dev, stream):
     exact = np.array_equal(out[:win].cpu().numpy().view(np.uint64), O.scan_count_symmetric(host, 64 * win, acc))
     t0 = time.perf_counter()
     reps = 0
-    while time.perf_counter() - t0 < 5.0:
+    while ctx.cpu and time.perf_counter() - t0 < 5.0:
         O.symmetric_port(host, 64 * win, acc, host_threads())
         reps += 1
     cpu_gbs = reps * n * win * 8 / (time.perf_counter() - t0) / 1e9
-    return _line("c3", in_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, in_bytes + nw * 8, args.steps, args.warmup,
+    line = _line("c3", in_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, in_bytes + nw * 8, args.steps, args.warmup,
                  {"workload": "C3: N=256, r=2^26 bits, p=0.05 (q=3277), accept = [2 <= count <= 10] (2 GiB)",
                   "n_bitmaps": n, "r_bits": 64 * nw, "accept": "interval [2,10]"},
                  {"matches_oracle_window": bool(exact), "popcount": int(pc.item()),
                   "cpu_baseline": {"value": round(cpu_gbs, 3), "unit": "GB/s", "cores": host_threads(), "kind": "port",
                                    "sample": "C3 window N=256 x 2^14 words, orc_symmetric_port, 5 s"}})
+    line["_rank_bytes"] = in_bytes  # replicas at N > 1
+    return line
 
 
 def _markov_streams(lib, n, r, m1, m0, threads):
@@ -510,7 +514,7 @@ def _markov_streams(lib, n, r, m1, m0, threads):
         return list(ex.map(one, range(n)))
 
 
-def run_c4(args, torch, bq, lib, dev, stream):
+def run_c4(args, torch, bq, lib, dev, stream, ctx):
     """Config 4: N=1024 RLE bitmaps, r=2^30, one-runs mean 256 bits, zero-runs mean
     12544 (density 0.02, interpretation A of SURVEY App. B), T=50; output uncompressed."""
     n, r, t = 1024, 1 << 30, 50
@@ -530,11 +534,14 @@ def run_c4(args, torch, bq, lib, dev, stream):
     dflat = flat.to(dev)
     dstreams = [bq.DeviceRleBitmap(dflat[a:a + b] if b else dflat[:0], r, b) for a, b in offs]
     torch.cuda.synchronize()
-    t_dir = time.perf_counter()
-    q = bq.RleQuery(dstreams, r)
-    t_dir = time.perf_counter() - t_dir
     nw = r // 64
-    out = torch.empty(nw, dtype=torch.int64, device=dev)
+    # N > 1: every rank holds the whole streams and decodes its 1024-aligned word range
+    from paper_1402_4073_b200.shard import shard_range
+    w0, w1 = shard_range(nw, ctx.world, ctx.rank, 1024)
+    t_dir = time.perf_counter()
+    q = bq.RleQuery(dstreams, r, word_range=(w0, w1))
+    t_dir = time.perf_counter() - t_dir
+    out = torch.empty(max(q.out_words, 1), dtype=torch.int64, device=dev)
     pc = torch.zeros(1, dtype=torch.int64, device=dev)
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -566,25 +573,26 @@ def run_c4(args, torch, bq, lib, dev, stream):
     comp_bytes = comp_words * 8
     from oracle import oracle as O
     # parity on a window: the first 2^20 bits of every stream (the generator is sequential, so a
-    # run with r = 2^20 reproduces exactly the prefix of the full stream)
+    # run with r = 2^20 reproduces exactly the prefix of the full stream); rank 0 holds it
     wr = 1 << 20
     wstreams = _markov_streams(lib, n, wr, m1, m0, host_threads())
     t0 = time.perf_counter()
     wexp = O.cdom_threshold(wstreams, wr, t)
     cpu_s = time.perf_counter() - t0
-    exact_window = np.array_equal(out[: wr // 64].cpu().numpy().view(np.uint64), wexp)
+    exact_window = ctx.rank != 0 or np.array_equal(out[: wr // 64].cpu().numpy().view(np.uint64), wexp)
     wbytes = sum(s.size for s in wstreams) * 8
     # K4s moves its tile-sliced layout, not the EWAH words: every 32-bit marker, one
     # 8-byte checkpoint per 128 markers and the output; literal words only at undecided
     # positions (popcount-sized here), so they are left out of the algorithmic bytes
     n_mk, n_lit = q.layout_stats
-    kernel_bytes = (n_mk * 4 + n_mk // 128 * 8 + nw * 8) if n_mk else comp_bytes + nw * 8
+    kernel_bytes = (n_mk * 4 + n_mk // 128 * 8 + q.out_words * 8) if n_mk else comp_bytes + q.out_words * 8
     line = _line("c4", comp_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, kernel_bytes, args.steps,
                  args.warmup,
                  {"workload": "C4: N=1024 RLE (EWAH-style) bitmaps, r=2^30 bits, Markov runs (ones mean 256, zeros "
                               "mean 12544 bits; density 0.02), T=50; output uncompressed; L2 flushed (256 MB read) between launches",
                   "n_bitmaps": n, "r_bits": r, "t": t, "compressed_bytes": comp_bytes,
-                  "uncompressed_equivalent_bytes": n * nw * 8},
+                  "uncompressed_equivalent_bytes": n * nw * 8,
+                  "parallelism": f"word-range shards x{ctx.world}, streams replicated" if ctx.world > 1 else "1 GPU"},
                  {"value_uncompressed_equivalent_gbs": round(n * nw * 8 / (statistics.mean(ms) / 1e3) / 1e9, 1),
                   "popcount": int(pc.item()), "directory_build_s": round(t_dir, 4),
                   "directory_bytes": q.directory_bytes, "host_generation_s": round(t_gen, 2),
@@ -600,36 +608,61 @@ def run_c4(args, torch, bq, lib, dev, stream):
                                    "sample": "oracle cdom_threshold (runmerge.py heap sweep restated in C, single "
                                              f"thread as the reference) on the first 2^20 bits of all 1024 streams "
                                              f"({wbytes} compressed bytes, {cpu_s:.2f} s)"}})
+    line["_rank_bytes"] = comp_bytes * q.out_words / nw  # this rank's share of the query
+    line["_scaling"] = "strong"
     return line
 
 
-def run_c5(args, torch, bq, lib, dev, stream):
-    """Config 5 at one GPU: N=511, r=2^32, p=0.5, T=256 (256 GiB) does not fit in
-    HBM, so it runs as generate -> compute waves of 2^23 words (32 GiB) each;
-    only the query kernels are timed.  Each wave is one GPU's shard at 8 GPUs."""
+def run_c5(args, torch, bq, lib, dev, stream, ctx):
+    """Config 5: N=511, r=2^32, p=0.5, T=256 (256 GiB), sharded by word range over the
+    ranks (8 GPUs: 32 GiB each) with the popcount all-reduced per query.  A rank's
+    shard is processed as generate -> compute waves of at most 2^23 words (32 GiB), so
+    one GPU runs the whole query as 8 waves; only the query kernels (and the
+    all-reduce) are timed."""
+    from paper_1402_4073_b200.shard import shard_range
+
     n, total, t = 511, 1 << 26, 256
-    wave = 1 << 23
+    b, e = shard_range(total, ctx.world, ctx.rank)
+    wave = min(1 << 23, max(e - b, 1))
     pitch = wave + args.pad_words
     data = torch.empty((n, pitch), dtype=torch.int64, device=dev)
     qarr = np.full(n, 32768, dtype=np.uint32)
     out = torch.empty(wave, dtype=torch.int64, device=dev)
     pc = torch.zeros(1, dtype=torch.int64, device=dev)
-    ms_all = []
+    ms_all, rank_ms, pc_total = [], 0.0, 0
     steps = max(1, args.steps // 10)
-    for w0 in range(0, total, wave):
-        _lib_check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, w0, wave, data.data_ptr(), pitch,
+
+    def launch(q):
+        q.threshold(t, out, pc, stream=stream)
+        if ctx.world > 1:
+            ctx.dist.all_reduce(pc)
+
+    for w0 in range(b, e, wave):
+        wl = min(wave, e - w0)
+        _lib_check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, w0, wl, data.data_ptr(), pitch,
                                              stream.cuda_stream))
-        q = bq.ThresholdQuery([data[i, :wave] for i in range(n)], 64 * wave)
-        ms_all += _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), steps,
-                                  1 if w0 else args.warmup, stream)
+        q = bq.ThresholdQuery([data[i, :wl] for i in range(n)], 64 * wl)
+        ms = _timed_launches(torch, lambda: launch(q), steps, 1 if w0 > b else args.warmup, stream)
+        ms_all += ms
+        rank_ms += statistics.mean(ms)
+        pc.zero_()
+        q.threshold(t, out, pc, stream=stream)
+        pc_total += int(pc.item())
         q.close()
     in_bytes_wave = n * wave * 8
     per = statistics.mean(ms_all)
-    return _line("c5", in_bytes_wave / (per / 1e3) / 1e9, ms_all, in_bytes_wave + wave * 8, len(ms_all), args.warmup,
-                 {"workload": "C5 at 1 GPU: N=511, r=2^32 bits, p=0.5, T=256 (256 GiB) as 8 generate->compute "
-                              "waves of 2^23 words (32 GiB, = one GPU's shard at 8 GPUs); kernels timed only",
-                  "n_bitmaps": n, "r_bits": 64 * total, "t": t, "wave_words": wave},
-                 {"full_query_ms_at_1gpu": round(per * total / wave, 3)})
+    line = _line("c5", in_bytes_wave / (per / 1e3) / 1e9, ms_all, in_bytes_wave + wave * 8, len(ms_all),
+                 args.warmup,
+                 {"workload": "C5: N=511, r=2^32 bits, p=0.5, T=256 (256 GiB), word-range shards over the GPUs, each "
+                              "processed as generate->compute waves of <= 2^23 words (32 GiB, one GPU's shard at 8 "
+                              "GPUs); kernels (+ popcount all-reduce) timed only",
+                  "n_bitmaps": n, "r_bits": 64 * total, "t": t, "wave_words": wave,
+                  "parallelism": f"word-range shards x{ctx.world}" if ctx.world > 1 else "1 GPU, 8 waves"},
+                 {"full_query_ms": round(rank_ms, 3), "popcount": pc_total})
+    line["_rank_bytes"] = n * (e - b) * 8
+    line["_rank_ms"] = rank_ms
+    line["_scaling"] = "strong"
+    return line
 
 
 def _lib_check(rc):
@@ -638,21 +671,52 @@ def _lib_check(rc):
 
 
 def run_extra(args):
+    """Workloads c1/c3/c4/c5.  Under torchrun (N > 1): c4 and c5 shard the query by word
+    range (strong scaling); c1 and c3 run one replica per GPU (weak scaling).  The
+    job's value is the bytes all ranks processed over the slowest rank's time."""
+    import types
+
     import torch
+    import torch.distributed as dist
 
     import paper_1402_4073_b200 as bq
     from paper_1402_4073_b200 import _lib
 
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
+    ctx = types.SimpleNamespace(world=world, rank=rank, dist=dist, cpu=(world == 1))
     fn = {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5}[args.workload]
     with ClockSampler(physical_gpu_index(local)) as clocks:
-        line = fn(args, torch, bq, lib, dev, stream)
+        line = fn(args, torch, bq, lib, dev, stream, ctx)
+    rank_bytes = float(line.pop("_rank_bytes", line["roofline"]["algorithmic_bytes_per_launch"]))
+    rank_ms = float(line.pop("_rank_ms", line["roofline"]["mean_launch_ms"]))
+    scaling = line.pop("_scaling", "weak")
+    if world > 1:
+        red = torch.tensor([rank_ms, rank_bytes, float(line.get("popcount", 0))], dtype=torch.float64, device=dev)
+        mx = red.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(red, op=dist.ReduceOp.SUM)
+        job_ms, job_bytes = float(mx[0]), float(red[1])
+        line["n_gpus"] = world
+        line["scaling"] = scaling
+        line["value"] = round(job_bytes / (job_ms / 1e3) / 1e9, 3)
+        line["ms_per_step"] = round(job_ms, 5)
+        if "popcount" in line and args.workload in ("c4", "c5"):
+            line["popcount"] = int(red[2])  # shards: the whole result's popcount
+        line.pop("cpu_baseline", None)  # CPU baseline: rank 0 at N=1 only
     line["clocks"] = clocks.summary()
-    print(json.dumps(line))
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 
