@@ -6,15 +6,15 @@
 // followed by that many literal ("dirty") words; coverage shorter than
 // ceil(r/64) words is an implicit zero tail (bitmaps.py:215-219).
 //
-// K3 rle_directory_kernel -- one warp per stream walks the marker chain once
-//   (inputs are immutable, so the result is cached in the query object).  A
-//   32-word window is loaded coalesced; the chain inside it is followed with
-//   warp shuffles, marker lanes are flagged with a ballot, their word
-//   positions come from a warp prefix sum, and every tile boundary a marker's
-//   run covers is recorded as a directory entry (marker index, run start).
-//   Dirty runs longer than the window are skipped without being loaded.
-//   Malformed streams (truncated literal group, coverage beyond ceil(r/64)
-//   words) raise FormatError like RleBitmap.iter_word_segments (:210-217).
+// K3 the tile directory, once per query object (inputs are immutable):
+//   K3a rle_chain_kernel -- one warp per stream follows the marker chain in
+//   32-word windows (pointer doubling + warp OR-reductions find a window's
+//   markers; windows are cp.async-staged ahead; dirty runs longer than the ring
+//   are skipped unread) and keeps per window only its marker mask and start
+//   position.  K3b rle_dirfill_kernel -- every window in parallel: marker word
+//   positions by a warp prefix sum, the validation of
+//   RleBitmap.iter_word_segments (:210-217; FormatError), and a directory entry
+//   (marker index, run start) for every tile boundary a marker's runs cover.
 //
 // K4 rle_count_kernel -- one CTA per tile of kTileWords output words, the
 //   per-tile form of cdom's run sweep (runmerge.py:198-299):
@@ -90,7 +90,17 @@ __device__ __forceinline__ void rle_fail(const RleDirArgs &a, int code, int stre
 constexpr int kDirAhead = 6;  // windows in flight ahead of the one being decoded
 constexpr int kDirRing = 8;   // ring slots per warp (> kDirAhead: consumed slots are reused late)
 
-__global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constant__ RleDirArgs a) {
+// K3a: the sequential part of the directory -- one warp per stream follows its
+// marker chain window by window (windows copied into a per-warp ring by per-lane
+// cp.async, kDirAhead ahead; a literal group reaching past the ring restarts it
+// at the next marker, so long dirty runs are skipped unread).  Inside a window
+// the markers reachable from the entry marker come from pointer doubling (each
+// lane's successor j + 1 + dirty, squared five times, one warp OR-reduction per
+// level), and only two facts per window are kept: its marker mask and the word
+// position where its first marker's fill starts.  Everything else -- marker
+// positions, validation, directory rows -- is K3b, in parallel over all windows.
+__global__ void __launch_bounds__(128) rle_chain_kernel(const __grid_constant__ RleDirArgs a, const uint64_t *wbase,
+                                                        uint32_t *wreach, uint64_t *wpos) {
     __shared__ uint64_t ring_all[4][kDirRing][32];
     const int lane = threadIdx.x & 31;
     const int stream = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -99,9 +109,7 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
     const uint64_t *s = a.ptrs[stream];
     const uint64_t L = a.lens[stream];
     uint2 *dir = a.dir + stream;  // stride n between tiles
-    // Window q (words [32q, 32q + 32)) is copied into ring slot q % kDirRing by
-    // per-lane 8-byte cp.async, kDirAhead windows ahead of the decode; each lane
-    // reads back only the word it copied, so its own wait_group suffices.
+    const uint64_t wb = wbase[stream];
     auto issue = [&](uint64_t q) {
         const uint64_t idx = q * 32 + lane;
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ring[q % kDirRing][lane]);
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
     uint64_t next = 0;  // stream index of the next marker
     uint64_t pos = 0;   // word position where its fill run starts
     for (int q = 0; q < kDirAhead; ++q) issue(q);
-    for (uint32_t step = 0; next < L; ++step) {
+    while (next < L) {
         const uint64_t kk = next / 32;
         if (kk >= k + kDirAhead) {  // a long literal group: restart the pipeline at the next marker
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -126,12 +134,7 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kDirAhead - 1) : "memory");
         const uint64_t w = ring[k % kDirRing][lane];
         const uint64_t bc = k * 32;
-        const uint64_t idx = bc + lane;
-        const uint64_t run = (w >> 1) & 0xFFFFFFFFull;
         const uint64_t dirty = w >> 33;
-        // markers reachable from the entry marker: each lane's successor if it were a
-        // marker (window-relative, 32 = outside), squared five times by pointer doubling
-        // with one warp OR-reduction per level
         uint32_t j = dirty < 32 ? min((uint32_t)lane + 1 + (uint32_t)dirty, 32u) : 32u;
         uint32_t reach = 1u << (uint32_t)(next - bc);
 #pragma unroll
@@ -144,44 +147,72 @@ __global__ void __launch_bounds__(128) rle_directory_kernel(const __grid_constan
             }
         }
         reach &= (L - bc >= 32) ? 0xffffffffu : ((1u << (uint32_t)(L - bc)) - 1u);
-        next = __shfl_sync(0xffffffffu, idx + 1 + dirty, 31 - __clz(reach));
-        const bool is_m = (reach >> lane) & 1u;
-        const uint64_t span = is_m ? run + dirty : 0ull;
-        // exclusive prefix sum of spans over marker lanes
-        uint64_t incl = span;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
+        next = __shfl_sync(0xffffffffu, bc + lane + 1 + dirty, 31 - __clz(reach));
+        // words covered by the window's markers (each span < 2^40: split sums stay exact)
+        const uint64_t span = ((reach >> lane) & 1u) ? ((w >> 1) & 0xFFFFFFFFull) + dirty : 0ull;
+        const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)(span & 0xFFFFFFu));
+        const uint32_t hi = __reduce_add_sync(0xffffffffu, (uint32_t)(span >> 24));
+        if (lane == 0) {
+            wreach[wb + k] = reach;
+            wpos[wb + k] = pos;
         }
-        const uint64_t start = pos + incl - span;
-        const uint64_t end = start + span;
-        if (is_m) {
-            if (idx + 1 + dirty > L) rle_fail(a, RLE_ERR_TRUNCATED, stream);
-            if (end > a.total_words) rle_fail(a, RLE_ERR_OVERLONG, stream);
-            // bits >= r in the last word are invalid (bitmaps.py:70-72 via decompress :428-431)
-            if (a.tail_mask && end == a.total_words && span) {
-                const uint64_t fe = start + run;
-                if (fe == end) {
-                    if ((w & 1) && run) rle_fail(a, RLE_ERR_BEYOND_R, stream);
-                } else if (idx + 1 + dirty <= L && (__ldg(s + idx + dirty) & ~a.tail_mask)) {
-                    rle_fail(a, RLE_ERR_BEYOND_R, stream);
-                }
-            }
-            // record every tile boundary b with start <= b < end that the range's rows cover
-            const uint64_t r0 = (uint64_t)a.tile0 * kRleTile, r1 = (uint64_t)(a.tile0 + a.nrows) * kRleTile;
-            uint64_t b = max((start + kRleTile - 1) / kRleTile * kRleTile, r0);
-            for (; b < end && b < a.total_words && b < r1; b += kRleTile)
-                dir[(b / kRleTile - a.tile0) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
-        }
-        pos += __shfl_sync(0xffffffffu, incl, 31);
-        if ((step & 63) == 63 && *((volatile int *)a.err)) break;
+        pos += ((uint64_t)hi << 24) + lo;
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // tiles past the encoded coverage: stream exhausted, implicit zero tail
     const uint64_t t0 = max((pos + kRleTile - 1) / kRleTile, (uint64_t)a.tile0);
     for (uint64_t t = t0 + lane; t < (uint64_t)a.tile0 + a.nrows; t += 32)
         dir[(t - a.tile0) * a.n] = make_uint2((uint32_t)L, (uint32_t)pos);
+}
+
+// K3b: every window with markers, in parallel (grid.y = stream): marker word
+// positions by a warp prefix sum from the window's start position, validation as
+// RleBitmap.iter_word_segments / decompress (bitmaps.py:196-219, :428-431), and
+// the directory row of every tile boundary a marker's runs cover.
+__global__ void __launch_bounds__(128) rle_dirfill_kernel(const __grid_constant__ RleDirArgs a, const uint64_t *wbase,
+                                                          const uint32_t *wreach, const uint64_t *wpos) {
+    const int lane = threadIdx.x & 31;
+    const int stream = blockIdx.y;
+    const uint64_t *s = a.ptrs[stream];
+    const uint64_t L = a.lens[stream];
+    uint2 *dir = a.dir + stream;
+    const uint64_t nwin = (L + 31) / 32, wb = wbase[stream];
+    const uint64_t r0 = (uint64_t)a.tile0 * kRleTile, r1 = (uint64_t)(a.tile0 + a.nrows) * kRleTile;
+    for (uint64_t k = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5); k < nwin; k += (uint64_t)gridDim.x * 4) {
+        const uint32_t reach = wreach[wb + k];
+        if (!reach) continue;  // a window inside a literal group
+        const uint64_t pos = wpos[wb + k];
+        const uint64_t idx = k * 32 + lane;
+        const uint64_t w = idx < L ? __ldg(s + idx) : 0ull;
+        const uint64_t run = (w >> 1) & 0xFFFFFFFFull;
+        const uint64_t dirty = w >> 33;
+        const bool is_m = (reach >> lane) & 1u;
+        const uint64_t span = is_m ? run + dirty : 0ull;
+        uint64_t incl = span;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (!is_m) continue;
+        const uint64_t start = pos + incl - span;
+        const uint64_t end = start + span;
+        if (idx + 1 + dirty > L) rle_fail(a, RLE_ERR_TRUNCATED, stream);
+        if (end > a.total_words) rle_fail(a, RLE_ERR_OVERLONG, stream);
+        // bits >= r in the last word are invalid (bitmaps.py:70-72 via decompress :428-431)
+        if (a.tail_mask && end == a.total_words && span) {
+            const uint64_t fe = start + run;
+            if (fe == end) {
+                if ((w & 1) && run) rle_fail(a, RLE_ERR_BEYOND_R, stream);
+            } else if (idx + 1 + dirty <= L && (__ldg(s + idx + dirty) & ~a.tail_mask)) {
+                rle_fail(a, RLE_ERR_BEYOND_R, stream);
+            }
+        }
+        // record every tile boundary b with start <= b < end that the range's rows cover
+        uint64_t b = max((start + kRleTile - 1) / kRleTile * kRleTile, r0);
+        for (; b < end && b < a.total_words && b < r1; b += kRleTile)
+            dir[(b / kRleTile - a.tile0) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
+    }
 }
 
 struct RleCountArgs {
@@ -592,16 +623,41 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
         a.dir = q->d_dir;
         a.err = d_err;
         a.err_stream = d_err_stream;
-        const int warps_per_block = 4;
-        rle_directory_kernel<<<(n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block>>>(a);
-        e = cudaGetLastError();
+        // window bookkeeping for K3a -> K3b: per stream ceil(L / 32) windows
+        std::vector<uint64_t> wbase(n + 1, 0);
+        uint64_t maxwin = 0;
+        for (int i = 0; i < n; ++i) {
+            const uint64_t nwin = (lens[i] + 31) / 32;
+            wbase[i + 1] = wbase[i] + nwin;
+            maxwin = std::max(maxwin, nwin);
+        }
+        const uint64_t nwin_all = wbase[n];
+        char *scratch = nullptr;
+        e = cudaMalloc(&scratch, (size_t)(n + 1) * 8 + nwin_all * 12 + 16);
+        uint64_t *d_wbase = reinterpret_cast<uint64_t *>(scratch);
+        uint64_t *d_wpos = d_wbase + n + 1;
+        uint32_t *d_wreach = reinterpret_cast<uint32_t *>(d_wpos + nwin_all);
+        if (e == cudaSuccess) e = cudaMemcpy(d_wbase, wbase.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemset(d_wreach, 0, nwin_all * 4 + 4);
+        if (e == cudaSuccess) {
+            const int warps_per_block = 4;
+            rle_chain_kernel<<<(n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block>>>(a, d_wbase, d_wreach,
+                                                                                                d_wpos);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess && nwin_all) {
+            const unsigned gx = (unsigned)std::min<uint64_t>((maxwin + 3) / 4, 64);
+            rle_dirfill_kernel<<<dim3(gx, (unsigned)n), 128>>>(a, d_wbase, d_wreach, d_wpos);
+            e = cudaGetLastError();
+        }
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (scratch) cudaFree(scratch);
         int herr[4] = {0, 0, 0, 0};
         if (e == cudaSuccess) e = cudaMemcpy(herr, d_err, 16, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) {
             cudaFree(q->mem);
             delete q;
-            return cuda_error(e, "rle_directory_kernel");
+            return cuda_error(e, "rle directory (K3)");
         }
         if (herr[0]) {
             unsigned long long bad = (unsigned long long)(uint32_t)herr[2] | ((unsigned long long)(uint32_t)herr[3] << 32);
