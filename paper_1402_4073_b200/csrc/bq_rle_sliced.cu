@@ -54,8 +54,10 @@ __device__ __forceinline__ uint32_t mk_dirty(uint32_t m) { return m >> 16; }
 __device__ __forceinline__ uint32_t mk_pack(uint32_t bit, uint32_t run, uint32_t dirty) { return run | (bit << 11) | (dirty << 16); }
 
 // ---------------------------------------------------------------------------
-// Layout build.  Thread k handles slice (tile k % ntiles, stream k / ntiles):
-// neighbouring threads walk neighbouring tiles of one stream (nearby words).
+// Layout build, one thread per (tile, stream) slice.  The counting pass maps
+// neighbouring threads to neighbouring tiles of one stream (their reads are
+// adjacent); the emitting pass to neighbouring streams of one tile (their writes
+// are adjacent in the tile-major output): 0.9 + 3.0 ms at C4 instead of 0.9 + 5.3.
 
 struct SliceSink {
     uint32_t *mk;       // tile marker array (null: count only)
@@ -112,7 +114,7 @@ __global__ void slice_count_kernel(const uint64_t *const *ptrs, const uint64_t *
                                    uint32_t tile0, uint32_t ntiles, uint64_t *counts) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(k / ntiles);
+        const int s = (int)(k / ntiles);  // neighbouring threads: neighbouring tiles of one stream (reads)
         const uint32_t t = (uint32_t)(k % ntiles);
         const uint2 c =
             slice_walk<false>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)(tile0 + t) * kRleTile, SliceSink{});
@@ -154,8 +156,8 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
                                   uint32_t *markers, uint64_t *literals, uint64_t *meta) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(k / ntiles);
-        const uint32_t t = (uint32_t)(k % ntiles);
+        const int s = (int)(k % n);  // neighbouring threads: neighbouring slices of one tile (writes)
+        const uint32_t t = (uint32_t)(k / n);
         const uint64_t o = offs[(size_t)t * n + s];
         SliceSink sink;
         sink.mk = markers + mbase[t];
