@@ -45,20 +45,17 @@
 
 namespace bq {
 
-constexpr int kRleThreads = 256;
 constexpr int kSlotsPerBatch = 256;   // undecided words resolved per phase-C pass
 constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
 constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
 constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
-constexpr int kSlotsUnstaged = 64;      // phase-C batch when nothing is staged (keeps L1 large)
 constexpr size_t phase_c_bytes(int slots) { return (size_t)slots * 128 + (size_t)kRleTile * 4 + (size_t)slots * 2; }
 constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * 2 * kPoolWords * 8;
 constexpr size_t kRegionBytes = kPoolBytes > phase_c_bytes(kSlotsPerBatch) ? kPoolBytes : phase_c_bytes(kSlotsPerBatch);
 
-inline size_t rle_smem_bytes(bool staged, int n) {
-    (void)n;
-    return kCntBytes + (staged ? kRegionBytes : phase_c_bytes(kSlotsUnstaged));
+inline size_t rle_smem_bytes() {
+    return kCntBytes + kRegionBytes;
 }
 
 enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };
@@ -253,11 +250,6 @@ __device__ __forceinline__ void walk_tile(const RleCountArgs &a, int st, uint32_
     }
 }
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 // Marker sweep of one stream over a tile of W words in 32-bit tile-relative
 // coordinates.  src[0] is the marker named by the stream's directory entry
@@ -317,27 +309,17 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
     if (carry) atomicAdd(&cnt[rel], carry);  // stream ended inside the tile
 }
 
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
 
-// Phase A strategies.
-//  STAGED (default): warp-private, double-buffered staging.  Lane l of warp w
-//    owns stream k*NT + 32w + l of batch k.  It computes its stream's segment for
-//    this tile (directory entry -> marker covering the next tile boundary,
-//    widened to 16-byte alignment), claims room in the warp's pool with a warp
-//    prefix sum, and copies the segment with cp.async.cg while the previous
-//    batch is being walked.  Each lane waits only for its own copies, so the
-//    warps never meet at a CTA barrier in phase A; __syncwarp guards pool reuse.
-//    A segment that does not fit the pool is walked straight from HBM.
-//  !STAGED: every lane walks its streams directly from global memory (kept for
-//    A/B measurement, BQ_RLE_STAGED=0).
-template <bool STAGED>
-__global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED ? 4 : 6)
-    rle_count_kernel(const __grid_constant__ RleCountArgs a) {
-    constexpr int NT = STAGED ? kStagedThreads : kRleThreads;
-    constexpr int kSlots = STAGED ? kSlotsPerBatch : kSlotsUnstaged;
+// Phase A: warp-private, double-buffered staging.  Lane l of warp w owns stream
+// k*NT + 32w + l of batch k.  It computes its stream's segment for this tile
+// (directory entry -> marker covering the next tile boundary, widened to 16-byte
+// alignment), claims room in the warp's pool with a warp prefix sum, and copies
+// the segment with one TMA bulk copy while the previous batch is being walked;
+// one mbarrier per pool half, so the warps never meet at a CTA barrier in phase
+// A.  A segment that does not fit the pool is walked straight from HBM.
+__global__ void __launch_bounds__(kStagedThreads, 4) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
+    constexpr int NT = kStagedThreads;
+    constexpr int kSlots = kSlotsPerBatch;
     extern __shared__ __align__(16) uint8_t rle_smem[];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);  // [kRleTile + 4] packed (ones | dirty << 16)
     uint8_t *region = rle_smem + kCntBytes;                  // phase A: warp pools; phases B/C: tile_resolve
@@ -357,27 +339,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedThreads : kRleThreads, STAGED 
     __syncthreads();
 
     // ---- A: run sweep over markers only -> difference array ------------------
-    if constexpr (!STAGED) {
-        // high occupancy, no staging: the next stream's segment is prefetched into
-        // L2 while the current one is walked, so marker loads are L2 hits and
-        // thousands of independent chains per SM hide their latency.
-        auto prefetch = [&](int st) {
-            const uint64_t L = a.lens[st];
-            const uint32_t first = a.dir[(size_t)tile * a.n + st].x;
-            if (first >= L) return;
-            const uint64_t next = a.dir[(size_t)(tile + 1) * a.n + st].x;  // row tile + 1 always exists
-            const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.ptrs[st] + first) & ~(uintptr_t)127;
-            const uintptr_t p1 = reinterpret_cast<uintptr_t>(a.ptrs[st] + min(next + 1, L));
-            for (uintptr_t p = p0; p < p1; p += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-        };
-        if (tid < n) prefetch(tid);
-        for (int st = tid; st < n; st += NT) {
-            if (st + NT < n) prefetch(st + NT);
-            const uint2 e = a.dir[(size_t)tile * a.n + st];
-            const uint64_t L = a.lens[st];
-            if (e.x < L) sweep_stream<true>(a.ptrs[st] + e.x, (uint32_t)(L - e.x), e.y, ts, width, cnt, a.four);
-        }
-    } else {
+    {
         // directory metadata of a lane's stream in batch k (tile-major rows: coalesced),
         // fetched one batch ahead of use so its latency hides behind a walk
         struct Pre {
@@ -734,10 +696,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.out = d_out;
     a.popcnt = d_popcnt;
     a.four = 4;
-    // BQ_RLE_STAGED=0 selects the unstaged phase A (A/B measurement)
-    static const char *env = getenv("BQ_RLE_STAGED");
-    const bool staged = !(env && env[0] == '0');
-    const size_t smem = rle_smem_bytes(staged, n);
+    const size_t smem = rle_smem_bytes();
     static const char *dbg = getenv("BQ_RLE_DEBUG");
     a.debug = dbg ? atoi(dbg) : 0;
     // Tile-sliced layout policy (BQ_RLE_SLICED): "0" never; "1" build at the first
@@ -751,7 +710,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         // SPEC.md:269-270): the layout is built once, under the query's lock
         std::lock_guard<std::mutex> guard(q->build_mu);
         ++q->evals;
-        if (staged && sliced_mode && !q->sliced_tried && q->evals >= sliced_mode) {
+        if (sliced_mode && !q->sliced_tried && q->evals >= sliced_mode) {
             q->sliced_tried = true;
             e = cudaStreamSynchronize(s);  // the build runs on the legacy stream
             if (e != cudaSuccess) {
@@ -766,7 +725,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         }
         sliced = q->sliced;
     }
-    if (sliced.mem && staged && sliced_mode) {
+    if (sliced.mem && sliced_mode) {
         SlicedEval se;
         se.n = n;
         se.total_words = q->total_words;
@@ -781,12 +740,9 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         rc = launch_sliced(sliced, se, s);
         cudaFreeAsync(d_tab, s);
         return rc;
-    } else if (staged) {
-        e = cudaFuncSetAttribute(rle_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) rle_count_kernel<true><<<q->ntiles, kStagedThreads, smem, s>>>(a);
     } else {
-        e = cudaFuncSetAttribute(rle_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) rle_count_kernel<false><<<q->ntiles, kRleThreads, smem, s>>>(a);
+        e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) rle_count_kernel<<<q->ntiles, kStagedThreads, smem, s>>>(a);
     }
     if (e != cudaSuccess) {
         cudaFreeAsync(d_tab, s);

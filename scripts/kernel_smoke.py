@@ -1,7 +1,7 @@
-"""Exercise every libbq kernel family on small inputs (run with BQ_RLE_STAGED=1
-and =0 for both K4 phase-A strategies):
-K1/K2 (all epilogues, ragged inputs, word ranges), K3/K4 (staged and unstaged
-phase A, phase C), the device encoder, set algebra, the program JIT, the host
+"""Exercise every libbq kernel family on small inputs (run with BQ_RLE_SLICED=1
+and =0 for both RLE paths, K4s and K4):
+K1/K2 (all epilogues, ragged inputs, word ranges), K3/K4/K4s (phase C
+included), the device encoder, set algebra, the program JIT, the host
 streaming path and the membership kernels.  Exits 0 when every result matches
 the CPU oracle."""
 
@@ -60,7 +60,7 @@ def main():
         k = ctypes.c_uint64(0)
         assert lib.bq_gen_markov_rle(5, i, r, 40.0, 200.0, buf.ctypes.data, cap, ctypes.byref(k)) == 0
         streams.append(buf[: k.value].copy())
-    for _ in range(1):  # phase-A strategy chosen by BQ_RLE_STAGED (read once by the library)
+    for _ in range(1):
         rq = bq.RleQuery([bq.DeviceRleBitmap(dev(s), r) for s in streams], r)
         for t in (1, 3, n):
             out, _ = rq.threshold(t)
