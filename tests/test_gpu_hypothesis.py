@@ -103,3 +103,35 @@ def test_threshold_and_symmetric_rle(bq, inst):
     exp_s = O.cdom_symmetric(comp, r, accept)
     assert got_t.words == O.rle_compress(O.trim(exp_t), r).tolist()
     assert got_s.words == O.rle_compress(O.trim(exp_s), r).tolist()
+
+
+@SETTINGS
+@given(instances())
+def test_rle_both_paths_device_query(bq, inst):
+    """The same random instance through K4 (BQ_RLE_SLICED=0) and K4s (=1), device
+    streams, threshold and symmetric."""
+    import os
+
+    arrs, bits, r, t, accept = inst
+    comp = [O.rle_compress(a, b) for a, b in zip(arrs, bits)]
+    dev = [torch.from_numpy(c.view(np.int64)).cuda() if c.size else torch.zeros(1, dtype=torch.int64, device="cuda")
+           for c in comp]
+    streams = [bq.DeviceRleBitmap(d, b, c.size) for d, b, c in zip(dev, bits, comp)]
+    nw = (r + 63) // 64
+    exp_t = O.cdom_threshold(comp, r, t)
+    exp_s = O.cdom_symmetric(comp, r, accept)
+    prev = os.environ.get("BQ_RLE_SLICED")
+    try:
+        for mode in ("0", "1"):
+            os.environ["BQ_RLE_SLICED"] = mode
+            q = bq.RleQuery(streams, r)
+            out, pc = q.threshold(t)
+            assert np.array_equal(out[:nw].cpu().numpy().view(np.uint64), exp_t), mode
+            out, pc = q.symmetric(accept)
+            assert np.array_equal(out[:nw].cpu().numpy().view(np.uint64), exp_s), mode
+            q.close()
+    finally:
+        if prev is None:
+            os.environ.pop("BQ_RLE_SLICED", None)
+        else:
+            os.environ["BQ_RLE_SLICED"] = prev
