@@ -164,7 +164,10 @@ BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q);
 BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals);
 
 /* Threshold / symmetric function over the compressed inputs, output
- * uncompressed (ceil(r/64) words).  Replaces runmerge.cdom_threshold
+ * uncompressed (bq_rle_query_out_words(q) words: ceil(r/64), or the query's
+ * word range), popcount ADDED to d_popcnt (optional).  Asynchronous on
+ * `stream`, except the evaluation that builds the tile-sliced layout, which
+ * synchronizes first.  Replaces runmerge.cdom_threshold
  * (runmerge.py:198-241) and runmerge.cdom_symmetric (:244-299): one-fills
  * count for whole tiles of words, zero-fills are skipped, and dirty words are
  * read only where the fills leave the outcome open. */

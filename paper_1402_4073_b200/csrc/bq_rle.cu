@@ -682,7 +682,10 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     cudaError_t e = cudaMallocAsync(&d_tab, bytes, s);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(accept)");
     e = cudaMemcpyAsync(d_tab, host.data(), bytes, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync(accept)");
+    if (e != cudaSuccess) {
+        cudaFreeAsync(d_tab, s);
+        return cuda_error(e, "cudaMemcpyAsync(accept)");
+    }
     RleCountArgs a;
     a.ptrs = q->d_ptrs;
     a.lens = q->d_lens;
