@@ -14,6 +14,7 @@
 // Kernels: classify + flag -> compact change points (CUB) -> per-marker sizes
 // -> scan (CUB) -> scatter markers and literal words.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -96,7 +97,7 @@ extern "C" BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_w
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // scratch: flags (u8), idx iterator output cp (u32), n_cp, sizes (u32), offs (u64), cub temp
     size_t t_sel = 0, t_scan = 0;
-    cub::CountingInputIterator<uint32_t> it(0);
+    thrust::counting_iterator<uint32_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, t_sel, it, (uint8_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                (int)total, s);
     cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (uint32_t *)nullptr, (uint64_t *)nullptr, (int)total, s);
