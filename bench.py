@@ -571,6 +571,32 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
     pc.zero_()
     q.threshold(t, out, pc, stream=stream)
     comp_bytes = comp_words * 8
+    # one-shot end to end through the public API from pinned host memory: upload the
+    # compressed streams, build the query (K3 directory), one evaluation (K4), result
+    # words back to the host -- what a drop-in cdom call on fresh host data costs
+    e2e_line = None
+    if not args.no_e2e and ctx.world == 1:
+        host_out = torch.empty(max(q.out_words, 1), dtype=torch.int64, pin_memory=True)
+        e2e_s = []
+        for _ in range(4):
+            torch.cuda.synchronize()
+            t_e = time.perf_counter()
+            d2 = flat.to(dev, non_blocking=True)
+            ds2 = [bq.DeviceRleBitmap(d2[a:a + b] if b else d2[:0], r, b) for a, b in offs]
+            q2 = bq.RleQuery(ds2, r)
+            o2, p2 = q2.threshold(t)
+            host_out.copy_(o2[: q2.out_words], non_blocking=True)
+            p2_host = int(p2.item())
+            torch.cuda.synchronize()
+            e2e_s.append(time.perf_counter() - t_e)
+            q2.close()
+            del d2, ds2, o2
+        e2e_best = statistics.median(e2e_s[1:])
+        e2e_line = {"value": round(comp_bytes / e2e_best / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": comp_bytes, "d2h_bytes_per_step": q.out_words * 8 + 8,
+                    "ms_per_step": round(e2e_best * 1e3, 3), "steps": len(e2e_s) - 1,
+                    "api": "torch pinned H2D -> engine.RleQuery (bq_rle_query_create: K3) -> threshold (K4) -> D2H",
+                    "matches_device_result": bool(p2_host == int(pc.item()))}
     from oracle import oracle as O
     # parity on a window: the first 2^20 bits of every stream (the generator is sequential, so a
     # run with r = 2^20 reproduces exactly the prefix of the full stream); rank 0 holds it
@@ -603,6 +629,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
                                     "note": "value = EWAH input bytes / kernel time; roofline = bytes K4s moves "
                                             "(32-bit markers + checkpoints + output)"},
                   "first_eval_s": first_evals_s[0], "second_eval_with_slice_build_s": first_evals_s[1],
+                  "e2e": e2e_line,
                   "matches_oracle_window": bool(exact_window),
                   "cpu_baseline": {"value": round(wbytes / cpu_s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
                                    "sample": "oracle cdom_threshold (runmerge.py heap sweep restated in C, single "
