@@ -386,10 +386,15 @@ def decompress(bitmap):
 
 def compress(bitmap):
     """bitmaps.compress (bitmaps.py:407-414): canonical encoding, returns RleBitmap
-    (the reference class if the input is a reference object)."""
-    words = host_words(bitmap) if not isinstance(bitmap, DeviceBitmap) else bitmap.to_numpy()
-    enc = compress_words(words, bitmap.bit_length)
-    return _sibling_class(bitmap, "RleBitmap", RleBitmap)(enc, bitmap.bit_length)
+    (the reference class if the input is a reference object).  Encoded on the
+    device (K7, bq_rle_encode_device); only the stream comes back to the host.
+    (``compress_words``, the host encoder, serves the bitmap-type constructors.)"""
+    k = kind_of(bitmap)
+    if k not in ("u", "du"):
+        raise InputError("compress needs an uncompressed bitmap")
+    b = to_device(bitmap)
+    enc = encode_device(b.data[: b.n_words], b.bit_length)
+    return _sibling_class(bitmap, "RleBitmap", RleBitmap)(enc.tolist(), bitmap.bit_length)
 
 
 def to_device(bitmap, device=None):
