@@ -96,6 +96,8 @@ struct SlicedEval {
     uint64_t last_mask;
     const uint32_t *accept_bits;
     const uint32_t *const_until;
+    const uint32_t *breaks;  // counts where accept[] changes; nbreak = -1: too many
+    int nbreak;
     uint64_t *out;
     unsigned long long *popcnt;
     int debug;

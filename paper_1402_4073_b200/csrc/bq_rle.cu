@@ -222,6 +222,8 @@ struct RleCountArgs {
     uint64_t last_mask;
     const uint32_t *accept_bits;  // (n + 1) bits
     const uint32_t *const_until;  // [n + 1]: largest j >= k with accept[k..j] constant
+    const uint32_t *breaks;       // counts where accept[] changes (phase C's bit-sliced decisions)
+    int nbreak;                   // their number, -1 when there are too many
     uint64_t *out;
     unsigned long long *popcnt;
     int debug;  // experiment knob (BQ_RLE_DEBUG): 1 = skip marker walks, 2 = also skip copies
@@ -459,13 +461,14 @@ __global__ void __launch_bounds__(kStagedThreads, 4) rle_count_kernel(const __gr
 
     // ---- B: prefix sum, then decide every word the fills decide ------------------
     const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
-    TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile};
+    TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile,
+                 a.breaks, a.nbreak};
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlots>());
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
 
     // ---- C: read dirty literals only where the fills leave the outcome open ----
-    pc += tile_resolve<NT, kSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &add_bits) {
+    pc += tile_resolve<NT, kSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &&add_bits) {
         for (int st = tid; st < a.n; st += NT) {
             walk_tile(a, st, tile, ts, te,
                       [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit, const uint64_t *s) {
@@ -676,6 +679,14 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     uint32_t *cu = host.data() + nbits_words;
     cu[n] = (uint32_t)n;
     for (int k = n - 1; k >= 0; --k) cu[k] = (acc[k] == acc[k + 1]) ? cu[k + 1] : (uint32_t)k;
+    // breakpoints b (accept[b] != accept[b - 1]): phase C decides 64 bits per comparison
+    constexpr int kMaxTileBreaks = 64;
+    std::vector<uint32_t> brk;
+    for (int b = 1; b <= n; ++b)
+        if (acc[b] != acc[b - 1]) brk.push_back((uint32_t)b);
+    const int nbreak = brk.size() <= (size_t)kMaxTileBreaks ? (int)brk.size() : -1;
+    const size_t brk_off = host.size();
+    if (nbreak > 0) host.insert(host.end(), brk.begin(), brk.end());
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     void *d_tab = nullptr;
     const size_t bytes = host.size() * 4;
@@ -696,6 +707,8 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.last_mask = (q->r_bits % W) ? ((1ull << (q->r_bits % W)) - 1) : ~0ull;
     a.accept_bits = static_cast<const uint32_t *>(d_tab);
     a.const_until = static_cast<const uint32_t *>(d_tab) + nbits_words;
+    a.breaks = static_cast<const uint32_t *>(d_tab) + brk_off;
+    a.nbreak = nbreak;
     a.out = d_out;
     a.popcnt = d_popcnt;
     a.four = 4;
@@ -737,6 +750,8 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         se.last_mask = a.last_mask;
         se.accept_bits = a.accept_bits;
         se.const_until = a.const_until;
+        se.breaks = a.breaks;
+        se.nbreak = a.nbreak;
         se.out = d_out;
         se.popcnt = d_popcnt;
         se.debug = a.debug;

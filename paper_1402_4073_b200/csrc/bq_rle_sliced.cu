@@ -310,14 +310,15 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
 
     // ---- B: prefix sum, then decide every word the fills decide ------------------
     const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
-    TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out, (uint64_t)E.tile0 * kRleTile};
+    TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out, (uint64_t)E.tile0 * kRleTile,
+                 E.breaks, E.nbreak};
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlSlots>());
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
 
     // ---- C: literal bits of undecided words (chunks decoded again, literals from HBM) --
     pc += tile_resolve<NT, kSlSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of,
-                                                                                 auto &add_bits) {
+                                                                                 auto &&add_bits) {
         for (uint32_t c = warp; c < nchunks; c += NT / 32) {
             const uint64_t cm = __ldg(meta + c);
             const uint4 v = __ldg(reinterpret_cast<const uint4 *>(tmk) + c * 32 + lane);

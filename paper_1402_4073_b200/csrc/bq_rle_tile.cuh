@@ -22,6 +22,8 @@ struct TileDecide {
     const uint32_t *const_until;  // [n + 1]: largest j >= k with accept[k..j] constant
     uint64_t *out;                // word g of the result is out[g - out_first]
     uint64_t out_first;           // first word of the query's range (a multiple of kRleTile)
+    const uint32_t *breaks;       // ascending counts b where accept[b] != accept[b - 1]
+    int nbreak;                   // their number, or -1 (too many: decide bit by bit)
 };
 
 // Warp inclusive prefix sum.  The shuffle's own in-range predicate guards the add
@@ -98,59 +100,177 @@ __device__ __forceinline__ unsigned long long tile_decide(const TileDecide &d, c
     return pc;
 }
 
-// Phase C shared memory: [SLOTS][32] packed bit counters | slot_of[kRleTile] | slot_word[SLOTS].
+// Phase C shared memory: slot_of[kRleTile] | slot_word[SLOTS] | soff[SLOTS + 1] |
+// sfill[SLOTS] | entries[CAP] (64-bit literal words, grouped by slot).
+constexpr int kResolveCap = 4096;
 template <int SLOTS>
 constexpr size_t tile_resolve_bytes() {
-    return (size_t)SLOTS * 128 + (size_t)kRleTile * 2 + (size_t)SLOTS * 2;
+    return (size_t)kRleTile * 2 + (size_t)SLOTS * 2 + (size_t)(SLOTS + 4) * 4 + (size_t)SLOTS * 4 +
+           (size_t)kResolveCap * 8;
 }
 
-// Phase C, in batches of SLOTS undecided words: count_bits(slot_of, add_bits) is
-// called by every thread between barriers and must call add_bits(slot, word)
-// for every literal word whose tile position p has slot_of[p] != kNoSlot.
+// Bit-sliced sum of n literal words into M planes (plane j = bit j of the 64 counts).
+template <int M>
+__device__ __forceinline__ void planes_sum(const uint64_t *lits, uint32_t n, uint64_t (&c)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = 0ull;
+    for (uint32_t i = 0; i < n; ++i) {
+        uint64_t carry = lits[i];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const uint64_t t = c[j] & carry;
+            c[j] ^= carry;
+            carry = t;
+        }
+    }
+}
+
+// count >= k per bit position, for the bit-sliced count c (planes 0..15), k a runtime value
+__device__ __forceinline__ uint64_t planes_ge(const uint64_t (&c)[16], uint32_t k) {
+    if (k >= (1u << 16)) return 0ull;
+    uint64_t gt = 0ull, eq = ~0ull;
+#pragma unroll
+    for (int j = 15; j >= 0; --j) {
+        const uint64_t kb = 0ull - (uint64_t)((k >> j) & 1u);
+        gt |= eq & c[j] & ~kb;
+        eq &= ~(c[j] ^ kb);
+    }
+    return gt | eq;
+}
+
+// Result word of an undecided position: accept[ones + count_b] for each bit b.
+__device__ __forceinline__ uint64_t decide_word(const TileDecide &d, uint32_t ones, uint32_t dirty,
+                                                const uint64_t (&c)[16]) {
+    if (d.nbreak >= 0) {  // accept(ones + k) = accept(ones) ^ sum over breakpoints b in (ones, ones + dirty] of [k >= b - ones]
+        uint64_t w = accept_at(d.accept_bits, ones) ? ~0ull : 0ull;
+        for (int i = 0; i < d.nbreak; ++i) {
+            const uint32_t b = __ldg(d.breaks + i);
+            if (b <= ones) continue;
+            if (b > ones + dirty) break;
+            w ^= planes_ge(c, b - ones);
+        }
+        return w;
+    }
+    uint64_t w = 0;
+    for (int bit = 0; bit < 64; ++bit) {
+        uint32_t cb = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cb |= (uint32_t)((c[j] >> bit) & 1u) << j;
+        if (accept_at(d.accept_bits, ones + cb)) w |= 1ull << bit;
+    }
+    return w;
+}
+
+// Phase C.  count_bits(slot_of, add) is called by every thread between barriers and
+// must call add(slot, word) for every literal word whose tile position p has
+// slot_of[p] != kNoSlot.  Undecided words are taken in batches whose literal words
+// (their dirty counts are known from phase B) fit the entries buffer; add() files
+// each literal word under its slot, and then one thread per slot sums them into
+// bit-sliced counters in registers (a ripple of a few planes per word -- no
+// atomics, no per-bit loop) and decides all 64 bits with bit-sliced comparisons
+// against the accept vector's breakpoints.  A word with more dirty inputs than the
+// buffer holds is resolved alone by atomic ripple-adds into shared planes.
 template <int NT, int SLOTS, class CountBits>
 __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, const uint32_t *cnt,
                                                            const uint16_t *undecided, uint32_t nu, uint8_t *region,
                                                            CountBits &&count_bits) {
-    const int tid = threadIdx.x;
-    uint32_t (*bitcnt)[32] = reinterpret_cast<uint32_t (*)[32]>(region);
-    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region + (size_t)SLOTS * 128);
+    static_assert(SLOTS <= NT * 8, "batch selection scans SLOTS candidates with NT threads");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint16_t *slot_of = reinterpret_cast<uint16_t *>(region);
     uint16_t *slot_word = slot_of + kRleTile;
+    uint32_t *soff = reinterpret_cast<uint32_t *>(slot_word + SLOTS);
+    uint32_t *sfill = soff + SLOTS + 4;
+    uint64_t *entries = reinterpret_cast<uint64_t *>(sfill + SLOTS);
+    uint32_t *big = reinterpret_cast<uint32_t *>(entries);  // [16][2] planes of a word too big for entries
+    __shared__ uint32_t batch_k, warp_tot[NT / 32];
     unsigned long long pc = 0;
     if (!nu) return 0;
     for (int k = tid; k < kRleTile; k += NT) slot_of[k] = kNoSlot;
-    __syncthreads();
-    auto add_bits = [&](uint16_t u, uint64_t x) {
-        while (x) {
-            const int b = __ffsll((long long)x) - 1;
-            atomicAdd(&bitcnt[u][b & 31], (b < 32) ? 1u : 0x10000u);
-            x &= x - 1;
+    constexpr int kPer = (SLOTS + NT - 1) / NT;
+    for (uint32_t base = 0; base < nu;) {
+        // batch: the longest prefix of undecided[base ..] (<= SLOTS words) whose dirty counts fit CAP
+        const uint32_t cand = min((uint32_t)SLOTS, nu - base);
+        uint32_t dv[kPer], run = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const uint32_t i = tid * kPer + q;
+            dv[q] = i < cand ? (cnt[undecided[base + i]] >> 16) : 0u;
+            run += dv[q];
         }
-    };
-    for (uint32_t base = 0; base < nu; base += SLOTS) {
-        const uint32_t nb = min((uint32_t)SLOTS, nu - base);
+        const uint32_t incl = warp_incl_scan_u32(run, lane);
+        if (lane == 31) warp_tot[warp] = incl;
+        if (tid == 0) batch_k = 0;
+        __syncthreads();
+        uint32_t off = incl - run;
+        for (int w = 0; w < warp; ++w) off += warp_tot[w];
+        uint32_t kk = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const uint32_t i = tid * kPer + q;
+            if (i < cand && off + dv[q] <= (uint32_t)kResolveCap) {
+                kk = i + 1;
+                soff[i] = off;
+                sfill[i] = 0;
+            }
+            off += dv[q];
+        }
+        if (kk) atomicMax(&batch_k, kk);
+        __syncthreads();
+        const uint32_t nb = batch_k;
+        if (nb == 0) {  // undecided[base] alone has more dirty inputs than the buffer holds
+            const uint16_t wk = undecided[base];
+            if (tid == 0) slot_of[wk] = 0;
+            for (int k = tid; k < 32; k += NT) big[k] = 0u;
+            __syncthreads();
+            auto add_big = [&](uint16_t, uint64_t x) {
+                uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+#pragma unroll 1
+                for (int j = 0; (lo | hi) && j < 16; ++j) {
+                    if (lo) lo &= atomicXor(&big[2 * j], lo);
+                    if (hi) hi &= atomicXor(&big[2 * j + 1], hi);
+                }
+            };
+            count_bits(static_cast<const uint16_t *>(slot_of), add_big);
+            __syncthreads();
+            if (tid == 0) {
+                uint64_t c[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) c[j] = ((uint64_t)big[2 * j + 1] << 32) | big[2 * j];
+                uint64_t w = decide_word(d, cnt[wk] & 0xFFFFu, cnt[wk] >> 16, c);
+                if (d.ts + wk == d.total_words - 1) w &= d.last_mask;
+                d.out[d.ts - d.out_first + wk] = w;
+                pc += __popcll(w);
+                slot_of[wk] = kNoSlot;
+            }
+            __syncthreads();
+            base += 1;
+            continue;
+        }
         for (uint32_t u = tid; u < nb; u += NT) {
             const uint16_t wk = undecided[base + u];
             slot_word[u] = wk;
             slot_of[wk] = (uint16_t)u;
         }
-        for (int k = tid; k < SLOTS * 32; k += NT) (&bitcnt[0][0])[k] = 0u;
         __syncthreads();
-        count_bits(static_cast<const uint16_t *>(slot_of), add_bits);
+        auto add_entry = [&](uint16_t u, uint64_t x) { entries[soff[u] + atomicAdd(&sfill[u], 1u)] = x; };
+        count_bits(static_cast<const uint16_t *>(slot_of), add_entry);
         __syncthreads();
         for (uint32_t u = tid; u < nb; u += NT) {
             const uint16_t wk = slot_word[u];
-            const uint32_t ones = cnt[wk] & 0xFFFFu;
-            uint64_t w = 0;
-            for (int b = 0; b < 64; ++b) {
-                const uint32_t cb = (bitcnt[u][b & 31] >> ((b >> 5) * 16)) & 0xFFFFu;
-                if (accept_at(d.accept_bits, ones + cb)) w |= 1ull << b;
-            }
+            const uint32_t ones = cnt[wk] & 0xFFFFu, dirty = cnt[wk] >> 16;
+            uint64_t c[16];
+            const uint64_t *lits = entries + soff[u];
+            if (dirty < 16) planes_sum<4>(lits, dirty, c);
+            else if (dirty < 256) planes_sum<8>(lits, dirty, c);
+            else planes_sum<16>(lits, dirty, c);
+            uint64_t w = decide_word(d, ones, dirty, c);
             if (d.ts + wk == d.total_words - 1) w &= d.last_mask;
             d.out[d.ts - d.out_first + wk] = w;
             pc += __popcll(w);
             slot_of[wk] = kNoSlot;
         }
         __syncthreads();
+        base += nb;
     }
     return pc;
 }

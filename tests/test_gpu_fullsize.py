@@ -162,3 +162,28 @@ def test_c5_full_size_properties(bq):
         assert torch.equal(out2[:wave], ~res), w0
         q.close()
     assert abs(total_pc / (64.0 * total) - 0.5) < 0.01
+
+
+def test_c4_full_size_low_t_and_symmetric(bq):
+    """Config 4's streams at full size with T=5 (most words undecided by the fills:
+    phase C reads literal words in nearly every tile) and a symmetric interval
+    [3, 40], through K4s, against the oracle's cdom sweeps."""
+    lib = bq._lib.load()
+    n, r = 1024, 1 << 30
+    nw = r // 64
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(16) as ex:
+        streams = list(ex.map(lambda i: _markov(lib, i, r), range(n)))
+    d = [torch.from_numpy(s.view(np.int64)).cuda() for s in streams]
+    q = bq.RleQuery(d, r)
+    q.threshold(50)  # first evaluation (K4); the next ones run on the tile-sliced layout
+    out, pc = q.threshold(5)
+    exp = O.cdom_threshold(streams, r, 5)
+    assert np.array_equal(_host(out[:nw]), exp)
+    assert int(pc.item()) == _popcount(exp)
+    acc = [3 <= k <= 40 for k in range(n + 1)]
+    out, pc = q.symmetric(acc)
+    exp = O.cdom_symmetric(streams, r, acc)
+    assert np.array_equal(_host(out[:nw]), exp)
+    assert int(pc.item()) == _popcount(exp)
