@@ -45,14 +45,15 @@
 
 namespace bq {
 
-constexpr int kSlotsPerBatch = 256;   // undecided words resolved per phase-C pass
+constexpr int kSlotsPerBatch = 512;   // undecided words resolved per phase-C pass
 constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
 constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
 constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
-constexpr size_t phase_c_bytes(int slots) { return (size_t)slots * 128 + (size_t)kRleTile * 4 + (size_t)slots * 2; }
+
 constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * 2 * kPoolWords * 8;
-constexpr size_t kRegionBytes = kPoolBytes > phase_c_bytes(kSlotsPerBatch) ? kPoolBytes : phase_c_bytes(kSlotsPerBatch);
+constexpr size_t kPhaseCBytes = tile_resolve_bytes<kSlotsPerBatch>() + (size_t)kRleTile * 2;  // + undecided list
+constexpr size_t kRegionBytes = kPoolBytes > kPhaseCBytes ? kPoolBytes : kPhaseCBytes;
 
 inline size_t rle_smem_bytes() {
     return kCntBytes + kRegionBytes;
@@ -475,7 +476,7 @@ __global__ void __launch_bounds__(kStagedThreads, 4) rle_count_kernel(const __gr
                           const uint64_t lo = max(ds, ts), hi = min(de, te);
                           for (uint64_t p = lo; p < hi; ++p) {
                               const uint16_t u = slot_of[p - ts];
-                              if (u != kNoSlot) add_bits(u, __ldg(s + lit + (p - ds)));
+                              if (u != kNoSlot) add_bits(u, s + lit + (p - ds));
                           }
                       });
         }

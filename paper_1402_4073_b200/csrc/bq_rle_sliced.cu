@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
                 const uint32_t fe = rel + run;
                 for (uint32_t q = 0; q < dirty; ++q) {
                     const uint16_t u = slot_of[fe + q];
-                    if (u != kNoSlot) add_bits(u, __ldg(tlit + lit + q));
+                    if (u != kNoSlot) add_bits(u, tlit + lit + q);
                 }
                 lit += dirty;
                 rel = (fe + dirty) & (kRleTile - 1);

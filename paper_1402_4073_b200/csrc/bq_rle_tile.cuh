@@ -101,28 +101,39 @@ __device__ __forceinline__ unsigned long long tile_decide(const TileDecide &d, c
 }
 
 // Phase C shared memory: slot_of[kRleTile] | slot_word[SLOTS] | soff[SLOTS + 1] |
-// sfill[SLOTS] | entries[CAP] (64-bit literal words, grouped by slot).
-constexpr int kResolveCap = 4096;
+// sfill[SLOTS] | entries[kResolveCap] (addresses of literal words, grouped by slot).
+constexpr int kResolveCap = 3584;  // literal words per phase-C batch (28 KB)
 template <int SLOTS>
 constexpr size_t tile_resolve_bytes() {
     return (size_t)kRleTile * 2 + (size_t)SLOTS * 2 + (size_t)(SLOTS + 4) * 4 + (size_t)SLOTS * 4 +
            (size_t)kResolveCap * 8;
 }
 
-// Bit-sliced sum of n literal words into M planes (plane j = bit j of the 64 counts).
 template <int M>
-__device__ __forceinline__ void planes_sum(const uint64_t *lits, uint32_t n, uint64_t (&c)[16]) {
+__device__ __forceinline__ void ripple(uint64_t (&c)[16], uint64_t carry) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const uint64_t t = c[j] & carry;
+        c[j] ^= carry;
+        carry = t;
+    }
+}
+
+// Bit-sliced sum of the n literal words at addrs[0..n) into M planes (plane j = bit j
+// of the 64 counts); four independent loads in flight at a time.
+template <int M>
+__device__ __forceinline__ void planes_sum(const uint64_t *addrs, uint32_t n, uint64_t (&c)[16]) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) c[j] = 0ull;
-    for (uint32_t i = 0; i < n; ++i) {
-        uint64_t carry = lits[i];
+    uint32_t i = 0;
+    for (; i + 4 <= n; i += 4) {
+        uint64_t x[4];
 #pragma unroll
-        for (int j = 0; j < M; ++j) {
-            const uint64_t t = c[j] & carry;
-            c[j] ^= carry;
-            carry = t;
-        }
+        for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const uint64_t *>(addrs[i + k]));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ripple<M>(c, x[k]);
     }
+    for (; i < n; ++i) ripple<M>(c, __ldg(reinterpret_cast<const uint64_t *>(addrs[i])));
 }
 
 // count >= k per bit position, for the bit-sliced count c (planes 0..15), k a runtime value
@@ -162,10 +173,11 @@ __device__ __forceinline__ uint64_t decide_word(const TileDecide &d, uint32_t on
 }
 
 // Phase C.  count_bits(slot_of, add) is called by every thread between barriers and
-// must call add(slot, word) for every literal word whose tile position p has
+// must call add(slot, &word) for every literal word whose tile position p has
 // slot_of[p] != kNoSlot.  Undecided words are taken in batches whose literal words
 // (their dirty counts are known from phase B) fit the entries buffer; add() files
-// each literal word under its slot, and then one thread per slot sums them into
+// each literal word's address under its slot (no load on the walk), and then one
+// thread per slot loads them, several at a time, and sums them into
 // bit-sliced counters in registers (a ripple of a few planes per word -- no
 // atomics, no per-bit loop) and decides all 64 bits with bit-sliced comparisons
 // against the accept vector's breakpoints.  A word with more dirty inputs than the
@@ -222,7 +234,8 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
             if (tid == 0) slot_of[wk] = 0;
             for (int k = tid; k < 32; k += NT) big[k] = 0u;
             __syncthreads();
-            auto add_big = [&](uint16_t, uint64_t x) {
+            auto add_big = [&](uint16_t, const uint64_t *p) {
+                const uint64_t x = __ldg(p);
                 uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
 #pragma unroll 1
                 for (int j = 0; (lo | hi) && j < 16; ++j) {
@@ -252,7 +265,9 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
             slot_of[wk] = (uint16_t)u;
         }
         __syncthreads();
-        auto add_entry = [&](uint16_t u, uint64_t x) { entries[soff[u] + atomicAdd(&sfill[u], 1u)] = x; };
+        auto add_entry = [&](uint16_t u, const uint64_t *p) {
+            entries[soff[u] + atomicAdd(&sfill[u], 1u)] = reinterpret_cast<uint64_t>(p);
+        };
         count_bits(static_cast<const uint16_t *>(slot_of), add_entry);
         __syncthreads();
         for (uint32_t u = tid; u < nb; u += NT) {
