@@ -394,3 +394,35 @@ def test_word_range_errors(bq):
         bq.RleQuery(d, r, word_range=(1024, 1500))  # interior end not aligned
     q = bq.RleQuery(d, r, word_range=(4096, 10 ** 9))  # end clamps to ceil(r/64)
     assert q.word_range == (4096, 5000)
+
+
+def test_max_inputs_rle(bq):
+    """N = BQ_MAX_INPUTS (65535) RLE streams: the directory's per-stream grid
+    dimension at its limit and 16-bit packed counts reaching N (all-ones words)."""
+    lib = bq._lib.load()
+    n, r = 65535, 64 * 1500 + 7
+    nw = (r + 63) // 64
+    rng = np.random.default_rng(65535)
+    ones = np.full(nw, 2**64 - 1, dtype=np.uint64)
+    ones[-1] = np.uint64((1 << 7) - 1)
+    pool = [O.rle_compress(ones, r), np.zeros(0, dtype=np.uint64)]
+    for k in range(6):
+        w = np.zeros(nw, dtype=np.uint64)
+        idx = rng.integers(0, nw, size=40)
+        w[idx] = rng.integers(1, 2**63, size=40, dtype=np.uint64)
+        w[-1] &= np.uint64((1 << 7) - 1)
+        pool.append(O.rle_compress(O.trim(w), r))
+    streams = [pool[0] if i % 3 == 0 else pool[1 + i % (len(pool) - 1)] for i in range(n)]
+    flat = np.concatenate([s for s in streams if s.size] + [np.zeros(1, dtype=np.uint64)])
+    dflat = torch.from_numpy(flat.view(np.int64)).cuda()
+    d, o = [], 0
+    for s in streams:
+        d.append(bq.DeviceRleBitmap(dflat[o:o + s.size] if s.size else dflat[:0], r, s.size))
+        o += s.size
+    q = bq.RleQuery(d, r)
+    for t in (1, n // 3, n // 3 + 1, n):
+        for _ in range(2):  # K4, then K4s
+            out, pc = q.threshold(t)
+            exp = O.cdom_threshold(streams, r, t)
+            assert np.array_equal(host(out, nw), exp), t
+            assert int(pc.item()) == popcount(exp)

@@ -230,7 +230,7 @@ def test_errors(bq):
         bq.scan_count([bq.UncompressedBitmap([1], 1 << 40)], 1, budget_bytes=1 << 20)
 
 
-@pytest.mark.parametrize("n", [8200, 20000])
+@pytest.mark.parametrize("n", [8200, 20000, 65535])
 def test_large_n_global_pointer_table(bq, n):
     """N > 8192: the kernel reads the pointer table from global memory; M = 14/16-bit counters."""
     lib = bq._lib.load()
