@@ -163,6 +163,11 @@ BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q);
  * literals only at undecided words (bench.py's roofline uses these). */
 BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals);
 
+/* Difference-array events of the tile-sliced layout once built (0 before):
+ * 16-bit entries, padded per tile and kind; phase A of K4s reads each once per
+ * evaluation instead of the markers (markers are read only where phase C runs). */
+BQ_API int bq_rle_query_layout_events(const bq_rle_query *q, uint64_t *n_events);
+
 /* Threshold / symmetric function over the compressed inputs, output
  * uncompressed (bq_rle_query_out_words(q) words: ceil(r/64), or the query's
  * word range), popcount ADDED to d_popcnt (optional).  Asynchronous on

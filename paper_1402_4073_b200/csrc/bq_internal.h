@@ -74,6 +74,24 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 // (word position within its slice, pending literal end, literal index) lets any
 // warp decode any chunk.
 constexpr int kSliceChunk = 128;
+//
+// Phase A of K4s reads neither: it reads the tile's difference-array events.  Each
+// slice contributes the nonzero updates its markers make to the packed difference
+// array (ones | dirty << 16) at positions inside the tile, coincident updates of
+// neighbouring markers merged: +1 / -1 where a one-fill starts / ends, +1 / -1 << 16
+// where a literal group starts / ends, +1 - (1 << 16) where a one-fill starts as a
+// literal group ends, -1 + (1 << 16) where a one-fill ends as a literal group starts.
+// Events are 16-bit byte offsets (position * 4) into the difference array, grouped
+// per tile into six lists by kind (all slices of the tile), each padded to whole
+// warp rows (kEvRow events: 32 lanes x one 16-byte vector of 8 events) with offsets
+// of dummy slots past the tile.  Inside a list the events are permuted so that the
+// 32 updates of each shared-memory atomic instruction (event j of the 32 vectors of
+// a row) fall in distinct banks wherever the list allows: phase A adds a
+// warp-uniform constant per event, every update nonzero and bank-conflict free.
+constexpr int kEvVec = 8;                                      // events per 16-byte vector
+constexpr int kEvRow = 32 * kEvVec;                            // events per warp row
+constexpr int kEvKinds = 6;
+constexpr uint16_t kEvDummy = (uint16_t)((kRleTile + 1) * 4);  // byte offset of the first dummy slot (32 follow)
 struct SlicedLayout {
     void *mem = nullptr;
     const uint32_t *markers = nullptr;    // [sum of padded tile marker counts]
@@ -81,8 +99,11 @@ struct SlicedLayout {
     const uint64_t *tile_mbase = nullptr; // [ntiles + 1] marker offset of each tile (multiple of kSliceChunk)
     const uint64_t *tile_lbase = nullptr; // [ntiles + 1] literal offset of each tile
     const uint64_t *chunk_meta = nullptr; // [markers / kSliceChunk]: rel | carry << 11 | literal index << 32
+    const uint16_t *events = nullptr;     // [sum of tile event counts] byte offsets into the difference array
+    const uint64_t *tile_ebase = nullptr; // [ntiles + 1] event offset of each tile (multiple of kEvRow)
+    const uint4 *tile_eends = nullptr;    // [2 ntiles] cumulative ends of the six lists in 16-byte vectors (+ 2 unused)
     uint64_t bytes = 0;
-    uint64_t n_markers = 0, n_literals = 0;
+    uint64_t n_markers = 0, n_literals = 0, n_events = 0;
 };
 // tiles [tile0, tile0 + ntiles) of the streams; directory rows are relative to tile0
 int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t tile0,

@@ -664,6 +664,13 @@ BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers,
     return BQ_OK;
 }
 
+BQ_API int bq_rle_query_layout_events(const bq_rle_query *q, uint64_t *n_events) {
+    if (!q || !n_events) return set_error(BQ_EINPUT, "NULL argument");
+    std::lock_guard<std::mutex> guard(q->build_mu);
+    *n_events = q->sliced.n_events;
+    return BQ_OK;
+}
+
 static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *d_out, unsigned long long *d_popcnt,
                     void *stream) {
     if (!q) return set_error(BQ_EINPUT, "query is NULL");

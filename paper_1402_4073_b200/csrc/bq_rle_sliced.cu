@@ -4,18 +4,22 @@
 // marker chain: a dependent shared-memory load per marker, and lanes idle while
 // the longest chain of the warp finishes (~47% lane efficiency on C4).  Here the
 // streams are re-encoded once per query into 1024-word slices whose markers are
-// contiguous per tile and cover exactly 1024 words each, so the word position of
-// a marker is the running sum of (run + dirty) modulo 1024 -- a warp prefix sum
-// over 128 markers at a time (4 per lane) replaces the chain walk, every lane is
-// busy, and phase A reads only the 32-bit markers (literal words are read in
-// phase C, only at undecided positions, as runmerge.cdom_threshold examines
-// dirty words only where the fill counts do not decide; runmerge.py:198-241).
+// contiguous per tile and cover exactly 1024 words each.  From them the build also
+// derives what phase A needs and nothing more: the nonzero updates every slice
+// makes to the tile's difference array, as 16-bit positions in four lists by kind
+// (+1 / -1 one-fill start / end, +1 / -1 << 16 literal start / end).  Phase A then
+// costs one shared-memory add per event with a warp-uniform constant -- no field
+// extraction, prefix sums or zero-update redirects (the marker decode it replaces
+// was ALU-pipe bound at ~28 thread instructions per marker).  Literal words are read
+// in phase C, only at undecided positions, as runmerge.cdom_threshold examines
+// dirty words only where the fill counts do not decide (runmerge.py:198-241);
+// phase C finds them by decoding the tile's markers (chunk checkpoints + warp
+// prefix sums).
 //
-// Per tile (one CTA): A) markers staged into shared memory by TMA bulk copies in
-// 16 KB pieces (double-buffered); each chunk of 128 markers is decoded by one
-// warp into the packed difference array cnt (ones | dirty << 16); B) prefix sum
-// and const_until decisions; C) bit counters of undecided words from their
-// literals.
+// Per tile (one CTA): A) events staged into shared memory by TMA bulk copies in
+// 16 KB pieces (double-buffered) and added into the packed difference array cnt
+// (ones | dirty << 16); B) prefix sum and const_until decisions; C) bit counters
+// of undecided words from their literals.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -38,11 +42,10 @@ namespace {
 #define BQ_SL_SLOTS 256
 #endif
 constexpr int kSlNT = BQ_SL_NT;                            // K4s threads per CTA (4 warps)
-constexpr int kPieceChunks = 32;                           // chunks per staged piece
-constexpr int kPieceMarkers = kPieceChunks * kSliceChunk;  // 4096 markers = 16 KB
+constexpr int kPieceVecs = 1024;                           // event vectors per staged piece (16 KB)
 constexpr int kSlSlots = BQ_SL_SLOTS;                      // undecided words per phase-C pass
 constexpr size_t kSlCntBytes = (size_t)(kRleTile + 36) * 4;  // + sentinel + 32 per-lane dummies (+ pad)
-constexpr size_t kSlBufBytes = 2 * (size_t)kPieceMarkers * 4;
+constexpr size_t kSlBufBytes = 2 * (size_t)kPieceVecs * 16;
 constexpr size_t kSlPhaseC = tile_resolve_bytes<kSlSlots>() + (size_t)kRleTile * 2;  // + undecided list
 constexpr size_t kSlRegion = kSlBufBytes > kSlPhaseC ? kSlBufBytes : kSlPhaseC;
 constexpr size_t kSlSmem = kSlCntBytes + 16 + kSlRegion;  // cnt | 2 mbarriers | region
@@ -64,26 +67,56 @@ struct SliceSink {
     uint64_t *lit;      // tile literal array
     uint64_t *meta;     // chunk checkpoints of this tile
     uint32_t mk0, lit0;  // within-tile index of the slice's first marker / literal
+    uint16_t *ev[kEvKinds];  // the slice's first entry in each of the tile's event lists
+};
+
+struct SliceCounts {
+    uint32_t mk, lit;
+    uint32_t ev[kEvKinds];  // events of each kind (bq_internal.h; deltas in add_vector)
 };
 
 // Re-encode stream words [ts, ts + 1024) starting at the directory entry e
-// (marker index, fill start).  Returns (markers, literals) of the slice.
+// (marker index, fill start): markers, literals, and the slice's nonzero updates
+// to the difference array (events at positions inside the tile; a literal group's
+// end is merged with what the next marker starts at the same position).
 template <bool EMIT>
-__device__ uint2 slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint64_t ts, const SliceSink &sink) {
+__device__ SliceCounts slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint64_t ts, const SliceSink &sink) {
     const uint64_t te = ts + kRleTile;
     uint64_t i = e.x, pos = e.y;
-    uint32_t rel = 0, n_mk = 0, n_lit = 0;
+    uint32_t rel = 0;
+    SliceCounts n{};
     bool prev_dirty = false;
+    bool pend = false;  // the previous marker's literal group ends at rel (its -1 << 16 not yet filed)
+    auto event = [&](int kind, uint32_t at) {
+        if (EMIT) sink.ev[kind][n.ev[kind]] = (uint16_t)(at * 4u);
+        ++n.ev[kind];
+    };
     auto emit = [&](uint32_t bit, uint32_t run, uint32_t dirty) {
         if (EMIT) {
-            const uint32_t j = sink.mk0 + n_mk;
+            const uint32_t j = sink.mk0 + n.mk;
             sink.mk[j] = mk_pack(bit, run, dirty);
             if (j % kSliceChunk == 0)
                 sink.meta[j / kSliceChunk] = (uint64_t)rel | ((uint64_t)(rel != 0 && prev_dirty) << 11) |
-                                             ((uint64_t)(sink.lit0 + n_lit) << 32);
+                                             ((uint64_t)(sink.lit0 + n.lit) << 32);
         }
-        ++n_mk;
-        rel += run + dirty;
+        const uint32_t fe = rel + run, de = fe + dirty;
+        bool cancel = false;  // a pending literal end meets this marker's literal start (run 0)
+        if (pend) {
+            if (bit) event(4, rel);
+            else if (run == 0u && dirty) cancel = true;
+            else event(3, rel);
+        } else if (bit) {
+            event(0, rel);
+        }
+        if (bit) {
+            if (dirty) event(5, fe);
+            else if (fe < (uint32_t)kRleTile) event(1, fe);
+        } else if (dirty && !cancel) {
+            event(2, fe);
+        }
+        pend = dirty && de < (uint32_t)kRleTile;
+        ++n.mk;
+        rel = de;
         prev_dirty = dirty != 0;
     };
     while (rel < (uint32_t)kRleTile) {
@@ -100,124 +133,232 @@ __device__ uint2 slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint64_t t
         const uint32_t cdirty = cde > cds ? (uint32_t)(cde - cds) : 0u;
         if (crun + cdirty) {
             if (EMIT)
-                for (uint32_t k = 0; k < cdirty; ++k) sink.lit[sink.lit0 + n_lit + k] = __ldg(src + i + 1 + (cds - fe) + k);
+                for (uint32_t k = 0; k < cdirty; ++k) sink.lit[sink.lit0 + n.lit + k] = __ldg(src + i + 1 + (cds - fe) + k);
             emit((uint32_t)(m & 1) & (crun != 0u), crun, cdirty);
-            n_lit += cdirty;
+            n.lit += cdirty;
         }
         pos = de;
         i += 1 + dirty;
     }
-    return make_uint2(n_mk, n_lit);
+    return n;
 }
 
 __global__ void slice_count_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
-                                   uint32_t tile0, uint32_t ntiles, uint64_t *counts) {
+                                   uint32_t tile0, uint32_t ntiles, uint64_t *counts, ulonglong4 *ecounts) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
         const int s = (int)(k / ntiles);  // neighbouring threads: neighbouring tiles of one stream (reads)
         const uint32_t t = (uint32_t)(k % ntiles);
-        const uint2 c =
+        const SliceCounts c =
             slice_walk<false>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)(tile0 + t) * kRleTile, SliceSink{});
-        counts[(size_t)t * n + s] = (uint64_t)c.x | ((uint64_t)c.y << 32);
+        counts[(size_t)t * n + s] = (uint64_t)c.mk | ((uint64_t)c.lit << 32);
+        ecounts[(size_t)t * n + s] = make_ulonglong4((uint64_t)c.ev[0] | ((uint64_t)c.ev[1] << 32),
+                                                     (uint64_t)c.ev[2] | ((uint64_t)c.ev[3] << 32),
+                                                     (uint64_t)c.ev[4] | ((uint64_t)c.ev[5] << 32), 0ull);
     }
 }
 
-// One CTA per tile: exclusive scan of the slice counts in place (markers in the low,
-// literals in the high half: each half of a tile's sum stays below 2^32), and the
-// tile totals, markers rounded up to whole chunks.
-__global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, int n, uint64_t *tile_m, uint64_t *tile_l) {
+// One CTA per tile: exclusive scans of the slice counts in place (two 32-bit counts
+// per 64-bit value: each half of a tile's sum stays below 2^32), and the tile totals:
+// markers rounded up to whole chunks, literals, the event lists' real lengths, their
+// cumulative ends in 16-byte vectors (each list padded to whole warp rows) and the
+// tile's event total.
+__global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, ulonglong4 *ecounts, int n, uint64_t *tile_m,
+                                                          uint64_t *tile_l, uint64_t *tile_e, uint4 *eends,
+                                                          uint32_t *ereal) {
     using Scan = cub::BlockScan<uint64_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint64_t carry;
+    __shared__ uint64_t carry[4];
     const uint32_t t = blockIdx.x;
     uint64_t *row = counts + (size_t)t * n;
-    if (threadIdx.x == 0) carry = 0;
+    ulonglong4 *erow = ecounts + (size_t)t * n;
+    if (threadIdx.x < 4) carry[threadIdx.x] = 0;
     __syncthreads();
     for (int base = 0; base < n; base += 1024) {
         const int s = base + (int)threadIdx.x;
-        const uint64_t v = s < n ? row[s] : 0ull;
-        uint64_t ex, agg;
-        Scan(tmp).ExclusiveSum(v, ex, agg);
-        const uint64_t c = carry;
-        if (s < n) row[s] = ex + c;
+        const ulonglong4 ev = s < n ? erow[s] : make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+        const uint64_t v[4] = {s < n ? row[s] : 0ull, ev.x, ev.y, ev.z};
+        uint64_t ex[4], agg[4], c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q) __syncthreads();
+            Scan(tmp).ExclusiveSum(v[q], ex[q], agg[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] = carry[q];
+        if (s < n) {
+            row[s] = ex[0] + c[0];
+            erow[s] = make_ulonglong4(ex[1] + c[1], ex[2] + c[2], ex[3] + c[3], 0ull);
+        }
         __syncthreads();
-        if (threadIdx.x == 0) carry = c + agg;
+        if (threadIdx.x == 0)
+            for (int q = 0; q < 4; ++q) carry[q] = c[q] + agg[q];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const uint64_t m = carry & 0xFFFFFFFFull, l = carry >> 32;
+        const uint64_t m = carry[0] & 0xFFFFFFFFull, l = carry[0] >> 32;
         tile_m[t] = (m + kSliceChunk - 1) / kSliceChunk * kSliceChunk;
         tile_l[t] = l;
+        uint32_t end[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, acc = 0;
+        for (int k = 0; k < kEvKinds; ++k) {
+            const uint32_t e = (uint32_t)(carry[1 + k / 2] >> (32 * (k & 1)));
+            ereal[(size_t)t * 8 + k] = e;
+            acc += (e + kEvRow - 1) / kEvRow * (kEvRow / kEvVec);
+            end[k] = acc;
+        }
+        eends[2 * (size_t)t] = make_uint4(end[0], end[1], end[2], end[3]);
+        eends[2 * (size_t)t + 1] = make_uint4(end[4], end[5], acc, 0u);
+        tile_e[t] = (uint64_t)acc * kEvVec;
     }
 }
 
 __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
-                                  uint32_t tile0, uint32_t ntiles, const uint64_t *offs, const uint64_t *mbase, const uint64_t *lbase,
-                                  uint32_t *markers, uint64_t *literals, uint64_t *meta) {
+                                  uint32_t tile0, uint32_t ntiles, const uint64_t *offs, const ulonglong4 *eoffs,
+                                  const uint64_t *mbase, const uint64_t *lbase, const uint64_t *ebase,
+                                  const uint4 *eends, uint32_t *markers, uint64_t *literals, uint64_t *meta,
+                                  uint16_t *events) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
         const int s = (int)(k % n);  // neighbouring threads: neighbouring slices of one tile (writes)
         const uint32_t t = (uint32_t)(k / n);
         const uint64_t o = offs[(size_t)t * n + s];
+        const ulonglong4 eo = eoffs[(size_t)t * n + s];
+        const uint4 ea = eends[2 * (size_t)t], eb = eends[2 * (size_t)t + 1];
+        const uint32_t starts[kEvKinds] = {0u, ea.x, ea.y, ea.z, ea.w, eb.x};
+        const uint32_t within[kEvKinds] = {(uint32_t)eo.x, (uint32_t)(eo.x >> 32), (uint32_t)eo.y,
+                                           (uint32_t)(eo.y >> 32), (uint32_t)eo.z, (uint32_t)(eo.z >> 32)};
+        uint16_t *tev = events + ebase[t];
         SliceSink sink;
         sink.mk = markers + mbase[t];
         sink.lit = literals + lbase[t];
         sink.meta = meta + mbase[t] / kSliceChunk;
         sink.mk0 = (uint32_t)o;
         sink.lit0 = (uint32_t)(o >> 32);
+#pragma unroll
+        for (int q = 0; q < kEvKinds; ++q) sink.ev[q] = tev + (size_t)starts[q] * kEvVec + within[q];
         slice_walk<true>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)(tile0 + t) * kRleTile, sink);
     }
+}
+
+// One CTA per (tile, event kind): permute the list (emitted slice by slice) so that
+// each shared-memory atomic instruction of phase A -- event j of the 32 vectors of a
+// warp row -- updates 32 distinct banks.  Events are ranked within their bank (bank =
+// position mod 32), ordered by (rank, bank) -- every round of ranks holds each bank at
+// most once -- and position s of that order goes to list index
+// row * kEvRow + (s mod 32) * kEvVec + (s mod kEvRow) / 32.  Groups of 32 spanning two
+// rounds can repeat a bank once.  Ranks follow list order (deterministic layout).
+// Padding after the real events: the 32 dummy slots in turn.
+__global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src, uint16_t *dst, const uint64_t *ebase,
+                                                             const uint4 *eends, const uint32_t *ereal) {
+    const uint32_t t = blockIdx.x, kind = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint4 ea = eends[2 * (size_t)t], eb = eends[2 * (size_t)t + 1];
+    const uint32_t ends[kEvKinds] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y};
+    const uint32_t vstart = kind ? ends[kind - 1] : 0u;
+    const uint32_t npad = (ends[kind] - vstart) * kEvVec;
+    const uint32_t nreal = ereal[(size_t)t * 8 + kind];
+    const uint64_t base = ebase[t] + (uint64_t)vstart * kEvVec;
+    const uint16_t *s = src + base;
+    uint16_t *d = dst + base;
+    __shared__ uint32_t bank_cnt[32], running[32], wcnt[8][32];
+    __shared__ uint32_t sorted_cnt[32], sorted_bank[32], prefix[33], sufmask[33];
+    auto place = [&](uint32_t sidx, uint16_t v) {
+        const uint32_t within = sidx % kEvRow;
+        d[sidx - within + (within % 32) * kEvVec + within / 32] = v;
+    };
+    if (tid < 32) {
+        bank_cnt[tid] = 0;
+        running[tid] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < nreal; i += 256) atomicAdd(&bank_cnt[(s[i] >> 2) & 31u], 1u);
+    __syncthreads();
+    if (tid < 32) {  // banks ordered by (count, bank)
+        const uint32_t c = bank_cnt[tid];
+        uint32_t pos = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t cb = bank_cnt[b];
+            pos += (cb < c || (cb == c && b < tid)) ? 1u : 0u;
+        }
+        sorted_cnt[pos] = c;
+        sorted_bank[pos] = (uint32_t)tid;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        prefix[0] = 0;
+        for (int k = 0; k < 32; ++k) prefix[k + 1] = prefix[k] + sorted_cnt[k];
+        sufmask[32] = 0;
+        for (int k = 31; k >= 0; --k) sufmask[k] = sufmask[k + 1] | (1u << sorted_bank[k]);
+    }
+    __syncthreads();
+    for (uint32_t c0 = 0; c0 < nreal; c0 += 256) {
+        const uint32_t i = c0 + tid;
+        const bool valid = i < nreal;
+        const uint16_t v = valid ? s[i] : (uint16_t)0;
+        const uint32_t b = (v >> 2) & 31u;
+        wcnt[warp][lane] = 0;
+        __syncwarp();
+        const uint32_t peers = __match_any_sync(0xffffffffu, valid ? b : 0xFFFFFFFFu);
+        const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && wrank == 0) wcnt[warp][b] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t r = running[b] + wrank;
+            for (int w2 = 0; w2 < warp; ++w2) r += wcnt[w2][b];
+            uint32_t k = 0;  // banks whose count is <= r (they are exhausted before round r)
+#pragma unroll
+            for (uint32_t step = 32; step; step >>= 1)
+                if (k + step <= 32u && sorted_cnt[k + step - 1] <= r) k += step;
+            place(prefix[k] + (32u - k) * r + __popc(sufmask[k] & ((1u << b) - 1u)), v);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            uint32_t add = 0;
+            for (int w2 = 0; w2 < 8; ++w2) add += wcnt[w2][tid];
+            running[tid] += add;
+        }
+        __syncthreads();
+    }
+    for (uint32_t i = nreal + tid; i < npad; i += 256) place(i, (uint16_t)(kEvDummy + 4u * (i % 32u)));
 }
 
 // ---------------------------------------------------------------------------
 // K4s: one CTA per tile.
 
-// K4s decode is bound by the ALU pipe (shifts, masks, selects, LEA); the shared-memory
-// byte offsets are formed as index * four with four a runtime value, so they go to
-// the FMA pipe (IMAD) instead of an ALU LEA.
-struct MulC {
-    uint32_t four;  // 4
-};
-
 struct SlArgs {
     const uint32_t *markers;
     const uint64_t *literals;
     const uint64_t *tile_mbase, *tile_lbase, *chunk_meta;
-    MulC mc;
+    const uint16_t *events;
+    const uint64_t *tile_ebase;
+    const uint4 *tile_eends;
     SlicedEval e;
 };
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) { return warp_incl_scan_u32(v, lane); }
 
-// Decode one chunk (4 markers per lane) into the difference array: the word
-// position of each marker is the chunk checkpoint plus the warp prefix sum of
-// (run + dirty), modulo 1024 (slices cover exactly 1024 words).  Two updates per
-// marker: (+one-fill start, -pending literal end) at its start, (-one-fill end,
-// +literal start) where its fill ends.
+// Two events (16-bit byte offsets into the difference array) of one 32-bit word.
+__device__ __forceinline__ void add_events(uint32_t *cnt, uint32_t w, uint32_t delta) {
+    atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (w & 0xFFFFu)), delta);
+    atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (w >> 16)), delta);
+}
 
-__device__ __forceinline__ void decode_chunk(const uint4 v, uint32_t cm, int lane, uint32_t *cnt, const MulC &c) {
-    const uint32_t four = c.four;
-    const uint32_t dummy = kRleTile + 1 + lane;  // per-lane slot for zero updates (no same-address conflicts)
-    const uint32_t m[4] = {v.x, v.y, v.z, v.w};
-    uint32_t tot = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) tot += mk_run(m[k]) + mk_dirty(m[k]);
-    const uint32_t incl = warp_incl_scan(tot, lane);
-    uint32_t rel = (cm + incl - tot) & (kRleTile - 1);
-    const uint32_t up = __shfl_up_sync(0xffffffffu, mk_dirty(m[3]), 1);
-    bool pd = lane ? (up != 0u) : ((cm >> 11) & 1u);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint32_t bit = mk_bit(m[k]), run = mk_run(m[k]), dirty = mk_dirty(m[k]);
-        const uint32_t fe = rel + run;
-        const uint32_t at_rel = bit + ((rel != 0u && pd) ? 0xFFFF0000u : 0u);
-        const uint32_t at_fe = (dirty ? 0x10000u : 0u) - bit;
-        // byte offsets through IMAD (runtime stride): keeps address arithmetic off the ALU pipe
-        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_rel ? rel : dummy) * four), at_rel);
-        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_fe ? fe : dummy) * four), at_fe);
-        pd = dirty != 0u;
-        rel = (fe + dirty) & (kRleTile - 1);
-    }
+// One 16-byte vector of events: 8 updates by the constant of the vector's list
+// (lists are padded to whole warp rows, so the constant is warp-uniform).
+struct EvEnds {
+    uint4 a, b;  // cumulative list ends in vectors: a.x..a.w, b.x, b.y
+};
+__device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, uint32_t g, const EvEnds &ee) {
+    const uint32_t delta = g < ee.a.x   ? 1u
+                           : g < ee.a.y ? 0xFFFFFFFFu
+                           : g < ee.a.z ? 0x10000u
+                           : g < ee.a.w ? 0xFFFF0000u
+                           : g < ee.b.x ? 0xFFFF0001u
+                                        : 0x0000FFFFu;
+    add_events(cnt, v.x, delta);
+    add_events(cnt, v.y, delta);
+    add_events(cnt, v.z, delta);
+    add_events(cnt, v.w, delta);
 }
 
 __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __grid_constant__ SlArgs a) {
@@ -226,7 +367,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     uint32_t *cnt = reinterpret_cast<uint32_t *>(sl_smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sl_smem + kSlCntBytes);
     uint8_t *region = sl_smem + kSlCntBytes + 16;
-    uint32_t *buf = reinterpret_cast<uint32_t *>(region);  // [2][kPieceMarkers]
+    uint4 *buf = reinterpret_cast<uint4 *>(region);  // [2][kPieceVecs]
     __shared__ uint32_t n_undecided;
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
@@ -240,19 +381,22 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     const uint64_t *meta = a.chunk_meta + mbase / kSliceChunk;
     const uint32_t *tmk = a.markers + mbase;
     const uint64_t *tlit = a.literals + a.tile_lbase[tile];
-    const uint32_t npieces = (nchunks + kPieceChunks - 1) / kPieceChunks;
+    const EvEnds ee{a.tile_eends[2 * tile], a.tile_eends[2 * tile + 1]};
+    const uint32_t nvec = ee.b.z;
+    const uint4 *tev = reinterpret_cast<const uint4 *>(a.events + a.tile_ebase[tile]);
+    const uint32_t npieces = (nvec + kPieceVecs - 1) / kPieceVecs;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
 
     auto issue = [&](uint32_t p) {  // thread 0: stage piece p into buf[p & 1]
-        const uint32_t nc = min((uint32_t)kPieceChunks, nchunks - p * kPieceChunks);
-        const uint32_t bytes = nc * kSliceChunk * 4;
+        const uint32_t nv = min((uint32_t)kPieceVecs, nvec - p * kPieceVecs);
+        const uint32_t bytes = nv * 16;
         const uint32_t bar = bar0 + 8 * (p & 1);
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + (size_t)(p & 1) * kPieceMarkers);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + (size_t)(p & 1) * kPieceVecs);
         asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
                      "r"(bytes)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-                     "l"(tmk + (size_t)p * kPieceMarkers), "r"(bytes), "r"(bar)
+                     "l"(tev + (size_t)p * kPieceVecs), "r"(bytes), "r"(bar)
                      : "memory");
     };
 
@@ -269,15 +413,8 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     }
     __syncthreads();
 
-    // ---- A: decode chunks into the difference array ----------------------------
-    // chunk checkpoints of a piece, one per lane (kPieceChunks == 32), loaded a piece ahead
-    auto piece_meta = [&](uint32_t p) {
-        return (p < npieces && p * kPieceChunks + lane < nchunks) ? __ldg(meta + p * kPieceChunks + lane) : 0ull;
-    };
-    uint64_t next_meta = piece_meta(0);
+    // ---- A: the tile's events into the difference array ---------------------------
     for (uint32_t p = 0; p < npieces && E.debug < 2; ++p) {
-        const uint64_t pmeta = next_meta;
-        next_meta = piece_meta(p + 1);
         const uint32_t bar = bar0 + 8 * (p & 1), parity = (p >> 1) & 1;
         uint32_t done = 0;
         while (!done) {
@@ -287,18 +424,17 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
                 : "r"(bar), "r"(parity)
                 : "memory");
         }
-        const uint32_t nc = min((uint32_t)kPieceChunks, nchunks - p * kPieceChunks);
-        const uint4 *pb = reinterpret_cast<const uint4 *>(buf + (size_t)(p & 1) * kPieceMarkers);
-        // two chunks per iteration: independent scans interleave (shuffle latency)
-        for (uint32_t c = warp; c < nc && !E.debug; c += 2 * (NT / 32)) {
-            const uint32_t c2 = c + NT / 32;
-            const bool two = c2 < nc;
-            const uint32_t cm0 = (uint32_t)__shfl_sync(0xffffffffu, pmeta, c);
-            const uint32_t cm1 = (uint32_t)__shfl_sync(0xffffffffu, pmeta, two ? c2 : c);
-            const uint4 v0 = pb[c * 32 + lane];
-            const uint4 v1 = two ? pb[c2 * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-            decode_chunk(v0, cm0, lane, cnt, a.mc);
-            decode_chunk(v1, two ? cm1 : 0u, lane, cnt, a.mc);
+        const uint32_t nv = min((uint32_t)kPieceVecs, nvec - p * kPieceVecs);
+        const uint4 *pb = buf + (size_t)(p & 1) * kPieceVecs;
+        const uint32_t g0 = p * kPieceVecs;
+        if (!E.debug) {
+            uint32_t i = tid;
+            for (; i + NT < nv; i += 2 * NT) {  // two vectors per iteration: both shared loads ahead of the updates
+                const uint4 v0 = pb[i], v1 = pb[i + NT];
+                add_vector(cnt, v0, g0 + i, ee);
+                add_vector(cnt, v1, g0 + i + NT, ee);
+            }
+            if (i < nv) add_vector(cnt, pb[i], g0 + i, ee);
         }
         __syncthreads();  // buf[p & 1] is free
         if (tid == 0 && p + 2 < npieces) {
@@ -359,79 +495,117 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     *out = SlicedLayout();
     if (!ntiles) return BQ_OK;
     const uint64_t cells = (uint64_t)ntiles * n;
-    // scratch: slice counts / offsets | tile marker totals | tile literal totals | CUB temp
+    const size_t T1 = (size_t)ntiles + 1;
+    // scratch: slice event counts / offsets (32 B per slice) | slice marker and literal
+    // counts / offsets | tile marker, literal, event totals and their scans | list ends
+    // | real list lengths | CUB temp
     size_t tmp_bytes = 0, tmp2 = 0;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                                  (int64_t)ntiles + 1);
+                                                  (int64_t)T1);
     if (e != cudaSuccess) return cuda_error(e, "DeviceScan sizing");
-    tmp2 = tmp_bytes;
-    const size_t scratch_bytes = cells * 8 + 4 * ((size_t)ntiles + 1) * 8 + tmp2 + 256;
+    const size_t scratch_bytes = cells * 40 + 6 * T1 * 8 + 16 + T1 * 32 + T1 * 32 + tmp_bytes + 256;
     char *scratch = nullptr;
     e = cudaMalloc(&scratch, scratch_bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return BQ_OK;  // no room: the query keeps the per-stream layout
     }
-    uint64_t *counts = reinterpret_cast<uint64_t *>(scratch);
-    uint64_t *tm = counts + cells, *tl = tm + ntiles + 1, *mb = tl + ntiles + 1, *lb = mb + ntiles + 1;
-    void *d_tmp = lb + ntiles + 1;
+    ulonglong4 *ecounts = reinterpret_cast<ulonglong4 *>(scratch);
+    uint64_t *counts = reinterpret_cast<uint64_t *>(ecounts + cells);
+    uint64_t *tm = counts + cells, *tl = tm + T1, *te = tl + T1, *mb = te + T1, *lb = mb + T1, *eb = lb + T1;
+    uint4 *eends = reinterpret_cast<uint4 *>(scratch + ((reinterpret_cast<char *>(eb + T1) - scratch) + 15) / 16 * 16);
+    uint32_t *ereal = reinterpret_cast<uint32_t *>(eends + 2 * T1);
+    void *d_tmp = ereal + 8 * T1;
     const int sms = sm_count();
     const unsigned grid = (unsigned)std::min<uint64_t>((cells + 255) / 256, (uint64_t)sms * 32);
+    char *evsrc = nullptr;
     auto fail = [&](cudaError_t err, const char *what) {
         cudaFree(scratch);
+        if (evsrc) cudaFree(evsrc);
         return cuda_error(err, what);
     };
-    slice_count_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts);
+    slice_count_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemset(tm + ntiles, 0, 8);
     if (e == cudaSuccess) e = cudaMemset(tl + ntiles, 0, 8);
+    if (e == cudaSuccess) e = cudaMemset(te + ntiles, 0, 8);
     if (e != cudaSuccess) return fail(e, "slice_count_kernel");
-    slice_scan_kernel<<<ntiles, 1024>>>(counts, n, tm, tl);
+    slice_scan_kernel<<<ntiles, 1024>>>(counts, ecounts, n, tm, tl, te, eends, ereal);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, tm, mb, (int64_t)ntiles + 1);
     tmp2 = tmp_bytes;
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, tl, lb, (int64_t)ntiles + 1);
-    uint64_t nm = 0, nl = 0;
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, tm, mb, (int64_t)T1);
+    tmp2 = tmp_bytes;
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, tl, lb, (int64_t)T1);
+    tmp2 = tmp_bytes;
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, te, eb, (int64_t)T1);
+    uint64_t nm = 0, nl = 0, ne = 0;
     if (e == cudaSuccess) e = cudaMemcpy(&nm, mb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(&nl, lb + ntiles, 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(&ne, eb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(e, "slice scans");
-    // markers (16-byte multiple) | literals | tile_mbase | tile_lbase | chunk_meta
-    const size_t mk_bytes = (nm * 4 + 15) / 16 * 16;
-    const size_t bytes = mk_bytes + nl * 8 + 2 * ((size_t)ntiles + 1) * 8 + nm / kSliceChunk * 8 + 64;
+    // markers | literals | tile_mbase | tile_lbase | chunk_meta | events | tile_ebase | tile_eends
+    // (markers, events and tile_eends at 16-byte boundaries)
+    auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
+    const size_t o_lit = r16(nm * 4);
+    const size_t o_tmb = o_lit + nl * 8;
+    const size_t o_tlb = o_tmb + T1 * 8;
+    const size_t o_meta = o_tlb + T1 * 8;
+    const size_t o_ev = r16(o_meta + nm / kSliceChunk * 8);
+    const size_t o_teb = o_ev + ne * 2;  // ne is a multiple of kEvRow: 16-byte multiple
+    const size_t o_tee = r16(o_teb + T1 * 8);
+    const size_t bytes = o_tee + (size_t)ntiles * 32;
     char *m = nullptr;
     e = cudaMalloc(&m, bytes);
+    if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * 2);  // events as emitted, slice by slice
     if (e != cudaSuccess) {
         cudaGetLastError();
+        if (m) cudaFree(m);
         cudaFree(scratch);
         return BQ_OK;
     }
     SlicedLayout l;
     l.mem = m;
     uint32_t *markers = reinterpret_cast<uint32_t *>(m);
-    uint64_t *literals = reinterpret_cast<uint64_t *>(m + mk_bytes);
-    uint64_t *tmb = literals + nl, *tlb = tmb + ntiles + 1, *meta = tlb + ntiles + 1;
-    e = cudaMemset(markers, 0, mk_bytes);  // chunk padding decodes to empty markers
-    if (e == cudaSuccess) e = cudaMemcpy(tmb, mb, ((size_t)ntiles + 1) * 8, cudaMemcpyDeviceToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(tlb, lb, ((size_t)ntiles + 1) * 8, cudaMemcpyDeviceToDevice);
+    uint64_t *literals = reinterpret_cast<uint64_t *>(m + o_lit);
+    uint64_t *tmb = reinterpret_cast<uint64_t *>(m + o_tmb), *tlb = reinterpret_cast<uint64_t *>(m + o_tlb);
+    uint64_t *meta = reinterpret_cast<uint64_t *>(m + o_meta);
+    uint16_t *events = reinterpret_cast<uint16_t *>(m + o_ev);
+    uint64_t *teb = reinterpret_cast<uint64_t *>(m + o_teb);
+    uint4 *tee = reinterpret_cast<uint4 *>(m + o_tee);
+    e = cudaMemset(markers, 0, o_lit);  // chunk padding decodes to empty markers
+    if (e == cudaSuccess) e = cudaMemcpy(tmb, mb, T1 * 8, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(tlb, lb, T1 * 8, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(teb, eb, T1 * 8, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(tee, eends, (size_t)ntiles * 32, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) {
-        slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, tmb, tlb, markers, literals,
-                                         meta);
+        slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts, tmb, tlb, teb, tee,
+                                         markers, literals, meta, reinterpret_cast<uint16_t *>(evsrc));
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && ne) {
+        arrange_events_kernel<<<dim3(ntiles, kEvKinds), 256>>>(reinterpret_cast<const uint16_t *>(evsrc), events, teb,
+                                                              tee, ereal);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaFree(scratch);
+    if (evsrc) cudaFree(evsrc);
     if (e != cudaSuccess) {
         cudaFree(m);
-        return cuda_error(e, "slice_emit_kernel");
+        return cuda_error(e, "slice_emit_kernel / arrange_events_kernel");
     }
     l.markers = markers;
     l.literals = literals;
     l.tile_mbase = tmb;
     l.tile_lbase = tlb;
     l.chunk_meta = meta;
+    l.events = events;
+    l.tile_ebase = teb;
+    l.tile_eends = tee;
     l.bytes = bytes;
     l.n_markers = nm;
     l.n_literals = nl;
+    l.n_events = ne;
     *out = l;
     return BQ_OK;
 }
@@ -448,7 +622,9 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
     a.tile_mbase = l.tile_mbase;
     a.tile_lbase = l.tile_lbase;
     a.chunk_meta = l.chunk_meta;
-    a.mc = MulC{4u};
+    a.events = l.events;
+    a.tile_ebase = l.tile_ebase;
+    a.tile_eends = l.tile_eends;
     a.e = e;
     cudaError_t err = cudaFuncSetAttribute(rle_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlSmem);
     if (err != cudaSuccess) return cuda_error(err, "cudaFuncSetAttribute(rle_sliced_kernel)");

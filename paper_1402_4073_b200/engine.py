@@ -222,6 +222,13 @@ class RleQuery:
                    "bq_rle_query_layout_stats")
         return int(m.value), int(l.value)
 
+    @property
+    def layout_events(self) -> int:
+        """Difference-array events of the tile-sliced layout (16-bit each, phase A's input); 0 until built."""
+        e = ctypes.c_uint64(0)
+        _lib.check(self._lib.bq_rle_query_layout_events(self._h, ctypes.byref(e)), "bq_rle_query_layout_events")
+        return int(e.value)
+
     def _outs(self, out, popcnt):
         if out is None:
             out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)
