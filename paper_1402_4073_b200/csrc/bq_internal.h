@@ -102,6 +102,8 @@ struct SlicedLayout {
     const uint16_t *events = nullptr;     // [sum of tile event counts] byte offsets into the difference array
     const uint64_t *tile_ebase = nullptr; // [ntiles + 1] event offset of each tile (multiple of kEvRow)
     const uint4 *tile_eends = nullptr;    // [2 ntiles] cumulative ends of the six lists in 16-byte vectors (+ 2 unused)
+    const uint32_t *tile_order = nullptr; // [ntiles] tiles by descending reach (max ones + dirty of a word):
+                                          // those that can need phase C are scheduled first
     uint64_t bytes = 0;
     uint64_t n_markers = 0, n_literals = 0, n_events = 0;
 };
@@ -121,7 +123,8 @@ struct SlicedEval {
     int nbreak;
     uint64_t *out;
     unsigned long long *popcnt;
-    int debug;
+    int debug;              // BQ_RLE_DEBUG: 1 = skip phase A's updates, 2 = also skip its copies
+    uint32_t *reach_out;    // layout build only: each tile's reach, no output
 };
 int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t stream);
 

@@ -750,7 +750,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         sliced = q->sliced;
     }
     if (sliced.mem && sliced_mode) {
-        SlicedEval se;
+        SlicedEval se{};
         se.n = n;
         se.total_words = q->total_words;
         se.tile0 = q->tile0;

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "bq_internal.h"
@@ -240,6 +241,11 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
     }
 }
 
+__global__ void iota_kernel(uint32_t *ids, uint32_t n) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) ids[k] = k;
+}
+
 // One CTA per (tile, event kind): permute the list (emitted slice by slice) so that
 // each shared-memory atomic instruction of phase A -- event j of the 32 vectors of a
 // warp row -- updates 32 distinct banks.  Events are ranked within their bank (bank =
@@ -332,6 +338,7 @@ struct SlArgs {
     const uint16_t *events;
     const uint64_t *tile_ebase;
     const uint4 *tile_eends;
+    const uint32_t *tile_order;
     SlicedEval e;
 };
 
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
-    const uint32_t tile = blockIdx.x;  // tile of the query's range; its words are global
+    const uint32_t tile = a.tile_order ? a.tile_order[blockIdx.x] : blockIdx.x;  // tile of the query's range
     const uint64_t ts = (uint64_t)(E.tile0 + tile) * kRleTile;
     const int width = (int)min((uint64_t)kRleTile, E.total_words - ts);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -446,11 +453,22 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
 
     // ---- B: prefix sum, then decide every word the fills decide ------------------
     const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
+    if (E.reach_out) {
+        if (tid == 0) E.reach_out[tile] = reach;
+        return;
+    }
     TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out, (uint64_t)E.tile0 * kRleTile,
                  E.breaks, E.nbreak};
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlSlots>());
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
+    if (tid == 0 && n_undecided) {  // phase C decodes the tile's markers: pull them into L2 first
+        const uint64_t m0 = reinterpret_cast<uint64_t>(tmk), m1 = reinterpret_cast<uint64_t>(tmk + nchunks * kSliceChunk);
+        const uint64_t c0 = reinterpret_cast<uint64_t>(meta) & ~15ull, c1 = (reinterpret_cast<uint64_t>(meta + nchunks) + 15) & ~15ull;
+        for (uint64_t p = m0; p < m1; p += 1u << 16)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"((uint32_t)min(m1 - p, (uint64_t)1 << 16)));
+        if (c1 > c0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(c0), "r"((uint32_t)(c1 - c0)));
+    }
 
     // ---- C: literal bits of undecided words (chunks decoded again, literals from HBM) --
     pc += tile_resolve<NT, kSlSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of,
@@ -553,7 +571,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     const size_t o_ev = r16(o_meta + nm / kSliceChunk * 8);
     const size_t o_teb = o_ev + ne * 2;  // ne is a multiple of kEvRow: 16-byte multiple
     const size_t o_tee = r16(o_teb + T1 * 8);
-    const size_t bytes = o_tee + (size_t)ntiles * 32;
+    const size_t o_ord = o_tee + (size_t)ntiles * 32;
+    const size_t bytes = o_ord + (size_t)ntiles * 4;
     char *m = nullptr;
     e = cudaMalloc(&m, bytes);
     if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * 2);  // events as emitted, slice by slice
@@ -594,6 +613,53 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         cudaFree(m);
         return cuda_error(e, "slice_emit_kernel / arrange_events_kernel");
     }
+    // tile order: a reach-only pass of K4s, then tiles sorted by descending reach
+    uint32_t *order = reinterpret_cast<uint32_t *>(m + o_ord);
+    {
+        char *ss = nullptr;
+        size_t sort_bytes = 0;
+        e = cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                      (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)ntiles);
+        if (e == cudaSuccess) e = cudaMalloc(&ss, (size_t)ntiles * 12 + 16 + sort_bytes);
+        if (e != cudaSuccess) {
+            cudaFree(m);
+            return cuda_error(e, "tile order scratch");
+        }
+        uint32_t *reach = reinterpret_cast<uint32_t *>(ss), *reach_sorted = reach + ntiles, *ids = reach_sorted + ntiles;
+        void *sort_tmp = ss + ((size_t)ntiles * 12 + 15) / 16 * 16;
+        SlicedLayout tmp;
+        tmp.markers = markers;
+        tmp.literals = literals;
+        tmp.tile_mbase = tmb;
+        tmp.tile_lbase = tlb;
+        tmp.chunk_meta = meta;
+        tmp.events = events;
+        tmp.tile_ebase = teb;
+        tmp.tile_eends = tee;
+        SlicedEval re{};
+        re.n = n;
+        re.total_words = ~0ull;
+        re.tile0 = tile0;
+        re.ntiles = ntiles;
+        re.reach_out = reach;
+        int rc = launch_sliced(tmp, re, 0);
+        if (rc) {
+            cudaFree(ss);
+            cudaFree(m);
+            return rc;
+        }
+        iota_kernel<<<(ntiles + 255) / 256, 256>>>(ids, ntiles);
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, sort_bytes, reach, reach_sorted, ids, order, (int)ntiles);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        cudaFree(ss);
+        if (e != cudaSuccess) {
+            cudaFree(m);
+            return cuda_error(e, "tile order");
+        }
+    }
+    l.tile_order = order;
     l.markers = markers;
     l.literals = literals;
     l.tile_mbase = tmb;
@@ -625,6 +691,7 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
     a.events = l.events;
     a.tile_ebase = l.tile_ebase;
     a.tile_eends = l.tile_eends;
+    a.tile_order = e.reach_out ? nullptr : l.tile_order;
     a.e = e;
     cudaError_t err = cudaFuncSetAttribute(rle_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlSmem);
     if (err != cudaSuccess) return cuda_error(err, "cudaFuncSetAttribute(rle_sliced_kernel)");

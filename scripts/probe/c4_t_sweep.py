@@ -1,4 +1,6 @@
-"""C4 streams, K4s time per query across thresholds (phase C grows as T falls)."""
+"""C4 streams, K4s time per query across thresholds (phase C grows as T falls).
+
+L2 flushed (256 MB) before each timed launch, as bench.py does."""
 import ctypes
 import json
 import statistics
@@ -34,6 +36,7 @@ pc = torch.zeros(1, dtype=torch.int64, device="cuda")
 q.threshold(50, out, pc)
 q.threshold(50, out, pc)
 res = {}
+scratch = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 TS = [int(x) for x in sys.argv[1:]] or [1, 2, 5, 10, 20, 30, 50, 100, 1024]
 cases = [(f"T={t}", (lambda t=t: q.threshold(t, out, pc))) for t in TS]
 if len(sys.argv) == 1:
@@ -44,6 +47,7 @@ for label, fn in cases:
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
     for a, b in ev:
+        scratch.add_(1)  # L2 flush; also gives the host time to queue the query (kernel time only)
         a.record()
         fn()
         b.record()
