@@ -66,46 +66,40 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 
 // Tile-sliced layout of n RLE streams, derived once per query from the inputs and
 // the K3 directory.  Every (tile, stream) slice -- the stream's words
-// [1024 t, 1024 t + 1024) -- is re-encoded as self-contained markers covering
-// exactly 1024 words (clipped fills, clipped literal groups, a zero fill after
-// the stream's end), stored as 32-bit markers (run | bit << 11 | dirty << 16) in
-// one array and their literal words in another, both tile-major.  Marker arrays
-// of a tile are padded to a multiple of kSliceChunk; one checkpoint per chunk
-// (word position within its slice, pending literal end, literal index) lets any
-// warp decode any chunk.
-constexpr int kSliceChunk = 128;
-//
-// Phase A of K4s reads neither: it reads the tile's difference-array events.  Each
-// slice contributes the nonzero updates its markers make to the packed difference
-// array (ones | dirty << 16) at positions inside the tile, coincident updates of
-// neighbouring markers merged: +1 / -1 where a one-fill starts / ends, +1 / -1 << 16
-// where a literal group starts / ends, +1 - (1 << 16) where a one-fill starts as a
-// literal group ends, -1 + (1 << 16) where a one-fill ends as a literal group starts.
-// Events are 16-bit byte offsets (position * 4) into the difference array, grouped
-// per tile into six lists by kind (all slices of the tile), each padded to whole
-// warp rows (kEvRow events: 32 lanes x one 16-byte vector of 8 events) with offsets
-// of dummy slots past the tile.  Inside a list the events are permuted so that the
-// 32 updates of each shared-memory atomic instruction (event j of the 32 vectors of
-// a row) fall in distinct banks wherever the list allows: phase A adds a
-// warp-uniform constant per event, every update nonzero and bank-conflict free.
+// [1024 t, 1024 t + 1024) -- is re-encoded as what K4s reads, tile-major:
+//  - events (phase A): the nonzero updates the slice's markers make to the packed
+//    difference array (ones | dirty << 16) at positions inside the tile, coincident
+//    updates of neighbouring markers merged: +1 / -1 where a one-fill starts / ends,
+//    +1 / -1 << 16 where a literal group starts / ends, +1 - (1 << 16) where a
+//    one-fill starts as a literal group ends, -1 + (1 << 16) where a one-fill ends as
+//    a literal group starts.  Events are 16-bit byte offsets (position * 4) into the
+//    difference array, grouped per tile into six lists by kind (all slices of the
+//    tile), each padded to whole warp rows (kEvRow events: 32 lanes x one 16-byte
+//    vector of 8 events) with offsets of dummy slots past the tile.  Inside a list
+//    the events are permuted so that the 32 updates of each shared-memory atomic
+//    instruction (event j of the 32 vectors of a row) fall in distinct banks wherever
+//    the list allows: phase A adds a warp-uniform constant per event, every update
+//    nonzero and bank-conflict free.
+//  - literals (phase C): the slice's literal words inside the tile (literal groups
+//    clipped to the tile) and, in a parallel array, each one's word position in the
+//    tile, so phase C finds the literal words of its undecided positions by one
+//    coalesced pass over the tile's positions, with no marker decoding.
 constexpr int kEvVec = 8;                                      // events per 16-byte vector
 constexpr int kEvRow = 32 * kEvVec;                            // events per warp row
 constexpr int kEvKinds = 6;
 constexpr uint16_t kEvDummy = (uint16_t)((kRleTile + 1) * 4);  // byte offset of the first dummy slot (32 follow)
 struct SlicedLayout {
     void *mem = nullptr;
-    const uint32_t *markers = nullptr;    // [sum of padded tile marker counts]
     const uint64_t *literals = nullptr;   // [sum of tile literal counts]
-    const uint64_t *tile_mbase = nullptr; // [ntiles + 1] marker offset of each tile (multiple of kSliceChunk)
+    const uint16_t *lit_pos = nullptr;    // [sum of tile literal counts] word position of each literal in its tile
     const uint64_t *tile_lbase = nullptr; // [ntiles + 1] literal offset of each tile
-    const uint64_t *chunk_meta = nullptr; // [markers / kSliceChunk]: rel | carry << 11 | literal index << 32
     const uint16_t *events = nullptr;     // [sum of tile event counts] byte offsets into the difference array
     const uint64_t *tile_ebase = nullptr; // [ntiles + 1] event offset of each tile (multiple of kEvRow)
     const uint4 *tile_eends = nullptr;    // [2 ntiles] cumulative ends of the six lists in 16-byte vectors (+ 2 unused)
     const uint32_t *tile_order = nullptr; // [ntiles] tiles by descending reach (max ones + dirty of a word):
                                           // those that can need phase C are scheduled first
     uint64_t bytes = 0;
-    uint64_t n_markers = 0, n_literals = 0, n_events = 0;
+    uint64_t n_markers = 0, n_literals = 0, n_events = 0;  // n_markers: slice markers (statistic; not stored)
 };
 // tiles [tile0, tile0 + ntiles) of the streams; directory rows are relative to tile0
 int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t tile0,

@@ -51,12 +51,6 @@ constexpr size_t kSlPhaseC = tile_resolve_bytes<kSlSlots>() + (size_t)kRleTile *
 constexpr size_t kSlRegion = kSlBufBytes > kSlPhaseC ? kSlBufBytes : kSlPhaseC;
 constexpr size_t kSlSmem = kSlCntBytes + 16 + kSlRegion;  // cnt | 2 mbarriers | region
 
-// 32-bit slice marker: run (bits 0-10) | fill bit (bit 11) | dirty (bits 16-26); run, dirty <= 1024
-__device__ __forceinline__ uint32_t mk_bit(uint32_t m) { return (m >> 11) & 1u; }
-__device__ __forceinline__ uint32_t mk_run(uint32_t m) { return m & 0x7FFu; }
-__device__ __forceinline__ uint32_t mk_dirty(uint32_t m) { return m >> 16; }
-__device__ __forceinline__ uint32_t mk_pack(uint32_t bit, uint32_t run, uint32_t dirty) { return run | (bit << 11) | (dirty << 16); }
-
 // ---------------------------------------------------------------------------
 // Layout build, one thread per (tile, stream) slice.  The counting pass maps
 // neighbouring threads to neighbouring tiles of one stream (their reads are
@@ -64,10 +58,8 @@ __device__ __forceinline__ uint32_t mk_pack(uint32_t bit, uint32_t run, uint32_t
 // are adjacent in the tile-major output): 0.9 + 3.0 ms at C4 instead of 0.9 + 5.3.
 
 struct SliceSink {
-    uint32_t *mk;       // tile marker array (null: count only)
-    uint64_t *lit;      // tile literal array
-    uint64_t *meta;     // chunk checkpoints of this tile
-    uint32_t mk0, lit0;  // within-tile index of the slice's first marker / literal
+    uint64_t *lit;           // the slice's first literal word in the tile's literal array
+    uint16_t *pos;           // ... and its word position in the parallel array
     uint16_t *ev[kEvKinds];  // the slice's first entry in each of the tile's event lists
 };
 
@@ -77,30 +69,25 @@ struct SliceCounts {
 };
 
 // Re-encode stream words [ts, ts + 1024) starting at the directory entry e
-// (marker index, fill start): markers, literals, and the slice's nonzero updates
-// to the difference array (events at positions inside the tile; a literal group's
-// end is merged with what the next marker starts at the same position).
+// (marker index, fill start): the slice's literal words with their positions, and
+// its nonzero updates to the difference array (events at positions inside the tile;
+// a literal group's end is merged with what the next marker starts at the same
+// position).  Markers are counted (a layout statistic), not stored.
 template <bool EMIT>
 __device__ SliceCounts slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint64_t ts, const SliceSink &sink) {
     const uint64_t te = ts + kRleTile;
     uint64_t i = e.x, pos = e.y;
     uint32_t rel = 0;
     SliceCounts n{};
-    bool prev_dirty = false;
     bool pend = false;  // the previous marker's literal group ends at rel (its -1 << 16 not yet filed)
     auto event = [&](int kind, uint32_t at) {
         if (EMIT) sink.ev[kind][n.ev[kind]] = (uint16_t)(at * 4u);
         ++n.ev[kind];
     };
     auto emit = [&](uint32_t bit, uint32_t run, uint32_t dirty) {
-        if (EMIT) {
-            const uint32_t j = sink.mk0 + n.mk;
-            sink.mk[j] = mk_pack(bit, run, dirty);
-            if (j % kSliceChunk == 0)
-                sink.meta[j / kSliceChunk] = (uint64_t)rel | ((uint64_t)(rel != 0 && prev_dirty) << 11) |
-                                             ((uint64_t)(sink.lit0 + n.lit) << 32);
-        }
         const uint32_t fe = rel + run, de = fe + dirty;
+        if (EMIT)
+            for (uint32_t k = 0; k < dirty; ++k) sink.pos[n.lit + k] = (uint16_t)(fe + k);
         bool cancel = false;  // a pending literal end meets this marker's literal start (run 0)
         if (pend) {
             if (bit) event(4, rel);
@@ -118,7 +105,6 @@ __device__ SliceCounts slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint
         pend = dirty && de < (uint32_t)kRleTile;
         ++n.mk;
         rel = de;
-        prev_dirty = dirty != 0;
     };
     while (rel < (uint32_t)kRleTile) {
         if (i >= L) {  // implicit zero tail
@@ -134,7 +120,7 @@ __device__ SliceCounts slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint
         const uint32_t cdirty = cde > cds ? (uint32_t)(cde - cds) : 0u;
         if (crun + cdirty) {
             if (EMIT)
-                for (uint32_t k = 0; k < cdirty; ++k) sink.lit[sink.lit0 + n.lit + k] = __ldg(src + i + 1 + (cds - fe) + k);
+                for (uint32_t k = 0; k < cdirty; ++k) sink.lit[n.lit + k] = __ldg(src + i + 1 + (cds - fe) + k);
             emit((uint32_t)(m & 1) & (crun != 0u), crun, cdirty);
             n.lit += cdirty;
         }
@@ -161,7 +147,7 @@ __global__ void slice_count_kernel(const uint64_t *const *ptrs, const uint64_t *
 
 // One CTA per tile: exclusive scans of the slice counts in place (two 32-bit counts
 // per 64-bit value: each half of a tile's sum stays below 2^32), and the tile totals:
-// markers rounded up to whole chunks, literals, the event lists' real lengths, their
+// markers, literals, the event lists' real lengths, their
 // cumulative ends in 16-byte vectors (each list padded to whole warp rows) and the
 // tile's event total.
 __global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, ulonglong4 *ecounts, int n, uint64_t *tile_m,
@@ -198,7 +184,7 @@ __global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, ulon
     }
     if (threadIdx.x == 0) {
         const uint64_t m = carry[0] & 0xFFFFFFFFull, l = carry[0] >> 32;
-        tile_m[t] = (m + kSliceChunk - 1) / kSliceChunk * kSliceChunk;
+        tile_m[t] = m;
         tile_l[t] = l;
         uint32_t end[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, acc = 0;
         for (int k = 0; k < kEvKinds; ++k) {
@@ -215,9 +201,8 @@ __global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, ulon
 
 __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
                                   uint32_t tile0, uint32_t ntiles, const uint64_t *offs, const ulonglong4 *eoffs,
-                                  const uint64_t *mbase, const uint64_t *lbase, const uint64_t *ebase,
-                                  const uint4 *eends, uint32_t *markers, uint64_t *literals, uint64_t *meta,
-                                  uint16_t *events) {
+                                  const uint64_t *lbase, const uint64_t *ebase, const uint4 *eends,
+                                  uint64_t *literals, uint16_t *lit_pos, uint16_t *events) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
         const int s = (int)(k % n);  // neighbouring threads: neighbouring slices of one tile (writes)
@@ -230,11 +215,8 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
                                            (uint32_t)(eo.y >> 32), (uint32_t)eo.z, (uint32_t)(eo.z >> 32)};
         uint16_t *tev = events + ebase[t];
         SliceSink sink;
-        sink.mk = markers + mbase[t];
-        sink.lit = literals + lbase[t];
-        sink.meta = meta + mbase[t] / kSliceChunk;
-        sink.mk0 = (uint32_t)o;
-        sink.lit0 = (uint32_t)(o >> 32);
+        sink.lit = literals + lbase[t] + (uint32_t)(o >> 32);
+        sink.pos = lit_pos + lbase[t] + (uint32_t)(o >> 32);
 #pragma unroll
         for (int q = 0; q < kEvKinds; ++q) sink.ev[q] = tev + (size_t)starts[q] * kEvVec + within[q];
         slice_walk<true>(ptrs[s], lens[s], dir[(size_t)t * n + s], (uint64_t)(tile0 + t) * kRleTile, sink);
@@ -332,17 +314,15 @@ __global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src
 // K4s: one CTA per tile.
 
 struct SlArgs {
-    const uint32_t *markers;
     const uint64_t *literals;
-    const uint64_t *tile_mbase, *tile_lbase, *chunk_meta;
+    const uint16_t *lit_pos;
+    const uint64_t *tile_lbase;
     const uint16_t *events;
     const uint64_t *tile_ebase;
     const uint4 *tile_eends;
     const uint32_t *tile_order;
     SlicedEval e;
 };
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) { return warp_incl_scan_u32(v, lane); }
 
 // Two events (16-bit byte offsets into the difference array) of one 32-bit word.
 __device__ __forceinline__ void add_events(uint32_t *cnt, uint32_t w, uint32_t delta) {
@@ -383,11 +363,10 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     const uint64_t ts = (uint64_t)(E.tile0 + tile) * kRleTile;
     const int width = (int)min((uint64_t)kRleTile, E.total_words - ts);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t mbase = a.tile_mbase[tile];
-    const uint32_t nchunks = (uint32_t)((a.tile_mbase[tile + 1] - mbase) / kSliceChunk);
-    const uint64_t *meta = a.chunk_meta + mbase / kSliceChunk;
-    const uint32_t *tmk = a.markers + mbase;
-    const uint64_t *tlit = a.literals + a.tile_lbase[tile];
+    const uint64_t lbase = a.tile_lbase[tile];
+    const uint32_t nlit = (uint32_t)(a.tile_lbase[tile + 1] - lbase);
+    const uint64_t *tlit = a.literals + lbase;
+    const uint16_t *tpos = a.lit_pos + lbase;
     const EvEnds ee{a.tile_eends[2 * tile], a.tile_eends[2 * tile + 1]};
     const uint32_t nvec = ee.b.z;
     const uint4 *tev = reinterpret_cast<const uint4 *>(a.events + a.tile_ebase[tile]);
@@ -462,41 +441,33 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlSlots>());
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
-    if (tid == 0 && n_undecided) {  // phase C decodes the tile's markers: pull them into L2 first
-        const uint64_t m0 = reinterpret_cast<uint64_t>(tmk), m1 = reinterpret_cast<uint64_t>(tmk + nchunks * kSliceChunk);
-        const uint64_t c0 = reinterpret_cast<uint64_t>(meta) & ~15ull, c1 = (reinterpret_cast<uint64_t>(meta + nchunks) + 15) & ~15ull;
-        for (uint64_t p = m0; p < m1; p += 1u << 16)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"((uint32_t)min(m1 - p, (uint64_t)1 << 16)));
-        if (c1 > c0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(c0), "r"((uint32_t)(c1 - c0)));
+    if (tid == 0 && n_undecided) {  // phase C reads the tile's literal positions and some of its literals
+        auto prefetch = [](const void *from, const void *to) {
+            const uint64_t p0 = reinterpret_cast<uint64_t>(from) & ~15ull;
+            const uint64_t p1 = (reinterpret_cast<uint64_t>(to) + 15) & ~15ull;
+            for (uint64_t p = p0; p < p1; p += 1u << 16)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"((uint32_t)min(p1 - p, (uint64_t)1 << 16)));
+        };
+        prefetch(tpos, tpos + nlit);
+        prefetch(tlit, tlit + nlit);
     }
 
-    // ---- C: literal bits of undecided words (chunks decoded again, literals from HBM) --
+    // ---- C: literal bits of undecided words ---------------------------------------
     pc += tile_resolve<NT, kSlSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of,
                                                                                  auto &&add_bits) {
-        for (uint32_t c = warp; c < nchunks; c += NT / 32) {
-            const uint64_t cm = __ldg(meta + c);
-            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(tmk) + c * 32 + lane);
-            const uint32_t m[4] = {v.x, v.y, v.z, v.w};
-            uint32_t tot = 0, dtot = 0;
+        constexpr int kAhead = 8;  // position loads in flight per thread
+        for (uint32_t base = 0; base < nlit; base += kAhead * NT) {
+            uint16_t p[kAhead];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                tot += mk_run(m[k]) + mk_dirty(m[k]);
-                dtot += mk_dirty(m[k]);
+            for (int k = 0; k < kAhead; ++k) {
+                const uint32_t i = base + k * NT + tid;
+                p[k] = i < nlit ? __ldg(tpos + i) : kNoSlot;
             }
-            const uint32_t incl_len = warp_incl_scan(tot, lane);
-            const uint32_t incl_lit = warp_incl_scan(dtot, lane);
-            uint32_t rel = ((uint32_t)cm + incl_len - tot) & (kRleTile - 1);
-            uint32_t lit = (uint32_t)(cm >> 32) + incl_lit - dtot;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t run = mk_run(m[k]), dirty = mk_dirty(m[k]);
-                const uint32_t fe = rel + run;
-                for (uint32_t q = 0; q < dirty; ++q) {
-                    const uint16_t u = slot_of[fe + q];
-                    if (u != kNoSlot) add_bits(u, tlit + lit + q);
-                }
-                lit += dirty;
-                rel = (fe + dirty) & (kRleTile - 1);
+            for (int k = 0; k < kAhead; ++k) {
+                if (p[k] == kNoSlot) continue;
+                const uint16_t u = slot_of[p[k]];
+                if (u != kNoSlot) add_bits(u, tlit + base + k * NT + tid);
             }
         }
     });
@@ -515,7 +486,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     const uint64_t cells = (uint64_t)ntiles * n;
     const size_t T1 = (size_t)ntiles + 1;
     // scratch: slice event counts / offsets (32 B per slice) | slice marker and literal
-    // counts / offsets | tile marker, literal, event totals and their scans | list ends
+    // counts / offsets | tile marker (statistic), literal, event totals and their scans | list ends
     // | real list lengths | CUB temp
     size_t tmp_bytes = 0, tmp2 = 0;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
@@ -561,18 +532,16 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     if (e == cudaSuccess) e = cudaMemcpy(&nl, lb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(&ne, eb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(e, "slice scans");
-    // markers | literals | tile_mbase | tile_lbase | chunk_meta | events | tile_ebase | tile_eends
-    // (markers, events and tile_eends at 16-byte boundaries)
+    // literals | tile_lbase | events | tile_ebase | tile_eends | tile_order | literal positions
+    // (literals, events and tile_eends at 16-byte boundaries)
     auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
-    const size_t o_lit = r16(nm * 4);
-    const size_t o_tmb = o_lit + nl * 8;
-    const size_t o_tlb = o_tmb + T1 * 8;
-    const size_t o_meta = o_tlb + T1 * 8;
-    const size_t o_ev = r16(o_meta + nm / kSliceChunk * 8);
+    const size_t o_tlb = nl * 8;
+    const size_t o_ev = r16(o_tlb + T1 * 8);
     const size_t o_teb = o_ev + ne * 2;  // ne is a multiple of kEvRow: 16-byte multiple
     const size_t o_tee = r16(o_teb + T1 * 8);
     const size_t o_ord = o_tee + (size_t)ntiles * 32;
-    const size_t bytes = o_ord + (size_t)ntiles * 4;
+    const size_t o_pos = o_ord + (size_t)ntiles * 4;
+    const size_t bytes = o_pos + nl * 2;
     char *m = nullptr;
     e = cudaMalloc(&m, bytes);
     if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * 2);  // events as emitted, slice by slice
@@ -584,21 +553,18 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     }
     SlicedLayout l;
     l.mem = m;
-    uint32_t *markers = reinterpret_cast<uint32_t *>(m);
-    uint64_t *literals = reinterpret_cast<uint64_t *>(m + o_lit);
-    uint64_t *tmb = reinterpret_cast<uint64_t *>(m + o_tmb), *tlb = reinterpret_cast<uint64_t *>(m + o_tlb);
-    uint64_t *meta = reinterpret_cast<uint64_t *>(m + o_meta);
+    uint64_t *literals = reinterpret_cast<uint64_t *>(m);
+    uint64_t *tlb = reinterpret_cast<uint64_t *>(m + o_tlb);
     uint16_t *events = reinterpret_cast<uint16_t *>(m + o_ev);
     uint64_t *teb = reinterpret_cast<uint64_t *>(m + o_teb);
     uint4 *tee = reinterpret_cast<uint4 *>(m + o_tee);
-    e = cudaMemset(markers, 0, o_lit);  // chunk padding decodes to empty markers
-    if (e == cudaSuccess) e = cudaMemcpy(tmb, mb, T1 * 8, cudaMemcpyDeviceToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(tlb, lb, T1 * 8, cudaMemcpyDeviceToDevice);
+    uint16_t *lit_pos = reinterpret_cast<uint16_t *>(m + o_pos);
+    e = cudaMemcpy(tlb, lb, T1 * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(teb, eb, T1 * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(tee, eends, (size_t)ntiles * 32, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) {
-        slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts, tmb, tlb, teb, tee,
-                                         markers, literals, meta, reinterpret_cast<uint16_t *>(evsrc));
+        slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts, tlb, teb, tee,
+                                         literals, lit_pos, reinterpret_cast<uint16_t *>(evsrc));
         e = cudaGetLastError();
     }
     if (e == cudaSuccess && ne) {
@@ -628,11 +594,9 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         uint32_t *reach = reinterpret_cast<uint32_t *>(ss), *reach_sorted = reach + ntiles, *ids = reach_sorted + ntiles;
         void *sort_tmp = ss + ((size_t)ntiles * 12 + 15) / 16 * 16;
         SlicedLayout tmp;
-        tmp.markers = markers;
         tmp.literals = literals;
-        tmp.tile_mbase = tmb;
+        tmp.lit_pos = lit_pos;
         tmp.tile_lbase = tlb;
-        tmp.chunk_meta = meta;
         tmp.events = events;
         tmp.tile_ebase = teb;
         tmp.tile_eends = tee;
@@ -660,11 +624,9 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         }
     }
     l.tile_order = order;
-    l.markers = markers;
     l.literals = literals;
-    l.tile_mbase = tmb;
+    l.lit_pos = lit_pos;
     l.tile_lbase = tlb;
-    l.chunk_meta = meta;
     l.events = events;
     l.tile_ebase = teb;
     l.tile_eends = tee;
@@ -683,11 +645,9 @@ void free_sliced(SlicedLayout *l) {
 
 int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t stream) {
     SlArgs a;
-    a.markers = l.markers;
     a.literals = l.literals;
-    a.tile_mbase = l.tile_mbase;
+    a.lit_pos = l.lit_pos;
     a.tile_lbase = l.tile_lbase;
-    a.chunk_meta = l.chunk_meta;
     a.events = l.events;
     a.tile_ebase = l.tile_ebase;
     a.tile_eends = l.tile_eends;

@@ -45,7 +45,7 @@ for label, fn in cases:
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
     for a, b in ev:
         scratch.add_(1)  # L2 flush; also gives the host time to queue the query (kernel time only)
         a.record()
@@ -54,5 +54,5 @@ for label, fn in cases:
     torch.cuda.synchronize()
     pc.zero_()
     fn()
-    res[label] = {"ms": round(statistics.mean(a.elapsed_time(b) for a, b in ev), 4), "popcount": int(pc.item())}
+    res[label] = {"ms": round(statistics.median(a.elapsed_time(b) for a, b in ev), 4), "popcount": int(pc.item())}
 print(json.dumps(res))
