@@ -80,10 +80,11 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 //    instruction (event j of the 32 vectors of a row) fall in distinct banks wherever
 //    the list allows: phase A adds a warp-uniform constant per event, every update
 //    nonzero and bank-conflict free.
-//  - literals (phase C): the slice's literal words inside the tile (literal groups
-//    clipped to the tile) and, in a parallel array, each one's word position in the
-//    tile, so phase C finds the literal words of its undecided positions by one
-//    coalesced pass over the tile's positions, with no marker decoding.
+//  - literals (phase C): every slice's literal words inside the tile (literal groups
+//    clipped to the tile), ordered position-major: the literal words at word p of
+//    the tile are [lit_start[p], lit_start[p + 1]) of the tile's literal array, so
+//    phase C reads an undecided word's literals contiguously, with no marker
+//    decoding.
 constexpr int kEvVec = 8;                                      // events per 16-byte vector
 constexpr int kEvRow = 32 * kEvVec;                            // events per warp row
 constexpr int kEvKinds = 6;
@@ -91,7 +92,7 @@ constexpr uint16_t kEvDummy = (uint16_t)((kRleTile + 1) * 4);  // byte offset of
 struct SlicedLayout {
     void *mem = nullptr;
     const uint64_t *literals = nullptr;   // [sum of tile literal counts]
-    const uint16_t *lit_pos = nullptr;    // [sum of tile literal counts] word position of each literal in its tile
+    const uint32_t *lit_start = nullptr;  // [ntiles][kRleTile + 1] offset of each word's literals in its tile
     const uint64_t *tile_lbase = nullptr; // [ntiles + 1] literal offset of each tile
     const uint16_t *events = nullptr;     // [sum of tile event counts] byte offsets into the difference array
     const uint64_t *tile_ebase = nullptr; // [ntiles + 1] event offset of each tile (multiple of kEvRow)

@@ -39,15 +39,13 @@ namespace {
 #define BQ_SL_NT 128
 #define BQ_SL_MINB 5
 #endif
-#ifndef BQ_SL_SLOTS
-#define BQ_SL_SLOTS 256
-#endif
 constexpr int kSlNT = BQ_SL_NT;                            // K4s threads per CTA (4 warps)
 constexpr int kPieceVecs = 1024;                           // event vectors per staged piece (16 KB)
-constexpr int kSlSlots = BQ_SL_SLOTS;                      // undecided words per phase-C pass
+constexpr uint32_t kThreadWordMax = 128;                   // phase C: words with more literals get a warp
+constexpr int kLitStarts = kRleTile + 1;                   // literal offsets per tile (position-major)
 constexpr size_t kSlCntBytes = (size_t)(kRleTile + 36) * 4;  // + sentinel + 32 per-lane dummies (+ pad)
 constexpr size_t kSlBufBytes = 2 * (size_t)kPieceVecs * 16;
-constexpr size_t kSlPhaseC = tile_resolve_bytes<kSlSlots>() + (size_t)kRleTile * 2;  // + undecided list
+constexpr size_t kSlPhaseC = (size_t)kRleTile * 4;  // undecided and heavy word lists
 constexpr size_t kSlRegion = kSlBufBytes > kSlPhaseC ? kSlBufBytes : kSlPhaseC;
 constexpr size_t kSlSmem = kSlCntBytes + 16 + kSlRegion;  // cnt | 2 mbarriers | region
 
@@ -228,6 +226,42 @@ __global__ void iota_kernel(uint32_t *ids, uint32_t n) {
     if (k < n) ids[k] = k;
 }
 
+// One CTA per tile: the tile's literal words (emitted slice by slice, each with its
+// word position) reordered position-major -- the literals at word p of the tile are
+// [lit_start[p], lit_start[p + 1]) -- by a counting sort over the 1024 positions.
+__global__ void __launch_bounds__(512) sort_literals_kernel(const uint64_t *lit_src, const uint16_t *pos_src,
+                                                            const uint64_t *lbase, uint64_t *lit, uint32_t *lit_start) {
+    using Scan = cub::BlockScan<uint32_t, 512>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t start[kRleTile], fill[kRleTile];
+    const uint32_t t = blockIdx.x;
+    const int tid = threadIdx.x;
+    const uint64_t b = lbase[t];
+    const uint32_t n = (uint32_t)(lbase[t + 1] - b);
+    for (int k = tid; k < kRleTile; k += 512) {
+        start[k] = 0;
+        fill[k] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += 512) atomicAdd(&start[pos_src[b + i]], 1u);
+    __syncthreads();
+    const uint32_t v0 = start[2 * tid], v1 = start[2 * tid + 1];
+    uint32_t ex;
+    Scan(tmp).ExclusiveSum(v0 + v1, ex);
+    __syncthreads();
+    start[2 * tid] = ex;
+    start[2 * tid + 1] = ex + v0;
+    uint32_t *ls = lit_start + (size_t)t * kLitStarts;
+    ls[2 * tid] = ex;
+    ls[2 * tid + 1] = ex + v0;
+    if (tid == 0) ls[kRleTile] = n;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += 512) {
+        const uint32_t p = pos_src[b + i];
+        lit[b + start[p] + atomicAdd(&fill[p], 1u)] = lit_src[b + i];
+    }
+}
+
 // One CTA per (tile, event kind): permute the list (emitted slice by slice) so that
 // each shared-memory atomic instruction of phase A -- event j of the 32 vectors of a
 // warp row -- updates 32 distinct banks.  Events are ranked within their bank (bank =
@@ -315,7 +349,7 @@ __global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src
 
 struct SlArgs {
     const uint64_t *literals;
-    const uint16_t *lit_pos;
+    const uint32_t *lit_start;
     const uint64_t *tile_lbase;
     const uint16_t *events;
     const uint64_t *tile_ebase;
@@ -348,6 +382,36 @@ __device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, uint32_
     add_events(cnt, v.w, delta);
 }
 
+// Bit-sliced sum (planes 0..M-1 of the 64 per-bit counts) of n contiguous literal
+// words, four loads in flight.
+template <int M>
+__device__ __forceinline__ void planes_sum_contig(const uint64_t *p, uint32_t n, uint64_t (&c)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) c[j] = 0ull;
+    uint32_t i = 0;
+    for (; i + 4 <= n; i += 4) {
+        uint64_t x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = __ldg(p + i + k);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ripple<M>(c, x[k]);
+    }
+    for (; i < n; ++i) ripple<M>(c, __ldg(p + i));
+}
+
+// Write result word p of the tile (masked past r); returns its popcount.
+__device__ __forceinline__ unsigned long long sl_store(const TileDecide &d, uint32_t p, uint64_t w) {
+    if (d.ts + p == d.total_words - 1) w &= d.last_mask;
+    d.out[d.ts - d.out_first + p] = w;
+    return __popcll(w);
+}
+
+__device__ __forceinline__ void sl_finish(unsigned long long pc, int lane, unsigned long long *popcnt) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
+    if (lane == 0 && pc && popcnt) atomicAdd(popcnt, pc);
+}
+
 __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __grid_constant__ SlArgs a) {
     constexpr int NT = kSlNT;
     extern __shared__ __align__(128) uint8_t sl_smem[];
@@ -355,7 +419,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     uint64_t *bars = reinterpret_cast<uint64_t *>(sl_smem + kSlCntBytes);
     uint8_t *region = sl_smem + kSlCntBytes + 16;
     uint4 *buf = reinterpret_cast<uint4 *>(region);  // [2][kPieceVecs]
-    __shared__ uint32_t n_undecided;
+    __shared__ uint32_t n_undecided, n_heavy;
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
@@ -366,7 +430,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     const uint64_t lbase = a.tile_lbase[tile];
     const uint32_t nlit = (uint32_t)(a.tile_lbase[tile + 1] - lbase);
     const uint64_t *tlit = a.literals + lbase;
-    const uint16_t *tpos = a.lit_pos + lbase;
+    const uint32_t *tls = a.lit_start + (size_t)tile * kLitStarts;
     const EvEnds ee{a.tile_eends[2 * tile], a.tile_eends[2 * tile + 1]};
     const uint32_t nvec = ee.b.z;
     const uint4 *tev = reinterpret_cast<const uint4 *>(a.events + a.tile_ebase[tile]);
@@ -389,6 +453,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     for (int k = tid; k < kRleTile + 36; k += NT) cnt[k] = 0u;
     if (tid == 0) {
         n_undecided = 0;
+        n_heavy = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -438,44 +503,69 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     }
     TileDecide d{ts, width, E.total_words, E.last_mask, E.accept_bits, E.const_until, E.out, (uint64_t)E.tile0 * kRleTile,
                  E.breaks, E.nbreak};
-    uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlSlots>());
+    uint16_t *undecided = reinterpret_cast<uint16_t *>(region);  // [kRleTile]
+    uint16_t *heavy = undecided + kRleTile;                      // [kRleTile]
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
-    if (tid == 0 && n_undecided) {  // phase C reads the tile's literal positions and some of its literals
+    const uint32_t nu = n_undecided;
+    if (!nu) {
+        sl_finish(pc, lane, E.popcnt);
+        return;
+    }
+    if (tid == 0) {  // phase C reads the tile's literal offsets and some of its literals
         auto prefetch = [](const void *from, const void *to) {
             const uint64_t p0 = reinterpret_cast<uint64_t>(from) & ~15ull;
             const uint64_t p1 = (reinterpret_cast<uint64_t>(to) + 15) & ~15ull;
             for (uint64_t p = p0; p < p1; p += 1u << 16)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"((uint32_t)min(p1 - p, (uint64_t)1 << 16)));
         };
-        prefetch(tpos, tpos + nlit);
+        prefetch(tls, tls + kRleTile);
         prefetch(tlit, tlit + nlit);
     }
 
     // ---- C: literal bits of undecided words ---------------------------------------
-    pc += tile_resolve<NT, kSlSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of,
-                                                                                 auto &&add_bits) {
-        constexpr int kAhead = 8;  // position loads in flight per thread
-        for (uint32_t base = 0; base < nlit; base += kAhead * NT) {
-            uint16_t p[kAhead];
+    // A word's literal words are contiguous (position-major literals): one thread
+    // sums them into bit-sliced counters in registers and decides all 64 bits with
+    // bit-sliced comparisons (runmerge.py:99-125's per-bit count, 64 positions at a
+    // time); words with many literals go to a warp each.
+    for (uint32_t u = tid; u < nu; u += NT) {
+        const uint32_t p = undecided[u];
+        const uint32_t c = cnt[p], ones = c & 0xFFFFu, dirty = c >> 16;
+        if (dirty >= kThreadWordMax) {
+            heavy[atomicAdd(&n_heavy, 1u)] = (uint16_t)p;
+            continue;
+        }
+        const uint64_t *lits = tlit + __ldg(tls + p);
+        uint64_t planes[16];
+        if (dirty < 16) planes_sum_contig<4>(lits, dirty, planes);
+        else planes_sum_contig<7>(lits, dirty, planes);
+        pc += sl_store(d, p, decide_word(d, ones, dirty, planes));
+    }
+    __syncthreads();
+    for (uint32_t h = warp; h < n_heavy; h += NT / 32) {
+        const uint32_t p = heavy[h];
+        const uint32_t c = cnt[p], ones = c & 0xFFFFu, dirty = c >> 16;
+        const uint64_t *lits = tlit + __ldg(tls + p);
+        uint32_t c_lo = 0, c_hi = 0;  // this lane's bit positions: lane, lane + 32
+        for (uint32_t j0 = 0; j0 < dirty; j0 += 32) {
+            const uint64_t x = j0 + lane < dirty ? __ldg(lits + j0 + lane) : 0ull;
 #pragma unroll
-            for (int k = 0; k < kAhead; ++k) {
-                const uint32_t i = base + k * NT + tid;
-                p[k] = i < nlit ? __ldg(tpos + i) : kNoSlot;
-            }
-#pragma unroll
-            for (int k = 0; k < kAhead; ++k) {
-                if (p[k] == kNoSlot) continue;
-                const uint16_t u = slot_of[p[k]];
-                if (u != kNoSlot) add_bits(u, tlit + base + k * NT + tid);
+            for (int b = 0; b < 32; ++b) {
+                const uint32_t lo = __popc(__ballot_sync(0xffffffffu, (x >> b) & 1u));
+                const uint32_t hi = __popc(__ballot_sync(0xffffffffu, (x >> (b + 32)) & 1u));
+                if (lane == b) {
+                    c_lo += lo;
+                    c_hi += hi;
+                }
             }
         }
-    });
-
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
-    if (lane == 0 && pc && E.popcnt) atomicAdd(E.popcnt, pc);
+        const uint64_t w = (uint64_t)__ballot_sync(0xffffffffu, accept_at(d.accept_bits, ones + c_lo)) |
+                           ((uint64_t)__ballot_sync(0xffffffffu, accept_at(d.accept_bits, ones + c_hi)) << 32);
+        if (lane == 0) pc += sl_store(d, p, w);
+    }
+    sl_finish(pc, lane, E.popcnt);
 }
+
 
 }  // namespace
 
@@ -532,22 +622,24 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     if (e == cudaSuccess) e = cudaMemcpy(&nl, lb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(&ne, eb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(e, "slice scans");
-    // literals | tile_lbase | events | tile_ebase | tile_eends | tile_order | literal positions
+    // literals | tile_lbase | lit_start | events | tile_ebase | tile_eends | tile_order
     // (literals, events and tile_eends at 16-byte boundaries)
     auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
     const size_t o_tlb = nl * 8;
-    const size_t o_ev = r16(o_tlb + T1 * 8);
+    const size_t o_ls = o_tlb + T1 * 8;
+    const size_t o_ev = r16(o_ls + (size_t)ntiles * kLitStarts * 4);
     const size_t o_teb = o_ev + ne * 2;  // ne is a multiple of kEvRow: 16-byte multiple
     const size_t o_tee = r16(o_teb + T1 * 8);
     const size_t o_ord = o_tee + (size_t)ntiles * 32;
-    const size_t o_pos = o_ord + (size_t)ntiles * 4;
-    const size_t bytes = o_pos + nl * 2;
-    char *m = nullptr;
+    const size_t bytes = o_ord + (size_t)ntiles * 4;
+    char *m = nullptr, *tmpl = nullptr;  // tmpl: literals and positions as emitted, slice by slice
     e = cudaMalloc(&m, bytes);
     if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * 2);  // events as emitted, slice by slice
+    if (e == cudaSuccess) e = cudaMalloc(&tmpl, nl * 10 + 16);
     if (e != cudaSuccess) {
         cudaGetLastError();
         if (m) cudaFree(m);
+        if (evsrc) cudaFree(evsrc);
         cudaFree(scratch);
         return BQ_OK;
     }
@@ -555,16 +647,22 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     l.mem = m;
     uint64_t *literals = reinterpret_cast<uint64_t *>(m);
     uint64_t *tlb = reinterpret_cast<uint64_t *>(m + o_tlb);
+    uint32_t *lit_start = reinterpret_cast<uint32_t *>(m + o_ls);
     uint16_t *events = reinterpret_cast<uint16_t *>(m + o_ev);
     uint64_t *teb = reinterpret_cast<uint64_t *>(m + o_teb);
     uint4 *tee = reinterpret_cast<uint4 *>(m + o_tee);
-    uint16_t *lit_pos = reinterpret_cast<uint16_t *>(m + o_pos);
+    uint64_t *lit_src = reinterpret_cast<uint64_t *>(tmpl);
+    uint16_t *pos_src = reinterpret_cast<uint16_t *>(tmpl + nl * 8);
     e = cudaMemcpy(tlb, lb, T1 * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(teb, eb, T1 * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(tee, eends, (size_t)ntiles * 32, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) {
         slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts, tlb, teb, tee,
-                                         literals, lit_pos, reinterpret_cast<uint16_t *>(evsrc));
+                                         lit_src, pos_src, reinterpret_cast<uint16_t *>(evsrc));
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        sort_literals_kernel<<<ntiles, 512>>>(lit_src, pos_src, tlb, literals, lit_start);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess && ne) {
@@ -574,10 +672,11 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaFree(scratch);
+    cudaFree(tmpl);
     if (evsrc) cudaFree(evsrc);
     if (e != cudaSuccess) {
         cudaFree(m);
-        return cuda_error(e, "slice_emit_kernel / arrange_events_kernel");
+        return cuda_error(e, "slice_emit_kernel / sort_literals_kernel / arrange_events_kernel");
     }
     // tile order: a reach-only pass of K4s, then tiles sorted by descending reach
     uint32_t *order = reinterpret_cast<uint32_t *>(m + o_ord);
@@ -595,7 +694,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         void *sort_tmp = ss + ((size_t)ntiles * 12 + 15) / 16 * 16;
         SlicedLayout tmp;
         tmp.literals = literals;
-        tmp.lit_pos = lit_pos;
+        tmp.lit_start = lit_start;
         tmp.tile_lbase = tlb;
         tmp.events = events;
         tmp.tile_ebase = teb;
@@ -625,7 +724,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     }
     l.tile_order = order;
     l.literals = literals;
-    l.lit_pos = lit_pos;
+    l.lit_start = lit_start;
     l.tile_lbase = tlb;
     l.events = events;
     l.tile_ebase = teb;
@@ -646,7 +745,7 @@ void free_sliced(SlicedLayout *l) {
 int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t stream) {
     SlArgs a;
     a.literals = l.literals;
-    a.lit_pos = l.lit_pos;
+    a.lit_start = l.lit_start;
     a.tile_lbase = l.tile_lbase;
     a.events = l.events;
     a.tile_ebase = l.tile_ebase;
