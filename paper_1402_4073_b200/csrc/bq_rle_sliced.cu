@@ -37,10 +37,13 @@ namespace {
 
 #ifndef BQ_SL_NT
 #define BQ_SL_NT 128
-#define BQ_SL_MINB 5
+#define BQ_SL_MINB 8
 #endif
 constexpr int kSlNT = BQ_SL_NT;                            // K4s threads per CTA (4 warps)
-constexpr int kPieceVecs = 1024;                           // event vectors per staged piece (16 KB)
+#ifndef BQ_SL_PIECE
+#define BQ_SL_PIECE 640
+#endif
+constexpr int kPieceVecs = BQ_SL_PIECE;                    // event vectors per staged piece (10 KB; 8 CTAs per SM)
 constexpr uint32_t kThreadWordMax = 128;                   // phase C: words with more literals get a warp
 constexpr int kLitStarts = kRleTile + 1;                   // literal offsets per tile (position-major)
 constexpr size_t kSlCntBytes = (size_t)(kRleTile + 36) * 4;  // + sentinel + 32 per-lane dummies (+ pad)
