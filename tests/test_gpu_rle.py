@@ -267,6 +267,42 @@ def test_all_literal_streams_overflow_pools(bq):
     assert np.array_equal(host(out, nw), exp)
 
 
+def test_heavy_words_and_bank_skewed_events(bq):
+    """K4s phase C's warp path (words with >= 128 literal words) next to its thread
+    path in the same tiles, and event lists skewed onto a few shared-memory banks
+    (literal words only at positions = 0 mod 32, so every literal start / end event
+    falls in banks 0 and 1 and the bank arrangement cannot spread them)."""
+    from oracle import oracle as Or
+
+    rng = np.random.default_rng(23)
+    n, r = 300, 64 * 2500 + 13
+    nw = (r + 63) // 64
+    streams = []
+    for i in range(n):
+        if i < 200:  # dense random words: every word a literal
+            w = rng.integers(0, 2**64 - 1, size=nw, dtype=np.uint64)
+        else:  # literals at multiples of 32, runs of ones in between for some streams
+            w = np.zeros(nw, dtype=np.uint64)
+            w[::32] = rng.integers(1, 2**63, size=len(w[::32]), dtype=np.uint64)
+            if i % 3 == 0:
+                w[5::64] = np.uint64(2**64 - 1)
+        w[-1] &= np.uint64((1 << (r % 64)) - 1)
+        streams.append(Or.rle_compress(Or.trim(w), r))
+    q = bq.RleQuery(dev(streams), r)
+    for t in (1, 100, 150, 201, 300):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+    for acc in ([bool(x) for x in rng.integers(0, 2, n + 1)],  # > 64 breakpoints: per-bit decisions
+                [k % 2 == 1 for k in range(n + 1)],
+                [90 <= k <= 110 for k in range(n + 1)]):
+        out, pc = q.symmetric(acc)
+        exp = O.cdom_symmetric(streams, r, acc)
+        assert np.array_equal(host(out, nw), exp)
+        assert int(pc.item()) == popcount(exp)
+
+
 def test_repeated_dropin_calls_reuse_the_prepared_query(bq):
     """Immutable inputs: the second cdom call on the same objects reuses the
     query (and its K3 directory) and returns the identical result."""
