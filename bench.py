@@ -607,14 +607,15 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
     cpu_s = time.perf_counter() - t0
     exact_window = ctx.rank != 0 or np.array_equal(out[: wr // 64].cpu().numpy().view(np.uint64), wexp)
     wbytes = sum(s.size for s in wstreams) * 8
-    # K4s moves its tile-sliced layout, not the EWAH words: every 16-bit difference-array
-    # event of phase A (padded lists), the per-tile list table and the output; markers and
+    # K4s moves its tile-sliced layout, not the EWAH words: every difference-array event
+    # of phase A (10-bit, 12 per 16-byte vector, padded lists), the per-tile tables and the
+    # output; markers and
     # literal words only at undecided positions (popcount-sized here), so they are left
     # out of the algorithmic bytes
     n_mk, n_lit = q.layout_stats
     n_ev = q.layout_events
     tiles = (q.out_words + 1023) // 1024
-    kernel_bytes = (n_ev * 2 + tiles * 40 + q.out_words * 8) if n_ev else comp_bytes + q.out_words * 8
+    kernel_bytes = (n_ev // 12 * 16 + tiles * 76 + q.out_words * 8) if n_ev else comp_bytes + q.out_words * 8
     line = _line("c4", comp_bytes / (statistics.mean(ms) / 1e3) / 1e9, ms, kernel_bytes, args.steps,
                  args.warmup,
                  {"workload": "C4: N=1024 RLE (EWAH-style) bitmaps, r=2^30 bits, Markov runs (ones mean 256, zeros "
@@ -630,7 +631,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
                                      "note": "per-stream K4 on the original EWAH streams (a query's first evaluation)"},
                   "sliced_layout": {"markers": n_mk, "literal_words": n_lit, "events": n_ev,
                                     "note": "value = EWAH input bytes / kernel time; roofline = bytes K4s moves "
-                                            "(16-bit events + per-tile list table + output)"},
+                                            "(packed 10-bit events + per-tile tables + output)"},
                   "first_eval_s": first_evals_s[0], "second_eval_with_slice_build_s": first_evals_s[1],
                   "e2e": e2e_line,
                   "matches_oracle_window": bool(exact_window),

@@ -72,11 +72,11 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 //    updates of neighbouring markers merged: +1 / -1 where a one-fill starts / ends,
 //    +1 / -1 << 16 where a literal group starts / ends, +1 - (1 << 16) where a
 //    one-fill starts as a literal group ends, -1 + (1 << 16) where a one-fill ends as
-//    a literal group starts.  Events are 16-bit byte offsets (position * 4) into the
-//    difference array, grouped per tile into six lists by kind (all slices of the
-//    tile), each padded to whole warp rows (kEvRow events: 32 lanes x one 16-byte
-//    vector of 8 events) with offsets of dummy slots past the tile.  Inside a list
-//    the events are permuted so that the 32 updates of each shared-memory atomic
+//    a literal group starts.  An event is its 10-bit word position; 16-byte vectors
+//    hold 12 (three per 32-bit word).  Each tile has six lists, one per kind, holding
+//    all slices' events of that kind, each padded to whole warp rows (kEvRow events:
+//    32 lanes x one vector), padding slots skipped by their index.  Inside a list the
+//    events are permuted so that the 32 updates of each shared-memory atomic
 //    instruction (event j of the 32 vectors of a row) fall in distinct banks wherever
 //    the list allows: phase A adds a warp-uniform constant per event, every update
 //    nonzero and bank-conflict free.
@@ -85,22 +85,22 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 //    the tile are [lit_start[p], lit_start[p + 1]) of the tile's literal array, so
 //    phase C reads an undecided word's literals contiguously, with no marker
 //    decoding.
-constexpr int kEvVec = 8;                                      // events per 16-byte vector
-constexpr int kEvRow = 32 * kEvVec;                            // events per warp row
+constexpr int kEvVec = 12;            // events per 16-byte vector (10-bit positions)
+constexpr int kEvRow = 32 * kEvVec;   // events per warp row
 constexpr int kEvKinds = 6;
-constexpr uint16_t kEvDummy = (uint16_t)((kRleTile + 1) * 4);  // byte offset of the first dummy slot (32 follow)
 struct SlicedLayout {
     void *mem = nullptr;
     const uint64_t *literals = nullptr;   // [sum of tile literal counts]
     const uint32_t *lit_start = nullptr;  // [ntiles][kRleTile + 1] offset of each word's literals in its tile
     const uint64_t *tile_lbase = nullptr; // [ntiles + 1] literal offset of each tile
-    const uint16_t *events = nullptr;     // [sum of tile event counts] byte offsets into the difference array
-    const uint64_t *tile_ebase = nullptr; // [ntiles + 1] event offset of each tile (multiple of kEvRow)
-    const uint4 *tile_eends = nullptr;    // [2 ntiles] cumulative ends of the six lists in 16-byte vectors (+ 2 unused)
+    const uint4 *events = nullptr;        // [sum of tile vector counts] 12 packed events per vector
+    const uint64_t *tile_ebase = nullptr; // [ntiles + 1] vector offset of each tile
+    const uint4 *tile_desc = nullptr;     // [3 ntiles] cumulative ends of the six lists in vectors, their real lengths
     const uint32_t *tile_order = nullptr; // [ntiles] tiles by descending reach (max ones + dirty of a word):
                                           // those that can need phase C are scheduled first
     uint64_t bytes = 0;
-    uint64_t n_markers = 0, n_literals = 0, n_events = 0;  // n_markers: slice markers (statistic; not stored)
+    uint64_t n_markers = 0, n_literals = 0;  // n_markers: slice markers (statistic; not stored)
+    uint64_t n_events = 0;                   // event slots, padding included (kEvVec per 16-byte vector)
 };
 // tiles [tile0, tile0 + ntiles) of the streams; directory rows are relative to tile0
 int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t tile0,

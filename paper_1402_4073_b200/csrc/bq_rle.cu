@@ -37,6 +37,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -505,7 +506,10 @@ struct bq_rle_query {
     int evals = 0;
     bool sliced_tried = false;
     SlicedLayout sliced;  // tile-sliced layout (K4s), the default derived layout
-    mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced
+    // device accept / const_until / breakpoint tables by accept vector: immutable once
+    // uploaded, so repeated evaluations (same T) need no allocation or copy
+    std::map<std::vector<uint8_t>, void *> tables;
+    mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced / tables
 };
 
 extern "C" {
@@ -645,6 +649,7 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     if (q->device >= 0) cudaSetDevice(q->device);
     cudaFree(q->mem);
     free_sliced(&q->sliced);
+    for (auto &kv : q->tables) cudaFree(kv.second);
     delete q;
 }
 
@@ -697,14 +702,38 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     if (nbreak > 0) host.insert(host.end(), brk.begin(), brk.end());
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     void *d_tab = nullptr;
+    bool owned = false;  // a table outside the query's cache, freed after this launch
     const size_t bytes = host.size() * 4;
-    cudaError_t e = cudaMallocAsync(&d_tab, bytes, s);
-    if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(accept)");
-    e = cudaMemcpyAsync(d_tab, host.data(), bytes, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) {
-        cudaFreeAsync(d_tab, s);
-        return cuda_error(e, "cudaMemcpyAsync(accept)");
+    cudaError_t e = cudaSuccess;
+    {
+        constexpr size_t kMaxTables = 64;
+        std::lock_guard<std::mutex> guard(q->build_mu);
+        auto it = q->tables.find(acc);
+        if (it != q->tables.end()) {
+            d_tab = it->second;
+        } else if (q->tables.size() < kMaxTables) {
+            e = cudaMalloc(&d_tab, bytes);
+            if (e == cudaSuccess) e = cudaMemcpy(d_tab, host.data(), bytes, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) {
+                if (d_tab) cudaFree(d_tab);
+                return cuda_error(e, "accept table upload");
+            }
+            q->tables.emplace(acc, d_tab);
+        }
     }
+    if (!d_tab) {
+        owned = true;
+        e = cudaMallocAsync(&d_tab, bytes, s);
+        if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(accept)");
+        e = cudaMemcpyAsync(d_tab, host.data(), bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(d_tab, s);
+            return cuda_error(e, "cudaMemcpyAsync(accept)");
+        }
+    }
+    auto release = [&] {
+        if (owned) cudaFreeAsync(d_tab, s);
+    };
     RleCountArgs a;
     a.ptrs = q->d_ptrs;
     a.lens = q->d_lens;
@@ -738,12 +767,12 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
             q->sliced_tried = true;
             e = cudaStreamSynchronize(s);  // the build runs on the legacy stream
             if (e != cudaSuccess) {
-                cudaFreeAsync(d_tab, s);
+                release();
                 return cuda_error(e, "cudaStreamSynchronize");
             }
             rc = build_sliced(q->d_ptrs, q->d_lens, q->d_dir, n, q->tile0, q->ntiles, &q->sliced);
             if (rc) {
-                cudaFreeAsync(d_tab, s);
+                release();
                 return rc;
             }
         }
@@ -764,18 +793,18 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         se.popcnt = d_popcnt;
         se.debug = a.debug;
         rc = launch_sliced(sliced, se, s);
-        cudaFreeAsync(d_tab, s);
+        release();
         return rc;
     } else {
         e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) rle_count_kernel<<<q->ntiles, kStagedThreads, smem, s>>>(a);
     }
     if (e != cudaSuccess) {
-        cudaFreeAsync(d_tab, s);
+        release();
         return cuda_error(e, "cudaFuncSetAttribute(rle_count_kernel)");
     }
     e = cudaGetLastError();
-    cudaFreeAsync(d_tab, s);
+    release();
     if (e != cudaSuccess) return cuda_error(e, "rle_count_kernel launch");
     return BQ_OK;
 }

@@ -82,7 +82,7 @@ __device__ SliceCounts slice_walk(const uint64_t *src, uint64_t L, uint2 e, uint
     SliceCounts n{};
     bool pend = false;  // the previous marker's literal group ends at rel (its -1 << 16 not yet filed)
     auto event = [&](int kind, uint32_t at) {
-        if (EMIT) sink.ev[kind][n.ev[kind]] = (uint16_t)(at * 4u);
+        if (EMIT) sink.ev[kind][n.ev[kind]] = (uint16_t)at;
         ++n.ev[kind];
     };
     auto emit = [&](uint32_t bit, uint32_t run, uint32_t dirty) {
@@ -148,12 +148,11 @@ __global__ void slice_count_kernel(const uint64_t *const *ptrs, const uint64_t *
 
 // One CTA per tile: exclusive scans of the slice counts in place (two 32-bit counts
 // per 64-bit value: each half of a tile's sum stays below 2^32), and the tile totals:
-// markers, literals, the event lists' real lengths, their
-// cumulative ends in 16-byte vectors (each list padded to whole warp rows) and the
-// tile's event total.
+// markers, literals, the tile's list descriptor (cumulative list ends in 16-byte
+// vectors, each list padded to whole warp rows, and the lists' real lengths) and
+// the tile's vector total.
 __global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, ulonglong4 *ecounts, int n, uint64_t *tile_m,
-                                                          uint64_t *tile_l, uint64_t *tile_e, uint4 *eends,
-                                                          uint32_t *ereal) {
+                                                          uint64_t *tile_l, uint64_t *tile_e, uint4 *desc) {
     using Scan = cub::BlockScan<uint64_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ uint64_t carry[4];
@@ -187,22 +186,22 @@ __global__ void __launch_bounds__(1024) slice_scan_kernel(uint64_t *counts, ulon
         const uint64_t m = carry[0] & 0xFFFFFFFFull, l = carry[0] >> 32;
         tile_m[t] = m;
         tile_l[t] = l;
-        uint32_t end[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, acc = 0;
+        uint32_t end[kEvKinds], real[kEvKinds], acc = 0;
         for (int k = 0; k < kEvKinds; ++k) {
-            const uint32_t e = (uint32_t)(carry[1 + k / 2] >> (32 * (k & 1)));
-            ereal[(size_t)t * 8 + k] = e;
-            acc += (e + kEvRow - 1) / kEvRow * (kEvRow / kEvVec);
+            real[k] = (uint32_t)(carry[1 + k / 2] >> (32 * (k & 1)));
+            acc += (real[k] + kEvRow - 1) / kEvRow * 32;
             end[k] = acc;
         }
-        eends[2 * (size_t)t] = make_uint4(end[0], end[1], end[2], end[3]);
-        eends[2 * (size_t)t + 1] = make_uint4(end[4], end[5], acc, 0u);
-        tile_e[t] = (uint64_t)acc * kEvVec;
+        desc[3 * (size_t)t] = make_uint4(end[0], end[1], end[2], end[3]);
+        desc[3 * (size_t)t + 1] = make_uint4(end[4], end[5], real[0], real[1]);
+        desc[3 * (size_t)t + 2] = make_uint4(real[2], real[3], real[4], real[5]);
+        tile_e[t] = acc;
     }
 }
 
 __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *lens, const uint2 *dir, int n,
                                   uint32_t tile0, uint32_t ntiles, const uint64_t *offs, const ulonglong4 *eoffs,
-                                  const uint64_t *lbase, const uint64_t *ebase, const uint4 *eends,
+                                  const uint64_t *lbase, const uint64_t *ebase, const uint4 *desc,
                                   uint64_t *literals, uint16_t *lit_pos, uint16_t *events) {
     const uint64_t total = (uint64_t)ntiles * n;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
@@ -210,11 +209,11 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
         const uint32_t t = (uint32_t)(k / n);
         const uint64_t o = offs[(size_t)t * n + s];
         const ulonglong4 eo = eoffs[(size_t)t * n + s];
-        const uint4 ea = eends[2 * (size_t)t], eb = eends[2 * (size_t)t + 1];
+        const uint4 ea = desc[3 * (size_t)t], eb = desc[3 * (size_t)t + 1];
         const uint32_t starts[kEvKinds] = {0u, ea.x, ea.y, ea.z, ea.w, eb.x};
         const uint32_t within[kEvKinds] = {(uint32_t)eo.x, (uint32_t)(eo.x >> 32), (uint32_t)eo.y,
                                            (uint32_t)(eo.y >> 32), (uint32_t)eo.z, (uint32_t)(eo.z >> 32)};
-        uint16_t *tev = events + ebase[t];
+        uint16_t *tev = events + ebase[t] * kEvVec;  // positions as emitted: one 16-bit slot per event
         SliceSink sink;
         sink.lit = literals + lbase[t] + (uint32_t)(o >> 32);
         sink.pos = lit_pos + lbase[t] + (uint32_t)(o >> 32);
@@ -267,36 +266,38 @@ __global__ void __launch_bounds__(512) sort_literals_kernel(const uint64_t *lit_
 
 // One CTA per (tile, event kind): permute the list (emitted slice by slice) so that
 // each shared-memory atomic instruction of phase A -- event j of the 32 vectors of a
-// warp row -- updates 32 distinct banks.  Events are ranked within their bank (bank =
-// position mod 32), ordered by (rank, bank) -- every round of ranks holds each bank at
-// most once -- and position s of that order goes to list index
-// row * kEvRow + (s mod 32) * kEvVec + (s mod kEvRow) / 32.  Groups of 32 spanning two
-// rounds can repeat a bank once.  Ranks follow list order (deterministic layout).
-// Padding after the real events: the 32 dummy slots in turn.
-__global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src, uint16_t *dst, const uint64_t *ebase,
-                                                             const uint4 *eends, const uint32_t *ereal) {
+// warp row -- updates 32 distinct banks, and pack it.  Events are ranked within their
+// bank (bank = position mod 32), ordered by (rank, bank) -- every round of ranks holds
+// each bank at most once -- and position s of that order becomes event j =
+// (s mod kEvRow) / 32 of vector (s / kEvRow) * 32 + s mod 32 of the list: 10-bit field
+// j mod 3 of 32-bit word j / 3.  Groups of 32 spanning two rounds can repeat a bank
+// once.  Ranks follow list order (deterministic layout).  Slots past the list's real
+// length stay zero; phase A skips them.  dst is zeroed beforehand.
+__global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src, uint32_t *dst, const uint64_t *ebase,
+                                                             const uint4 *desc) {
     const uint32_t t = blockIdx.x, kind = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint4 ea = eends[2 * (size_t)t], eb = eends[2 * (size_t)t + 1];
+    const uint4 ea = desc[3 * (size_t)t], eb = desc[3 * (size_t)t + 1], ec = desc[3 * (size_t)t + 2];
     const uint32_t ends[kEvKinds] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y};
+    const uint32_t reals[kEvKinds] = {eb.z, eb.w, ec.x, ec.y, ec.z, ec.w};
     const uint32_t vstart = kind ? ends[kind - 1] : 0u;
-    const uint32_t npad = (ends[kind] - vstart) * kEvVec;
-    const uint32_t nreal = ereal[(size_t)t * 8 + kind];
-    const uint64_t base = ebase[t] + (uint64_t)vstart * kEvVec;
-    const uint16_t *s = src + base;
-    uint16_t *d = dst + base;
+    const uint32_t nreal = reals[kind];
+    const uint64_t vbase = ebase[t] + vstart;
+    const uint16_t *s = src + vbase * kEvVec;
+    uint32_t *d = dst + vbase * 4;
     __shared__ uint32_t bank_cnt[32], running[32], wcnt[8][32];
     __shared__ uint32_t sorted_cnt[32], sorted_bank[32], prefix[33], sufmask[33];
-    auto place = [&](uint32_t sidx, uint16_t v) {
-        const uint32_t within = sidx % kEvRow;
-        d[sidx - within + (within % 32) * kEvVec + within / 32] = v;
+    auto place = [&](uint32_t sidx, uint32_t pos) {
+        const uint32_t within = sidx % kEvRow, j = within / 32;
+        const uint32_t vec = sidx / kEvRow * 32 + within % 32;
+        atomicOr(d + (size_t)vec * 4 + j / 3, pos << (10 * (j % 3)));
     };
     if (tid < 32) {
         bank_cnt[tid] = 0;
         running[tid] = 0;
     }
     __syncthreads();
-    for (uint32_t i = tid; i < nreal; i += 256) atomicAdd(&bank_cnt[(s[i] >> 2) & 31u], 1u);
+    for (uint32_t i = tid; i < nreal; i += 256) atomicAdd(&bank_cnt[s[i] & 31u], 1u);
     __syncthreads();
     if (tid < 32) {  // banks ordered by (count, bank)
         const uint32_t c = bank_cnt[tid];
@@ -319,8 +320,8 @@ __global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src
     for (uint32_t c0 = 0; c0 < nreal; c0 += 256) {
         const uint32_t i = c0 + tid;
         const bool valid = i < nreal;
-        const uint16_t v = valid ? s[i] : (uint16_t)0;
-        const uint32_t b = (v >> 2) & 31u;
+        const uint32_t v = valid ? s[i] : 0u;
+        const uint32_t b = v & 31u;
         wcnt[warp][lane] = 0;
         __syncwarp();
         const uint32_t peers = __match_any_sync(0xffffffffu, valid ? b : 0xFFFFFFFFu);
@@ -344,45 +345,58 @@ __global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src
         }
         __syncthreads();
     }
-    for (uint32_t i = nreal + tid; i < npad; i += 256) place(i, (uint16_t)(kEvDummy + 4u * (i % 32u)));
 }
-
-// ---------------------------------------------------------------------------
-// K4s: one CTA per tile.
 
 struct SlArgs {
     const uint64_t *literals;
     const uint32_t *lit_start;
     const uint64_t *tile_lbase;
-    const uint16_t *events;
+    const uint4 *events;
     const uint64_t *tile_ebase;
-    const uint4 *tile_eends;
+    const uint4 *tile_desc;
     const uint32_t *tile_order;
     SlicedEval e;
 };
 
-// Two events (16-bit byte offsets into the difference array) of one 32-bit word.
-__device__ __forceinline__ void add_events(uint32_t *cnt, uint32_t w, uint32_t delta) {
-    atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (w & 0xFFFFu)), delta);
-    atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (w >> 16)), delta);
+// The tile's list descriptor (see slice_scan_kernel).
+struct EvDesc {
+    uint4 a, b, c;  // ends: a.x..a.w, b.x, b.y; real lengths: b.z, b.w, c.x..c.w
+};
+
+// Three 10-bit events (word positions) of one 32-bit word: event j of the vector is
+// field j mod 3 of word j / 3; events j with 32 j >= limit are padding.
+template <int J0>
+__device__ __forceinline__ void add_events(uint32_t *cnt, uint32_t w, uint32_t delta, int limit) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+        if ((J0 + f) * 32 < limit) atomicAdd(cnt + ((w >> (10 * f)) & 0x3FFu), delta);
 }
 
-// One 16-byte vector of events: 8 updates by the constant of the vector's list
-// (lists are padded to whole warp rows, so the constant is warp-uniform).
-struct EvEnds {
-    uint4 a, b;  // cumulative list ends in vectors: a.x..a.w, b.x, b.y
-};
-__device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, uint32_t g, const EvEnds &ee) {
-    const uint32_t delta = g < ee.a.x   ? 1u
-                           : g < ee.a.y ? 0xFFFFFFFFu
-                           : g < ee.a.z ? 0x10000u
-                           : g < ee.a.w ? 0xFFFF0000u
-                           : g < ee.b.x ? 0xFFFF0001u
-                                        : 0x0000FFFFu;
-    add_events(cnt, v.x, delta);
-    add_events(cnt, v.y, delta);
-    add_events(cnt, v.z, delta);
-    add_events(cnt, v.w, delta);
+// One 16-byte vector (12 events) at vector g of the tile: every update adds the
+// constant of the vector's list (lists are padded to whole warp rows, so the
+// constant is warp-uniform).  The vector is lane (g - list start) mod 32 of row
+// (g - list start) / 32, so its event j is position 32 j + lane of that row.
+__device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, uint32_t g, const EvDesc &ed) {
+    uint32_t delta, start, real;
+    if (g < ed.a.x) delta = 1u, start = 0u, real = ed.b.z;
+    else if (g < ed.a.y) delta = 0xFFFFFFFFu, start = ed.a.x, real = ed.b.w;
+    else if (g < ed.a.z) delta = 0x10000u, start = ed.a.y, real = ed.c.x;
+    else if (g < ed.a.w) delta = 0xFFFF0000u, start = ed.a.z, real = ed.c.y;
+    else if (g < ed.b.x) delta = 0xFFFF0001u, start = ed.a.w, real = ed.c.z;
+    else delta = 0x0000FFFFu, start = ed.b.x, real = ed.c.w;
+    const uint32_t rel = g - start;
+    const int limit = (int)real - (int)((rel >> 5) * kEvRow + (rel & 31u));
+    if (limit >= kEvRow) {  // every row but a list's last: no padding
+        add_events<0>(cnt, v.x, delta, kEvRow);
+        add_events<3>(cnt, v.y, delta, kEvRow);
+        add_events<6>(cnt, v.z, delta, kEvRow);
+        add_events<9>(cnt, v.w, delta, kEvRow);
+    } else {
+        add_events<0>(cnt, v.x, delta, limit);
+        add_events<3>(cnt, v.y, delta, limit);
+        add_events<6>(cnt, v.z, delta, limit);
+        add_events<9>(cnt, v.w, delta, limit);
+    }
 }
 
 // Bit-sliced sum (planes 0..M-1 of the 64 per-bit counts) of n contiguous literal
@@ -434,9 +448,9 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     const uint32_t nlit = (uint32_t)(a.tile_lbase[tile + 1] - lbase);
     const uint64_t *tlit = a.literals + lbase;
     const uint32_t *tls = a.lit_start + (size_t)tile * kLitStarts;
-    const EvEnds ee{a.tile_eends[2 * tile], a.tile_eends[2 * tile + 1]};
-    const uint32_t nvec = ee.b.z;
-    const uint4 *tev = reinterpret_cast<const uint4 *>(a.events + a.tile_ebase[tile]);
+    const EvDesc ee{a.tile_desc[3 * tile], a.tile_desc[3 * tile + 1], a.tile_desc[3 * tile + 2]};
+    const uint32_t nvec = ee.b.y;
+    const uint4 *tev = a.events + a.tile_ebase[tile];
     const uint32_t npieces = (nvec + kPieceVecs - 1) / kPieceVecs;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
 
@@ -585,7 +599,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
                                                   (int64_t)T1);
     if (e != cudaSuccess) return cuda_error(e, "DeviceScan sizing");
-    const size_t scratch_bytes = cells * 40 + 6 * T1 * 8 + 16 + T1 * 32 + T1 * 32 + tmp_bytes + 256;
+    const size_t scratch_bytes = cells * 40 + 6 * T1 * 8 + 16 + T1 * 48 + tmp_bytes + 256;
     char *scratch = nullptr;
     e = cudaMalloc(&scratch, scratch_bytes);
     if (e != cudaSuccess) {
@@ -595,9 +609,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     ulonglong4 *ecounts = reinterpret_cast<ulonglong4 *>(scratch);
     uint64_t *counts = reinterpret_cast<uint64_t *>(ecounts + cells);
     uint64_t *tm = counts + cells, *tl = tm + T1, *te = tl + T1, *mb = te + T1, *lb = mb + T1, *eb = lb + T1;
-    uint4 *eends = reinterpret_cast<uint4 *>(scratch + ((reinterpret_cast<char *>(eb + T1) - scratch) + 15) / 16 * 16);
-    uint32_t *ereal = reinterpret_cast<uint32_t *>(eends + 2 * T1);
-    void *d_tmp = ereal + 8 * T1;
+    uint4 *desc = reinterpret_cast<uint4 *>(scratch + ((reinterpret_cast<char *>(eb + T1) - scratch) + 15) / 16 * 16);
+    void *d_tmp = desc + 3 * T1;
     const int sms = sm_count();
     const unsigned grid = (unsigned)std::min<uint64_t>((cells + 255) / 256, (uint64_t)sms * 32);
     char *evsrc = nullptr;
@@ -612,7 +625,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     if (e == cudaSuccess) e = cudaMemset(tl + ntiles, 0, 8);
     if (e == cudaSuccess) e = cudaMemset(te + ntiles, 0, 8);
     if (e != cudaSuccess) return fail(e, "slice_count_kernel");
-    slice_scan_kernel<<<ntiles, 1024>>>(counts, ecounts, n, tm, tl, te, eends, ereal);
+    slice_scan_kernel<<<ntiles, 1024>>>(counts, ecounts, n, tm, tl, te, desc);
     e = cudaGetLastError();
     tmp2 = tmp_bytes;
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, tm, mb, (int64_t)T1);
@@ -620,24 +633,24 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, tl, lb, (int64_t)T1);
     tmp2 = tmp_bytes;
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp2, te, eb, (int64_t)T1);
-    uint64_t nm = 0, nl = 0, ne = 0;
+    uint64_t nm = 0, nl = 0, ne = 0;  // ne: event vectors
     if (e == cudaSuccess) e = cudaMemcpy(&nm, mb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(&nl, lb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(&ne, eb + ntiles, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(e, "slice scans");
-    // literals | tile_lbase | lit_start | events | tile_ebase | tile_eends | tile_order
-    // (literals, events and tile_eends at 16-byte boundaries)
+    // literals | tile_lbase | lit_start | events | tile_ebase | tile_desc | tile_order
+    // (literals, events and tile_desc at 16-byte boundaries)
     auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
     const size_t o_tlb = nl * 8;
     const size_t o_ls = o_tlb + T1 * 8;
     const size_t o_ev = r16(o_ls + (size_t)ntiles * kLitStarts * 4);
-    const size_t o_teb = o_ev + ne * 2;  // ne is a multiple of kEvRow: 16-byte multiple
+    const size_t o_teb = o_ev + ne * 16;
     const size_t o_tee = r16(o_teb + T1 * 8);
-    const size_t o_ord = o_tee + (size_t)ntiles * 32;
+    const size_t o_ord = o_tee + (size_t)ntiles * 48;
     const size_t bytes = o_ord + (size_t)ntiles * 4;
     char *m = nullptr, *tmpl = nullptr;  // tmpl: literals and positions as emitted, slice by slice
     e = cudaMalloc(&m, bytes);
-    if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * 2);  // events as emitted, slice by slice
+    if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * kEvVec * 2);  // event positions as emitted, slice by slice
     if (e == cudaSuccess) e = cudaMalloc(&tmpl, nl * 10 + 16);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -651,14 +664,15 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     uint64_t *literals = reinterpret_cast<uint64_t *>(m);
     uint64_t *tlb = reinterpret_cast<uint64_t *>(m + o_tlb);
     uint32_t *lit_start = reinterpret_cast<uint32_t *>(m + o_ls);
-    uint16_t *events = reinterpret_cast<uint16_t *>(m + o_ev);
+    uint4 *events = reinterpret_cast<uint4 *>(m + o_ev);
     uint64_t *teb = reinterpret_cast<uint64_t *>(m + o_teb);
     uint4 *tee = reinterpret_cast<uint4 *>(m + o_tee);
     uint64_t *lit_src = reinterpret_cast<uint64_t *>(tmpl);
     uint16_t *pos_src = reinterpret_cast<uint16_t *>(tmpl + nl * 8);
     e = cudaMemcpy(tlb, lb, T1 * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(teb, eb, T1 * 8, cudaMemcpyDeviceToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(tee, eends, (size_t)ntiles * 32, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(tee, desc, (size_t)ntiles * 48, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemset(events, 0, ne * 16);  // packed by atomicOr
     if (e == cudaSuccess) {
         slice_emit_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts, tlb, teb, tee,
                                          lit_src, pos_src, reinterpret_cast<uint16_t *>(evsrc));
@@ -669,8 +683,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         e = cudaGetLastError();
     }
     if (e == cudaSuccess && ne) {
-        arrange_events_kernel<<<dim3(ntiles, kEvKinds), 256>>>(reinterpret_cast<const uint16_t *>(evsrc), events, teb,
-                                                              tee, ereal);
+        arrange_events_kernel<<<dim3(ntiles, kEvKinds), 256>>>(reinterpret_cast<const uint16_t *>(evsrc),
+                                                              reinterpret_cast<uint32_t *>(events), teb, tee);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -701,7 +715,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         tmp.tile_lbase = tlb;
         tmp.events = events;
         tmp.tile_ebase = teb;
-        tmp.tile_eends = tee;
+        tmp.tile_desc = tee;
         SlicedEval re{};
         re.n = n;
         re.total_words = ~0ull;
@@ -731,11 +745,11 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     l.tile_lbase = tlb;
     l.events = events;
     l.tile_ebase = teb;
-    l.tile_eends = tee;
+    l.tile_desc = tee;
     l.bytes = bytes;
     l.n_markers = nm;
     l.n_literals = nl;
-    l.n_events = ne;
+    l.n_events = ne * kEvVec;
     *out = l;
     return BQ_OK;
 }
@@ -752,7 +766,7 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
     a.tile_lbase = l.tile_lbase;
     a.events = l.events;
     a.tile_ebase = l.tile_ebase;
-    a.tile_eends = l.tile_eends;
+    a.tile_desc = l.tile_desc;
     a.tile_order = e.reach_out ? nullptr : l.tile_order;
     a.e = e;
     cudaError_t err = cudaFuncSetAttribute(rle_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlSmem);
