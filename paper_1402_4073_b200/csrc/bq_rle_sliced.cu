@@ -372,11 +372,11 @@ __device__ __forceinline__ void add_events(uint32_t *cnt, uint32_t w, uint32_t d
         if ((J0 + f) * 32 < limit) atomicAdd(cnt + ((w >> (10 * f)) & 0x3FFu), delta);
 }
 
-// One 16-byte vector (12 events) at vector g of the tile: every update adds the
-// constant of the vector's list (lists are padded to whole warp rows, so the
-// constant is warp-uniform).  The vector is lane (g - list start) mod 32 of row
-// (g - list start) / 32, so its event j is position 32 j + lane of that row.
-__device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, uint32_t g, const EvDesc &ed) {
+// Row descriptor of the warp row starting at vector g of the tile: the constant of
+// its list and the real events left in the list from the row's start (lists are
+// padded to whole rows, so every row lies in one list).  Vector lane of the row holds
+// the row's events 32 j + lane, j < 12.
+__device__ __forceinline__ uint2 row_desc(uint32_t g, const EvDesc &ed) {
     uint32_t delta, start, real;
     if (g < ed.a.x) delta = 1u, start = 0u, real = ed.b.z;
     else if (g < ed.a.y) delta = 0xFFFFFFFFu, start = ed.a.x, real = ed.b.w;
@@ -384,18 +384,22 @@ __device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, uint32_
     else if (g < ed.a.w) delta = 0xFFFF0000u, start = ed.a.z, real = ed.c.y;
     else if (g < ed.b.x) delta = 0xFFFF0001u, start = ed.a.w, real = ed.c.z;
     else delta = 0x0000FFFFu, start = ed.b.x, real = ed.c.w;
-    const uint32_t rel = g - start;
-    const int limit = (int)real - (int)((rel >> 5) * kEvRow + (rel & 31u));
+    return make_uint2(delta, real - (g - start) / 32 * kEvRow);
+}
+
+// One 16-byte vector (12 events) of a row with descriptor rd, at lane `lane`.
+__device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, const uint2 rd, int lane) {
+    const int limit = (int)rd.y - lane;
     if (limit >= kEvRow) {  // every row but a list's last: no padding
-        add_events<0>(cnt, v.x, delta, kEvRow);
-        add_events<3>(cnt, v.y, delta, kEvRow);
-        add_events<6>(cnt, v.z, delta, kEvRow);
-        add_events<9>(cnt, v.w, delta, kEvRow);
+        add_events<0>(cnt, v.x, rd.x, kEvRow);
+        add_events<3>(cnt, v.y, rd.x, kEvRow);
+        add_events<6>(cnt, v.z, rd.x, kEvRow);
+        add_events<9>(cnt, v.w, rd.x, kEvRow);
     } else {
-        add_events<0>(cnt, v.x, delta, limit);
-        add_events<3>(cnt, v.y, delta, limit);
-        add_events<6>(cnt, v.z, delta, limit);
-        add_events<9>(cnt, v.w, delta, limit);
+        add_events<0>(cnt, v.x, rd.x, limit);
+        add_events<3>(cnt, v.y, rd.x, limit);
+        add_events<6>(cnt, v.z, rd.x, limit);
+        add_events<9>(cnt, v.w, rd.x, limit);
     }
 }
 
@@ -437,6 +441,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     uint8_t *region = sl_smem + kSlCntBytes + 16;
     uint4 *buf = reinterpret_cast<uint4 *>(region);  // [2][kPieceVecs]
     __shared__ uint32_t n_undecided, n_heavy;
+    __shared__ uint2 rowtab[2][kPieceVecs / 32];  // row descriptors of the staged pieces
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
@@ -467,6 +472,11 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
                      : "memory");
     };
 
+    auto fill_rows = [&](uint32_t p) {  // threads < rows per piece: descriptors of piece p's rows
+        const uint32_t g = p * kPieceVecs + tid * 32;
+        if (tid < kPieceVecs / 32 && g < nvec) rowtab[p & 1][tid] = row_desc(g, ee);
+    };
+    fill_rows(0);
     for (int k = tid; k < kRleTile + 36; k += NT) cnt[k] = 0u;
     if (tid == 0) {
         n_undecided = 0;
@@ -496,14 +506,16 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
         const uint4 *pb = buf + (size_t)(p & 1) * kPieceVecs;
         const uint32_t g0 = p * kPieceVecs;
         if (!E.debug) {
+            const uint2 *rt = rowtab[p & 1];
             uint32_t i = tid;
             for (; i + NT < nv; i += 2 * NT) {  // two vectors per iteration: both shared loads ahead of the updates
                 const uint4 v0 = pb[i], v1 = pb[i + NT];
-                add_vector(cnt, v0, g0 + i, ee);
-                add_vector(cnt, v1, g0 + i + NT, ee);
+                add_vector(cnt, v0, rt[i >> 5], lane);
+                add_vector(cnt, v1, rt[(i + NT) >> 5], lane);
             }
-            if (i < nv) add_vector(cnt, pb[i], g0 + i, ee);
+            if (i < nv) add_vector(cnt, pb[i], rt[i >> 5], lane);
         }
+        fill_rows(p + 1);  // into the other table: piece p - 1's, free since the last barrier
         __syncthreads();  // buf[p & 1] is free
         if (tid == 0 && p + 2 < npieces) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
