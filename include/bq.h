@@ -153,19 +153,22 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q);
 /* Output words of one evaluation (w_end - w_begin). */
 BQ_API uint64_t bq_rle_query_out_words(const bq_rle_query *q);
 /* Device bytes the query owns: the directory plus, once built, the tile-sliced
- * layout (every 1024-word slice of every stream re-encoded as 32-bit markers
- * covering exactly that slice, literal words apart, tile-major; K4s decodes it
- * with warp prefix sums).  The layout is built at the second evaluation of a
- * query (BQ_RLE_SLICED: 0 never, 1 at the first evaluation). */
+ * layout (every 1024-word slice of every stream re-encoded as what K4s reads:
+ * the nonzero updates its markers make to the tile's difference array, as packed
+ * 10-bit positions in six per-tile lists by update kind, and its literal words,
+ * position-major per tile; see SlicedLayout in csrc/bq_internal.h).  The layout is
+ * built at the second evaluation of a query (BQ_RLE_SLICED: 0 never, 1 at the
+ * first evaluation). */
 BQ_API uint64_t bq_rle_query_directory_bytes(const bq_rle_query *q);
-/* Size of the tile-sliced layout once built (0, 0 before): 32-bit markers and
- * 64-bit literal words.  K4s reads every marker once per evaluation and
- * literals only at undecided words (bench.py's roofline uses these). */
+/* Size of the tile-sliced layout once built (0, 0 before): markers of the
+ * re-encoded slices (a statistic; they are not stored) and 64-bit literal words.
+ * K4s reads literals only at undecided words. */
 BQ_API int bq_rle_query_layout_stats(const bq_rle_query *q, uint64_t *n_markers, uint64_t *n_literals);
 
-/* Difference-array events of the tile-sliced layout once built (0 before):
- * 16-bit entries, padded per tile and kind; phase A of K4s reads each once per
- * evaluation instead of the markers (markers are read only where phase C runs). */
+/* Difference-array event slots of the tile-sliced layout once built (0 before):
+ * 10-bit entries, 12 per 16-byte vector, padded per tile and kind to whole warp
+ * rows; phase A of K4s reads every vector once per evaluation (bench.py's
+ * roofline counts n_events / 12 * 16 bytes). */
 BQ_API int bq_rle_query_layout_events(const bq_rle_query *q, uint64_t *n_events);
 
 /* Threshold / symmetric function over the compressed inputs, output
