@@ -230,6 +230,26 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU side
 
+def _dist_setup(torch, dist):
+    """One process per GPU: (rank, world, device index).  The collective backend is
+    NCCL.  Functional checks of the multi-rank flow on a one-GPU box may set
+    BQ_BENCH_BACKEND=gloo and BQ_BENCH_SHARE_GPU=1 (ranks then share device
+    LOCAL_RANK mod device_count; their numbers are not measurements)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BQ_BENCH_SHARE_GPU") == "1":
+        local %= torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world > 1:
+        backend = os.environ.get("BQ_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -237,12 +257,7 @@ def run_ours(args):
     import paper_1402_4073_b200 as bq
     from paper_1402_4073_b200 import _lib
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = _dist_setup(torch, dist)
     lib = _lib.load()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -713,12 +728,7 @@ def run_extra(args):
     import paper_1402_4073_b200 as bq
     from paper_1402_4073_b200 import _lib
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = _dist_setup(torch, dist)
     lib = _lib.load()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()

@@ -51,3 +51,32 @@ def test_c4_line_contract():
     assert {"metric", "value", "roofline", "cpu_baseline", "gpu_launches", "clocks"} <= set(d)
     assert d["matches_oracle_window"] and d["popcount"] > 0
     assert d["sliced_layout"]["markers"] > 0 and d["direct_ewah_k4"]["mean_launch_ms"] > 0
+
+
+@pytest.mark.parametrize("workload", ["c2", "c4"])
+def test_two_ranks_under_torchrun(workload):
+    """The multi-rank flow (word-range shards, popcount all-reduce, max-over-ranks
+    timing, rank 0 prints) with two ranks sharing the one GPU over gloo; a
+    functional check of the N > 1 path, not a measurement."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--workload", workload, "--gpus",
+           "2", "--steps", "3", "--warmup", "3", "--e2e-steps", "1"]
+    env = dict(os.environ, BQ_BENCH_BACKEND="gloo", BQ_BENCH_SHARE_GPU="1", OMP_NUM_THREADS="2")
+    p = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "clocks" in d
+    if workload == "c2":
+        assert d["e2e"]["matches_device_result"]
+    else:
+        assert d["matches_oracle_window"] and d["popcount"] > 0
