@@ -46,11 +46,11 @@ constexpr int kSlNT = BQ_SL_NT;                            // K4s threads per CT
 constexpr int kPieceVecs = BQ_SL_PIECE;                    // event vectors per staged piece (10 KB; 8 CTAs per SM)
 constexpr uint32_t kThreadWordMax = 128;                   // phase C: words with more literals get a warp
 constexpr int kLitStarts = kRleTile + 1;                   // literal offsets per tile (position-major)
-constexpr size_t kSlCntBytes = (size_t)(kRleTile + 36) * 4;  // + sentinel + 32 per-lane dummies (+ pad)
+constexpr int kSlCntWords = kRleTile + 4;                  // difference array + sentinel (+ pad)
 constexpr size_t kSlBufBytes = 2 * (size_t)kPieceVecs * 16;
 constexpr size_t kSlPhaseC = (size_t)kRleTile * 4;  // undecided and heavy word lists
 constexpr size_t kSlRegion = kSlBufBytes > kSlPhaseC ? kSlBufBytes : kSlPhaseC;
-constexpr size_t kSlSmem = kSlCntBytes + 16 + kSlRegion;  // cnt | 2 mbarriers | region
+constexpr size_t kSlSmem = 16 + kSlRegion;  // 2 mbarriers | region (dynamic; the difference array is static)
 
 // ---------------------------------------------------------------------------
 // Layout build, one thread per (tile, stream) slice.  The counting pass maps
@@ -403,19 +403,41 @@ __device__ __forceinline__ void add_vector(uint32_t *cnt, const uint4 v, const u
     }
 }
 
-// Bit-sliced sum (planes 0..M-1 of the 64 per-bit counts) of n contiguous literal
-// words, four loads in flight.
+__device__ __forceinline__ void full_add(uint64_t a, uint64_t b, uint64_t c, uint64_t &s, uint64_t &cy) {
+    s = a ^ b ^ c;                    // LOP3 0x96
+    cy = (a & b) | (c & (a ^ b));     // LOP3 0xE8
+}
+
+// Bit-sliced sum (planes 0..M-1 of the 64 per-bit counts, M >= 3) of n contiguous
+// literal words: full groups of 7 loaded at once and reduced by a 4-adder carry-save
+// tree to a 3-bit bit-sliced number, which is then added into the planes; the last
+// words rippled in one at a time.
 template <int M>
 __device__ __forceinline__ void planes_sum_contig(const uint64_t *p, uint32_t n, uint64_t (&c)[16]) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) c[j] = 0ull;
     uint32_t i = 0;
-    for (; i + 4 <= n; i += 4) {
-        uint64_t x[4];
+    for (; i + 7 <= n; i += 7) {
+        uint64_t x[7];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = __ldg(p + i + k);
+        for (int k = 0; k < 7; ++k) x[k] = __ldg(p + i + k);
+        uint64_t a0, a1, b0, b1, s1, c1, s2, s4, cy, t;
+        full_add(x[0], x[1], x[2], a0, a1);
+        full_add(x[3], x[4], x[5], b0, b1);
+        full_add(a0, b0, x[6], s1, c1);
+        full_add(a1, b1, c1, s2, s4);
+        cy = c[0] & s1;
+        c[0] ^= s1;
+        full_add(c[1], s2, cy, t, cy);
+        c[1] = t;
+        full_add(c[2], s4, cy, t, cy);
+        c[2] = t;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ripple<M>(c, x[k]);
+        for (int j = 3; j < M; ++j) {
+            t = c[j] & cy;
+            c[j] ^= cy;
+            cy = t;
+        }
     }
     for (; i < n; ++i) ripple<M>(c, __ldg(p + i));
 }
@@ -436,9 +458,10 @@ __device__ __forceinline__ void sl_finish(unsigned long long pc, int lane, unsig
 __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __grid_constant__ SlArgs a) {
     constexpr int NT = kSlNT;
     extern __shared__ __align__(128) uint8_t sl_smem[];
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(sl_smem);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sl_smem + kSlCntBytes);
-    uint8_t *region = sl_smem + kSlCntBytes + 16;
+    // static: its address is a constant, so every update is ATOMS [offset + imm]
+    __shared__ __align__(16) uint32_t cnt[kSlCntWords];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sl_smem);
+    uint8_t *region = sl_smem + 16;
     uint4 *buf = reinterpret_cast<uint4 *>(region);  // [2][kPieceVecs]
     __shared__ uint32_t n_undecided, n_heavy;
     __shared__ uint2 rowtab[2][kPieceVecs / 32];  // row descriptors of the staged pieces
@@ -477,7 +500,7 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
         if (tid < kPieceVecs / 32 && g < nvec) rowtab[p & 1][tid] = row_desc(g, ee);
     };
     fill_rows(0);
-    for (int k = tid; k < kRleTile + 36; k += NT) cnt[k] = 0u;
+    for (int k = tid; k < kSlCntWords; k += NT) cnt[k] = 0u;
     if (tid == 0) {
         n_undecided = 0;
         n_heavy = 0;
@@ -566,9 +589,13 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
         }
         const uint64_t *lits = tlit + __ldg(tls + p);
         uint64_t planes[16];
-        if (dirty < 16) planes_sum_contig<4>(lits, dirty, planes);
-        else planes_sum_contig<7>(lits, dirty, planes);
-        pc += sl_store(d, p, decide_word(d, ones, dirty, planes));
+        if (dirty < 16) {
+            planes_sum_contig<4>(lits, dirty, planes);
+            pc += sl_store(d, p, decide_word<4>(d, ones, dirty, planes));
+        } else {
+            planes_sum_contig<7>(lits, dirty, planes);
+            pc += sl_store(d, p, decide_word<7>(d, ones, dirty, planes));
+        }
     }
     __syncthreads();
     for (uint32_t h = warp; h < n_heavy; h += NT / 32) {

@@ -136,12 +136,14 @@ __device__ __forceinline__ void planes_sum(const uint64_t *addrs, uint32_t n, ui
     for (; i < n; ++i) ripple<M>(c, __ldg(reinterpret_cast<const uint64_t *>(addrs[i])));
 }
 
-// count >= k per bit position, for the bit-sliced count c (planes 0..15), k a runtime value
+// count >= k per bit position, for the bit-sliced count c (planes 0..M-1 in use, the
+// rest zero), k a runtime value
+template <int M = 16>
 __device__ __forceinline__ uint64_t planes_ge(const uint64_t (&c)[16], uint32_t k) {
-    if (k >= (1u << 16)) return 0ull;
+    if (k >= (1u << M)) return 0ull;
     uint64_t gt = 0ull, eq = ~0ull;
 #pragma unroll
-    for (int j = 15; j >= 0; --j) {
+    for (int j = M - 1; j >= 0; --j) {
         const uint64_t kb = 0ull - (uint64_t)((k >> j) & 1u);
         gt |= eq & c[j] & ~kb;
         eq &= ~(c[j] ^ kb);
@@ -149,7 +151,9 @@ __device__ __forceinline__ uint64_t planes_ge(const uint64_t (&c)[16], uint32_t 
     return gt | eq;
 }
 
-// Result word of an undecided position: accept[ones + count_b] for each bit b.
+// Result word of an undecided position: accept[ones + count_b] for each bit b
+// (counts in planes 0..M-1).
+template <int M = 16>
 __device__ __forceinline__ uint64_t decide_word(const TileDecide &d, uint32_t ones, uint32_t dirty,
                                                 const uint64_t (&c)[16]) {
     if (d.nbreak >= 0) {  // accept(ones + k) = accept(ones) ^ sum over breakpoints b in (ones, ones + dirty] of [k >= b - ones]
@@ -158,7 +162,7 @@ __device__ __forceinline__ uint64_t decide_word(const TileDecide &d, uint32_t on
             const uint32_t b = __ldg(d.breaks + i);
             if (b <= ones) continue;
             if (b > ones + dirty) break;
-            w ^= planes_ge(c, b - ones);
+            w ^= planes_ge<M>(c, b - ones);
         }
         return w;
     }
@@ -166,7 +170,7 @@ __device__ __forceinline__ uint64_t decide_word(const TileDecide &d, uint32_t on
     for (int bit = 0; bit < 64; ++bit) {
         uint32_t cb = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) cb |= (uint32_t)((c[j] >> bit) & 1u) << j;
+        for (int j = 0; j < M; ++j) cb |= (uint32_t)((c[j] >> bit) & 1u) << j;
         if (accept_at(d.accept_bits, ones + cb)) w |= 1ull << bit;
     }
     return w;
