@@ -593,7 +593,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
     if not args.no_e2e and ctx.world == 1:
         host_out = torch.empty(max(q.out_words, 1), dtype=torch.int64, pin_memory=True)
         e2e_s = []
-        for _ in range(4):
+        for _ in range(8):
             torch.cuda.synchronize()
             t_e = time.perf_counter()
             d2 = flat.to(dev, non_blocking=True)
