@@ -83,21 +83,62 @@ __device__ __forceinline__ void rle_fail(const RleDirArgs &a, int code, int stre
 // start, so window loads do not wait for the marker chain: the next window is
 // loaded while the current one is decoded (a dirty group reaching past the next
 // window jumps straight to the window of the next marker, skipping literals
-// unread).  Inside a window the markers reachable from the entry marker are found
-// by pointer doubling (each lane's successor j + 1 + dirty, squared five times,
-// with a warp OR-reduction per level), their word positions by a warp prefix sum.
-constexpr int kDirAhead = 6;  // windows in flight ahead of the one being decoded
-constexpr int kDirRing = 8;   // ring slots per warp (> kDirAhead: consumed slots are reused late)
+// unread).  Inside a window, the markers on the chain from every possible entry
+// are found at once by pointer jumping; following the chain is a lookup per
+// window; marker word positions come from a warp prefix sum in K3b.
+constexpr int kDirAhead = 14;  // windows in flight ahead of the one being decoded
+constexpr int kDirRing = 16;  // ring slots per warp (> kDirAhead: consumed slots are reused late)
+#ifndef BQ_CHAIN_GROUP
+#define BQ_CHAIN_GROUP 4
+#endif
+constexpr int kChainGroup = BQ_CHAIN_GROUP;  // K3a: windows whose chain tables are computed together
 
 // K3a: the sequential part of the directory -- one warp per stream follows its
 // marker chain window by window (windows copied into a per-warp ring by per-lane
 // cp.async, kDirAhead ahead; a literal group reaching past the ring restarts it
-// at the next marker, so long dirty runs are skipped unread).  Inside a window
-// the markers reachable from the entry marker come from pointer doubling (each
-// lane's successor j + 1 + dirty, squared five times, one warp OR-reduction per
-// level), and only two facts per window are kept: its marker mask and the word
-// position where its first marker's fill starts.  Everything else -- marker
-// positions, validation, directory rows -- is K3b, in parallel over all windows.
+// at the next marker, so long dirty runs are skipped unread).  The chain's
+// dependency from window to window is kept short: for every window the warp
+// first computes, for all 32 possible entry lanes at once, where the chain from
+// that entry leaves the window, which markers it passes and the words they cover
+// (pointer jumping: five levels, each combining a lane's aggregate with the one at
+// its successor), which does not depend on the actual entry; several windows'
+// tables are computed interleaved (kChainGroup windows).  Following the chain is then a lookup (a
+// shuffle from the entry lane) per window.  Only two facts per window are kept:
+// its marker mask and the word position where its first marker's fill starts.
+// Everything else -- marker positions, validation, directory rows -- is K3b, in
+// parallel over all windows.
+struct ChainTable {
+    uint32_t m;   // markers on the chain from this lane, within the window
+    uint32_t nx;  // where the chain leaves: window-relative index of its next marker (>= 32, or a lane past L)
+};
+
+// This lane's entry of a window's chain table (word w at index bc + lane, valid:
+// bc + lane < L).
+__device__ __forceinline__ ChainTable chain_table(uint64_t w, bool valid, int lane) {
+    ChainTable t;
+    t.m = valid ? 1u << lane : 0u;
+    t.nx = valid ? (uint32_t)lane + 1u + (uint32_t)(w >> 33) : (uint32_t)lane;  // dirty < 2^31
+    return t;
+}
+
+__device__ __forceinline__ void chain_jump(ChainTable &t, int lane) {
+    const bool on = t.nx < 32u;
+    const int src = on ? (int)t.nx : lane;
+    const uint32_t m = __shfl_sync(0xffffffffu, t.m, src);
+    const uint32_t nx = __shfl_sync(0xffffffffu, t.nx, src);
+    t.m |= on ? m : 0u;
+    t.nx = on ? nx : t.nx;
+}
+
+// Words covered by the fills and literal groups of the window's markers in `reach`
+// (each span < 2^40: the two 24-bit-split sums stay exact).
+__device__ __forceinline__ uint64_t chain_span(uint64_t w, uint32_t reach, int lane) {
+    const uint64_t span = ((reach >> lane) & 1u) ? ((w >> 1) & 0xFFFFFFFFull) + (w >> 33) : 0ull;
+    const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)(span & 0xFFFFFFu));
+    const uint32_t hi = __reduce_add_sync(0xffffffffu, (uint32_t)(span >> 24));
+    return ((uint64_t)hi << 24) + lo;
+}
+
 __global__ void __launch_bounds__(128) rle_chain_kernel(const __grid_constant__ RleDirArgs a, const uint64_t *wbase,
                                                         uint32_t *wreach, uint64_t *wpos) {
     __shared__ uint64_t ring_all[4][kDirRing][32];
@@ -117,45 +158,49 @@ __global__ void __launch_bounds__(128) rle_chain_kernel(const __grid_constant__ 
                      : "memory");
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    uint64_t k = 0;     // window being decoded
+    constexpr int G = kChainGroup;  // windows whose tables are computed per iteration
+    uint64_t k = 0;     // first window of the group being decoded
     uint64_t next = 0;  // stream index of the next marker
     uint64_t pos = 0;   // word position where its fill run starts
     for (int q = 0; q < kDirAhead; ++q) issue(q);
     while (next < L) {
         const uint64_t kk = next / 32;
-        if (kk >= k + kDirAhead) {  // a long literal group: restart the pipeline at the next marker
+        if (kk + G - 1 >= k + kDirAhead) {  // a long literal group: restart the pipeline at the next marker
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
             k = kk;
             for (int q = 0; q < kDirAhead; ++q) issue(k + q);
         } else {
             for (; k < kk; ++k) issue(k + kDirAhead);  // windows of literals only
         }
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDirAhead - 1) : "memory");
-        const uint64_t w = ring[k % kDirRing][lane];
-        const uint64_t bc = k * 32;
-        const uint64_t dirty = w >> 33;
-        uint32_t j = dirty < 32 ? min((uint32_t)lane + 1 + (uint32_t)dirty, 32u) : 32u;
-        uint32_t reach = 1u << (uint32_t)(next - bc);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDirAhead - G) : "memory");
+        // tables of windows k .. k + G - 1 (independent of the entry; interleaved)
+        const uint64_t bc0 = k * 32;
+        uint64_t w[G];
+        ChainTable t[G];
 #pragma unroll
-        for (int level = 0; level < 5; ++level) {
-            const bool in = ((reach >> lane) & 1u) && j < 32u;
-            reach |= __reduce_or_sync(0xffffffffu, in ? (1u << j) : 0u);
-            if (level < 4) {
-                const uint32_t jj = __shfl_sync(0xffffffffu, j, j < 32u ? (int)j : lane);
-                j = j < 32u ? jj : 32u;
+        for (int g = 0; g < G; ++g) {
+            w[g] = ring[(k + g) % kDirRing][lane];
+            t[g] = chain_table(w[g], bc0 + 32 * g + lane < L, lane);
+        }
+#pragma unroll
+        for (int level = 0; level < 5; ++level)
+#pragma unroll
+            for (int g = 0; g < G; ++g) chain_jump(t[g], lane);
+        // follow the chain through the group while it enters the next window
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const uint64_t bc = bc0 + 32 * g;
+            if (g > 0 && !(next < bc + 32 && next < L)) break;  // g == 0 holds the entry; later ones have next >= bc
+            const int e = (int)(next - bc);
+            const uint32_t reach = __shfl_sync(0xffffffffu, t[g].m, e);
+            const uint32_t nx = __shfl_sync(0xffffffffu, t[g].nx, e);
+            if (lane == 0) {
+                wreach[wb + k + g] = reach;
+                wpos[wb + k + g] = pos;
             }
+            pos += chain_span(w[g], reach, lane);
+            next = bc + nx;
         }
-        reach &= (L - bc >= 32) ? 0xffffffffu : ((1u << (uint32_t)(L - bc)) - 1u);
-        next = __shfl_sync(0xffffffffu, bc + lane + 1 + dirty, 31 - __clz(reach));
-        // words covered by the window's markers (each span < 2^40: split sums stay exact)
-        const uint64_t span = ((reach >> lane) & 1u) ? ((w >> 1) & 0xFFFFFFFFull) + dirty : 0ull;
-        const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)(span & 0xFFFFFFu));
-        const uint32_t hi = __reduce_add_sync(0xffffffffu, (uint32_t)(span >> 24));
-        if (lane == 0) {
-            wreach[wb + k] = reach;
-            wpos[wb + k] = pos;
-        }
-        pos += ((uint64_t)hi << 24) + lo;
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // tiles past the encoded coverage: stream exhausted, implicit zero tail
