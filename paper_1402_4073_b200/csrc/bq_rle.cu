@@ -222,12 +222,25 @@ __global__ void __launch_bounds__(128) rle_dirfill_kernel(const __grid_constant_
     uint2 *dir = a.dir + stream;
     const uint64_t nwin = (L + 31) / 32, wb = wbase[stream];
     const uint64_t r0 = (uint64_t)a.tile0 * kRleTile, r1 = (uint64_t)(a.tile0 + a.nrows) * kRleTile;
-    for (uint64_t k = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5); k < nwin; k += (uint64_t)gridDim.x * 4) {
-        const uint32_t reach = wreach[wb + k];
+    const uint64_t stride = (uint64_t)gridDim.x * 4;
+    uint64_t k = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    // the next window's mask, position and words are loaded one window ahead
+    auto load = [&](uint64_t q, uint32_t &r, uint64_t &p, uint64_t &w) {
+        if (q < nwin) {
+            r = wreach[wb + q];
+            p = wpos[wb + q];
+            w = q * 32 + lane < L ? __ldg(s + q * 32 + lane) : 0ull;
+        }
+    };
+    uint32_t r_n = 0;
+    uint64_t p_n = 0, w_n = 0;
+    load(k, r_n, p_n, w_n);
+    for (; k < nwin; k += stride) {
+        const uint32_t reach = r_n;
+        const uint64_t pos = p_n, w = w_n;
+        load(k + stride, r_n, p_n, w_n);
         if (!reach) continue;  // a window inside a literal group
-        const uint64_t pos = wpos[wb + k];
         const uint64_t idx = k * 32 + lane;
-        const uint64_t w = idx < L ? __ldg(s + idx) : 0ull;
         const uint64_t run = (w >> 1) & 0xFFFFFFFFull;
         const uint64_t dirty = w >> 33;
         const bool is_m = (reach >> lane) & 1u;
