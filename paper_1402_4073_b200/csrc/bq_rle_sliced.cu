@@ -3,23 +3,25 @@
 // The per-stream K4 (bq_rle.cu) gives each lane one stream and follows its
 // marker chain: a dependent shared-memory load per marker, and lanes idle while
 // the longest chain of the warp finishes (~47% lane efficiency on C4).  Here the
-// streams are re-encoded once per query into 1024-word slices whose markers are
-// contiguous per tile and cover exactly 1024 words each.  From them the build also
-// derives what phase A needs and nothing more: the nonzero updates every slice
-// makes to the tile's difference array, as 16-bit positions in four lists by kind
-// (+1 / -1 one-fill start / end, +1 / -1 << 16 literal start / end).  Phase A then
-// costs one shared-memory add per event with a warp-uniform constant -- no field
-// extraction, prefix sums or zero-update redirects (the marker decode it replaces
-// was ALU-pipe bound at ~28 thread instructions per marker).  Literal words are read
-// in phase C, only at undecided positions, as runmerge.cdom_threshold examines
-// dirty words only where the fill counts do not decide (runmerge.py:198-241);
-// phase C finds them by decoding the tile's markers (chunk checkpoints + warp
-// prefix sums).
+// streams are re-encoded once per query, every 1024-word slice of every stream
+// into what K4s reads and nothing more:
+//  - for phase A, the nonzero updates the slice's markers make to the tile's
+//    difference array (ones | dirty << 16), as 10-bit positions in six per-tile
+//    lists by update kind, packed 12 to a 16-byte vector and permuted so that each
+//    shared-memory atomic instruction hits 32 distinct banks.  Phase A then costs
+//    two ALU instructions and one shared-memory add per event, with a warp-uniform
+//    constant -- no field extraction, prefix sums or zero-update redirects (the
+//    marker decode it replaces was ALU-pipe bound at ~28 thread instructions per
+//    marker);
+//  - for phase C, the slice's literal words, position-major per tile, so the
+//    literal words of an undecided word are contiguous.  Literal words are read
+//    only at undecided positions, as runmerge.cdom_threshold examines dirty words
+//    only where the fill counts do not decide (runmerge.py:198-241).
 //
-// Per tile (one CTA): A) events staged into shared memory by TMA bulk copies in
-// 16 KB pieces (double-buffered) and added into the packed difference array cnt
-// (ones | dirty << 16); B) prefix sum and const_until decisions; C) bit counters
-// of undecided words from their literals.
+// Per tile (one CTA, tiles in descending order of reach): A) events staged into
+// shared memory by TMA bulk copies in 10 KB pieces (double-buffered) and added into
+// the packed difference array cnt; B) prefix sum and const_until decisions;
+// C) bit-sliced literal counts of undecided words.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
