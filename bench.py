@@ -613,9 +613,10 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
                     "api": "torch pinned H2D -> engine.RleQuery (bq_rle_query_create: K3) -> threshold (K4) -> D2H",
                     "matches_device_result": bool(p2_host == int(pc.item()))}
     from oracle import oracle as O
-    # parity on a window: the first 2^20 bits of every stream (the generator is sequential, so a
-    # run with r = 2^20 reproduces exactly the prefix of the full stream); rank 0 holds it
-    wr = 1 << 20
+    # parity on a window: the first 2^26 bits of every stream (the generator is sequential, so a
+    # run with r = 2^26 reproduces exactly the prefix of the full stream); rank 0 holds it.  The
+    # same window is the CPU baseline's sample (~1-2 s of the single-threaded cdom sweep).
+    wr = min(1 << 26, q.out_words * 64) if ctx.rank == 0 else 1 << 12
     wstreams = _markov_streams(lib, n, wr, m1, m0, host_threads())
     t0 = time.perf_counter()
     wexp = O.cdom_threshold(wstreams, wr, t)
@@ -652,7 +653,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
                   "matches_oracle_window": bool(exact_window),
                   "cpu_baseline": {"value": round(wbytes / cpu_s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
                                    "sample": "oracle cdom_threshold (runmerge.py heap sweep restated in C, single "
-                                             f"thread as the reference) on the first 2^20 bits of all 1024 streams "
+                                             f"thread as the reference) on the first 2^{wr.bit_length() - 1} bits of all 1024 streams "
                                              f"({wbytes} compressed bytes, {cpu_s:.2f} s)"}})
     line["_rank_bytes"] = comp_bytes * q.out_words / nw  # this rank's share of the query
     line["_scaling"] = "strong"
