@@ -88,6 +88,14 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 constexpr int kEvVec = 12;            // events per 16-byte vector (10-bit positions)
 constexpr int kEvRow = 32 * kEvVec;   // events per warp row
 constexpr int kEvKinds = 6;
+// Per-tile metadata of K4s in schedule order (one 64-byte load per CTA, no
+// dependent lookup through the tile order).
+struct __align__(16) TileMeta {
+    uint4 desc[3];   // the tile's list descriptor (tile_desc)
+    uint64_t ebase;  // its first event vector (tile_ebase)
+    uint32_t tile;   // the tile
+    uint32_t pad;
+};
 struct SlicedLayout {
     void *mem = nullptr;
     const uint64_t *literals = nullptr;   // [sum of tile literal counts]
@@ -98,6 +106,7 @@ struct SlicedLayout {
     const uint4 *tile_desc = nullptr;     // [3 ntiles] cumulative ends of the six lists in vectors, their real lengths
     const uint32_t *tile_order = nullptr; // [ntiles] tiles by descending reach (max ones + dirty of a word):
                                           // those that can need phase C are scheduled first
+    const TileMeta *tile_meta = nullptr;  // [ntiles] metadata of tile_order[i]
     uint64_t bytes = 0;
     uint64_t n_markers = 0, n_literals = 0;  // n_markers: slice markers (statistic; not stored)
     uint64_t n_events = 0;                   // event slots, padding included (kEvVec per 16-byte vector)

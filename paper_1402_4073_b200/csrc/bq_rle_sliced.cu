@@ -225,6 +225,21 @@ __global__ void slice_emit_kernel(const uint64_t *const *ptrs, const uint64_t *l
     }
 }
 
+__global__ void gather_meta_kernel(const uint32_t *order, const uint4 *desc, const uint64_t *ebase, TileMeta *meta,
+                                   uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = order[i];
+    TileMeta tm;
+    tm.desc[0] = desc[3 * (size_t)t];
+    tm.desc[1] = desc[3 * (size_t)t + 1];
+    tm.desc[2] = desc[3 * (size_t)t + 2];
+    tm.ebase = ebase[t];
+    tm.tile = t;
+    tm.pad = 0;
+    meta[i] = tm;
+}
+
 __global__ void iota_kernel(uint32_t *ids, uint32_t n) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) ids[k] = k;
@@ -357,6 +372,7 @@ struct SlArgs {
     const uint64_t *tile_ebase;
     const uint4 *tile_desc;
     const uint32_t *tile_order;
+    const TileMeta *tile_meta;
     SlicedEval e;
 };
 
@@ -470,17 +486,23 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
     const SlicedEval &E = a.e;
-    const uint32_t tile = a.tile_order ? a.tile_order[blockIdx.x] : blockIdx.x;  // tile of the query's range
+    uint32_t tile;  // tile of the query's range
+    EvDesc ee;
+    const uint4 *tev;
+    if (a.tile_meta) {  // schedule order: one metadata load
+        const TileMeta &tm = a.tile_meta[blockIdx.x];
+        ee = EvDesc{tm.desc[0], tm.desc[1], tm.desc[2]};
+        tev = a.events + tm.ebase;
+        tile = tm.tile;
+    } else {  // layout build (reach pass): tile order
+        tile = blockIdx.x;
+        ee = EvDesc{a.tile_desc[3 * tile], a.tile_desc[3 * tile + 1], a.tile_desc[3 * tile + 2]};
+        tev = a.events + a.tile_ebase[tile];
+    }
     const uint64_t ts = (uint64_t)(E.tile0 + tile) * kRleTile;
     const int width = (int)min((uint64_t)kRleTile, E.total_words - ts);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t lbase = a.tile_lbase[tile];
-    const uint32_t nlit = (uint32_t)(a.tile_lbase[tile + 1] - lbase);
-    const uint64_t *tlit = a.literals + lbase;
-    const uint32_t *tls = a.lit_start + (size_t)tile * kLitStarts;
-    const EvDesc ee{a.tile_desc[3 * tile], a.tile_desc[3 * tile + 1], a.tile_desc[3 * tile + 2]};
     const uint32_t nvec = ee.b.y;
-    const uint4 *tev = a.events + a.tile_ebase[tile];
     const uint32_t npieces = (nvec + kPieceVecs - 1) / kPieceVecs;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
 
@@ -566,6 +588,10 @@ __global__ void __launch_bounds__(kSlNT, BQ_SL_MINB) rle_sliced_kernel(const __g
         sl_finish(pc, lane, E.popcnt);
         return;
     }
+    const uint64_t lbase = a.tile_lbase[tile];
+    const uint32_t nlit = (uint32_t)(a.tile_lbase[tile + 1] - lbase);
+    const uint64_t *tlit = a.literals + lbase;
+    const uint32_t *tls = a.lit_start + (size_t)tile * kLitStarts;
     if (tid == 0) {  // phase C reads the tile's literal offsets and some of its literals
         auto prefetch = [](const void *from, const void *to) {
             const uint64_t p0 = reinterpret_cast<uint64_t>(from) & ~15ull;
@@ -688,7 +714,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     const size_t o_teb = o_ev + ne * 16;
     const size_t o_tee = r16(o_teb + T1 * 8);
     const size_t o_ord = o_tee + (size_t)ntiles * 48;
-    const size_t bytes = o_ord + (size_t)ntiles * 4;
+    const size_t o_meta = (o_ord + (size_t)ntiles * 4 + 63) / 64 * 64;
+    const size_t bytes = o_meta + (size_t)ntiles * sizeof(TileMeta);
     char *m = nullptr, *tmpl = nullptr;  // tmpl: literals and positions as emitted, slice by slice
     e = cudaMalloc(&m, bytes);
     if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * kEvVec * 2);  // event positions as emitted, slice by slice
@@ -773,6 +800,11 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         e = cudaGetLastError();
         if (e == cudaSuccess)
             e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, sort_bytes, reach, reach_sorted, ids, order, (int)ntiles);
+        if (e == cudaSuccess) {
+            gather_meta_kernel<<<(ntiles + 255) / 256, 256>>>(order, tee, teb, reinterpret_cast<TileMeta *>(m + o_meta),
+                                                             ntiles);
+            e = cudaGetLastError();
+        }
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         cudaFree(ss);
         if (e != cudaSuccess) {
@@ -781,6 +813,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         }
     }
     l.tile_order = order;
+    l.tile_meta = reinterpret_cast<const TileMeta *>(m + o_meta);
     l.literals = literals;
     l.lit_start = lit_start;
     l.tile_lbase = tlb;
@@ -809,6 +842,7 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
     a.tile_ebase = l.tile_ebase;
     a.tile_desc = l.tile_desc;
     a.tile_order = e.reach_out ? nullptr : l.tile_order;
+    a.tile_meta = e.reach_out ? nullptr : l.tile_meta;
     a.e = e;
     cudaError_t err = cudaFuncSetAttribute(rle_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlSmem);
     if (err != cudaSuccess) return cuda_error(err, "cudaFuncSetAttribute(rle_sliced_kernel)");
