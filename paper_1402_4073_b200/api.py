@@ -13,8 +13,11 @@ HBM-resident ``DeviceBitmap`` / ``DeviceRleBitmap``:
 
 All the reference's algorithm variants compute the same function, so they all
 dispatch to the same kernels; they differ only in their argument contracts and
-``stats`` keys, which are reproduced.  There is no CPU fallback: without the
-CUDA library every call raises ``ExtensionMissing``.
+``stats`` keys.  Keys that describe the query (counter_width, increments,
+bitmap_ops) are reproduced; cdom's keys count the steps of its CPU heap sweep
+(segments, heap_pops, branches; runmerge.py:238-240), which the device path does
+not take, so its ``stats`` dict is left as passed.  There is no CPU fallback:
+without the CUDA library every call raises ``ExtensionMissing``.
 """
 
 from __future__ import annotations
@@ -297,7 +300,9 @@ def csv_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
 
 
 def cdom_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
-    """runmerge.cdom_threshold (runmerge.py:198-241): RLE inputs only."""
+    """runmerge.cdom_threshold (runmerge.py:198-241): RLE inputs only.  ``stats`` is
+    accepted for the signature; the heap-sweep counters it would hold
+    (runmerge.py:238-240) have no device counterpart."""
     n = len(bitmaps)
     _check_t(n, t)
     if any(kind_of(b) not in ("r", "dr") for b in bitmaps):
@@ -306,7 +311,8 @@ def cdom_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
 
 
 def cdom_symmetric(bitmaps: Sequence, spec, stats: dict | None = None):
-    """runmerge.cdom_symmetric (runmerge.py:244-299): RLE inputs only."""
+    """runmerge.cdom_symmetric (runmerge.py:244-299): RLE inputs only.  ``stats`` as
+    for cdom_threshold."""
     accept_bytes(spec, len(bitmaps))
     if any(kind_of(b) not in ("r", "dr") for b in bitmaps):
         raise InputError("cdom operates on RLE bitmaps; compress inputs first")
