@@ -412,16 +412,24 @@ def _l2_flush(scratch):
 def _timed_launches(torch, launch, steps, warmup, stream, flush=None):
     """Run `launch()` (which enqueues kernels on `stream`) warmup+steps times;
     return per-launch CUDA-event times in ms.  `flush()` (L2 flush) runs
-    between launches outside the events."""
+    between launches outside the events; without a flush the launches run back
+    to back between one event pair and each gets the average."""
     for _ in range(warmup):
         if flush:
             flush()
         launch()
     torch.cuda.synchronize()
+    if not flush:  # back-to-back launches: one event pair around all of them (no instrumentation inside)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            launch()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) / steps] * steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for s in range(steps):
-        if flush:
-            flush()
+        flush()
         ev[s][0].record(stream)
         launch()
         ev[s][1].record(stream)
