@@ -158,6 +158,41 @@ def test_ragged_and_degenerate_streams(bq):
         assert np.array_equal(exp, O.scan_count(dec, r, t))
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_directory_ring_horizon(bq, seed):
+    """K3a's staging ring (14 windows of 32 words ahead) and its 4-window chain
+    tables: literal groups whose lengths straddle the ring horizon (a restart at the
+    next marker) and the group boundary, markers landing on window and group edges,
+    streams whose length is not a multiple of 32, and an implicit zero tail."""
+    mk = lambda bit, run, dirty: bit | (run << 1) | (dirty << 33)  # noqa: E731
+    rng = np.random.default_rng(100 + seed)
+    r = 64 * 1024 * 24 + 5
+    nw = (r + 63) // 64
+    streams = []
+    for i in range(24):
+        out, covered = [], 0
+        while covered < nw - 2000:
+            kind = rng.integers(0, 4)
+            if kind == 0:  # a literal group around the ring horizon (448 words) or a group edge (128)
+                d = int(rng.choice([1, 31, 32, 33, 95, 127, 128, 129, 445, 446, 447, 448, 449, 480, 900]))
+            else:
+                d = int(rng.integers(0, 4))
+            run = int(rng.integers(0, 300))
+            d = min(d, nw - covered - run)
+            out.append(mk(int(rng.integers(0, 2)) if run else 0, run, d))
+            out.extend(int(x) for x in rng.integers(1, 2**63, size=d))
+            covered += run + d
+        if i % 3 == 0:  # explicit fill to the end; otherwise the implicit zero tail
+            out.append(mk(0, nw - covered, 0))
+        streams.append(np.array(out, dtype=np.uint64))
+    q = bq.RleQuery(dev(streams), r)
+    for t in (1, 3, 12, 24):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+
+
 def test_c4_shape_scaled(bq):
     """Config 4 generator (one-runs mean 256, zero-runs 12544, density 0.02) at
     N=1024 and r=2^24 bits, T=50 (the config's T) and T=5,10,20 where the dirty
