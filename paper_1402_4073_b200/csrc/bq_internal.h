@@ -72,8 +72,9 @@ __device__ __forceinline__ bool accept_at(const uint32_t *bits, uint32_t c) { re
 //    updates of neighbouring markers merged: +1 / -1 where a one-fill starts / ends,
 //    +1 / -1 << 16 where a literal group starts / ends, +1 - (1 << 16) where a
 //    one-fill starts as a literal group ends, -1 + (1 << 16) where a one-fill ends as
-//    a literal group starts.  An event is its 10-bit word position; 16-byte vectors
-//    hold 12 (three per 32-bit word).  Each tile has six lists, one per kind, holding
+//    a literal group starts.  An event is its 10-bit word position, stored as a byte
+//    offset (position * 4) in bits 2-11, 12-21 or 22-31 of a 32-bit word; 16-byte
+//    vectors hold 12.  Each tile has six lists, one per kind, holding
 //    all slices' events of that kind, each padded to whole warp rows (kEvRow events:
 //    32 lanes x one vector), padding slots skipped by their index.  Inside a list the
 //    events are permuted so that the 32 updates of each shared-memory atomic

@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256) arrange_events_kernel(const uint16_t *src
     auto place = [&](uint32_t sidx, uint32_t pos) {
         const uint32_t within = sidx % kEvRow, j = within / 32;
         const uint32_t vec = sidx / kEvRow * 32 + within % 32;
-        atomicOr(d + (size_t)vec * 4 + j / 3, pos << (10 * (j % 3)));
+        atomicOr(d + (size_t)vec * 4 + j / 3, pos << (10 * (j % 3) + 2));  // byte offsets: bits 2-11, 12-21, 22-31
     };
     if (tid < 32) {
         bank_cnt[tid] = 0;
@@ -381,13 +381,16 @@ struct EvDesc {
     uint4 a, b, c;  // ends: a.x..a.w, b.x, b.y; real lengths: b.z, b.w, c.x..c.w
 };
 
-// Three 10-bit events (word positions) of one 32-bit word: event j of the vector is
-// field j mod 3 of word j / 3; events j with 32 j >= limit are padding.
+// Three 10-bit events of one 32-bit word, stored as byte offsets into the difference
+// array (position * 4 in bits 2-11, 12-21, 22-31: one LOP3 for the first, a shift and
+// a LOP3 for the others): event j of the vector is field j mod 3 of word j / 3;
+// events j with 32 j >= limit are padding.
 template <int J0>
 __device__ __forceinline__ void add_events(uint32_t *cnt, uint32_t w, uint32_t delta, int limit) {
 #pragma unroll
     for (int f = 0; f < 3; ++f)
-        if ((J0 + f) * 32 < limit) atomicAdd(cnt + ((w >> (10 * f)) & 0x3FFu), delta);
+        if ((J0 + f) * 32 < limit)
+            atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + ((w >> (10 * f)) & 0xFFCu)), delta);
 }
 
 // Row descriptor of the warp row starting at vector g of the tile: the constant of
