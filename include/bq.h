@@ -67,6 +67,12 @@ BQ_API int bq_version(void);
 /* Message of the last failing call on this thread ("" if none). */
 BQ_API const char *bq_last_error(void);
 
+/* Return the device memory the library keeps cached for later queries (RLE
+ * directories, tile-sliced layouts and their build scratch are taken from a
+ * stream-ordered pool that retains up to 16 GiB after frees) to the driver.
+ * Synchronizes the current device. */
+BQ_API int bq_release_cached_memory(void);
+
 /* Prepare a query over inputs[0..n) whose result has bit length r_bits
  * (= max input bit_length, counters.py:51-52).  Computes output words
  * [w_begin, w_end) of the result (w_end = UINT64_MAX means ceil(r/64)); w_begin

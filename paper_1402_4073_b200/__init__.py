@@ -45,7 +45,7 @@ from .api import (
     wide_or,
 )
 from .bitmaps import DeviceBitmap, DeviceRleBitmap, RleBitmap, UncompressedBitmap
-from .engine import RleQuery, ThresholdQuery, sweep_host
+from .engine import RleQuery, ThresholdQuery, release_cached_memory, sweep_host
 from .errors import (
     BitquorumError,
     CorrectnessError,

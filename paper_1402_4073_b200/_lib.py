@@ -36,6 +36,7 @@ _I = ctypes.c_int
 SIGNATURES = {
     "bq_version": (_I, []),
     "bq_last_error": (ctypes.c_char_p, []),
+    "bq_release_cached_memory": (_I, []),
     "bq_query_create": (_I, [_P, _I, _U64, _U64, _U64, _I, _P]),
     "bq_query_destroy": (None, [_P]),
     "bq_query_out_words": (_U64, [_P]),

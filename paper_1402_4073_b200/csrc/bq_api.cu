@@ -43,6 +43,50 @@ int use_device(int device) {
     return BQ_OK;
 }
 
+// Library memory pool (one per device): RLE query directories, tile-sliced layouts
+// and their build scratch are large and allocated once per query object; a
+// stream-ordered pool that keeps up to kPoolKeep bytes after frees makes the next
+// query's allocations cheap instead of remapping gigabytes per query.
+constexpr uint64_t kPoolKeep = 16ull << 30;
+static cudaMemPool_t device_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[dev] = p;
+    }
+    return pools[dev];
+}
+
+cudaError_t pool_alloc(void **p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = device_pool(dev);
+    if (!pool) return cudaMalloc(p, bytes);
+    cudaError_t e = cudaMallocFromPoolAsync(p, bytes, pool, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);  // usable from any stream on return
+    return e;
+}
+
+void pool_free(void *p) {
+    if (!p) return;
+    cudaDeviceSynchronize();  // no evaluation may still be reading it (cudaFree's implicit sync)
+    if (cudaFreeAsync(p, 0) != cudaSuccess) cudaGetLastError();
+    cudaStreamSynchronize(0);
+}
+
 int sm_count() {
     static int cache[64] = {0};
     int dev = 0;
@@ -134,6 +178,16 @@ extern "C" {
 BQ_API int bq_version(void) { return 100; }
 
 BQ_API const char *bq_last_error(void) { return g_last_error.c_str(); }
+
+BQ_API int bq_release_cached_memory(void) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = bq::device_pool(dev);
+    if (!pool) return BQ_OK;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+    return e == cudaSuccess ? BQ_OK : bq::cuda_error(e, "cudaMemPoolTrimTo");
+}
 
 BQ_API int bq_query_create(const bq_span *inputs, int n, uint64_t r_bits, uint64_t w_begin,
                            uint64_t w_end, int device, bq_query **out) {

@@ -26,6 +26,10 @@ int cuda_error(cudaError_t e, const char *what);
     } while (0)
 
 int use_device(int device);  // cudaSetDevice when device >= 0
+// The library's stream-ordered memory pool (query directories, tile-sliced layouts
+// and their build scratch): freed blocks are kept for the next query.
+cudaError_t pool_alloc(void **p, size_t bytes);
+void pool_free(void *p);
 int sm_count();              // SMs of the current device
 
 // ---- K1/K2: uncompressed counting kernel ------------------------------------

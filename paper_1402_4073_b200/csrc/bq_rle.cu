@@ -614,7 +614,7 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
     q->tile0 = tile0;
     q->ntiles = ntiles;
     q->dir_bytes = dirb;
-    cudaError_t e = cudaMalloc(&q->mem, bytes);
+    cudaError_t e = pool_alloc(reinterpret_cast<void **>(&q->mem), bytes);
     if (e != cudaSuccess) {
         delete q;
         return cuda_error(e, "cudaMalloc(rle directory)");
@@ -635,7 +635,7 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
     if (e == cudaSuccess) e = cudaMemcpy(q->d_lens, lens.data(), (size_t)n * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(d_err, 0, 16);
     if (e != cudaSuccess) {
-        cudaFree(q->mem);
+        pool_free(q->mem);
         delete q;
         return cuda_error(e, "rle query setup");
     }
@@ -661,7 +661,7 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
         }
         const uint64_t nwin_all = wbase[n];
         char *scratch = nullptr;
-        e = cudaMalloc(&scratch, (size_t)(n + 1) * 8 + nwin_all * 12 + 16);
+        e = pool_alloc(reinterpret_cast<void **>(&scratch), (size_t)(n + 1) * 8 + nwin_all * 12 + 16);
         uint64_t *d_wbase = reinterpret_cast<uint64_t *>(scratch);
         uint64_t *d_wpos = d_wbase + n + 1;
         uint32_t *d_wreach = reinterpret_cast<uint32_t *>(d_wpos + nwin_all);
@@ -679,17 +679,17 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        if (scratch) cudaFree(scratch);
+        if (scratch) pool_free(scratch);
         int herr[4] = {0, 0, 0, 0};
         if (e == cudaSuccess) e = cudaMemcpy(herr, d_err, 16, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) {
-            cudaFree(q->mem);
+            pool_free(q->mem);
             delete q;
             return cuda_error(e, "rle directory (K3)");
         }
         if (herr[0]) {
             unsigned long long bad = (unsigned long long)(uint32_t)herr[2] | ((unsigned long long)(uint32_t)herr[3] << 32);
-            cudaFree(q->mem);
+            pool_free(q->mem);
             delete q;
             if (herr[0] == RLE_ERR_TRUNCATED)
                 return set_error(BQ_EFORMAT, "stream %llu: marker announces more literal words than present", bad);
@@ -705,9 +705,9 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
 BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     if (!q) return;
     if (q->device >= 0) cudaSetDevice(q->device);
-    cudaFree(q->mem);
+    pool_free(q->mem);
     free_sliced(&q->sliced);
-    for (auto &kv : q->tables) cudaFree(kv.second);
+    for (auto &kv : q->tables) pool_free(kv.second);
     delete q;
 }
 
@@ -770,10 +770,10 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         if (it != q->tables.end()) {
             d_tab = it->second;
         } else if (q->tables.size() < kMaxTables) {
-            e = cudaMalloc(&d_tab, bytes);
+            e = pool_alloc(reinterpret_cast<void **>(&d_tab), bytes);
             if (e == cudaSuccess) e = cudaMemcpy(d_tab, host.data(), bytes, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) {
-                if (d_tab) cudaFree(d_tab);
+                if (d_tab) pool_free(d_tab);
                 return cuda_error(e, "accept table upload");
             }
             q->tables.emplace(acc, d_tab);

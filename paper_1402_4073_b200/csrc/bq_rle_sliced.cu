@@ -671,7 +671,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     if (e != cudaSuccess) return cuda_error(e, "DeviceScan sizing");
     const size_t scratch_bytes = cells * 40 + 6 * T1 * 8 + 16 + T1 * 48 + tmp_bytes + 256;
     char *scratch = nullptr;
-    e = cudaMalloc(&scratch, scratch_bytes);
+    e = pool_alloc(reinterpret_cast<void **>(&scratch), scratch_bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return BQ_OK;  // no room: the query keeps the per-stream layout
@@ -685,8 +685,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     const unsigned grid = (unsigned)std::min<uint64_t>((cells + 255) / 256, (uint64_t)sms * 32);
     char *evsrc = nullptr;
     auto fail = [&](cudaError_t err, const char *what) {
-        cudaFree(scratch);
-        if (evsrc) cudaFree(evsrc);
+        pool_free(scratch);
+        if (evsrc) pool_free(evsrc);
         return cuda_error(err, what);
     };
     slice_count_kernel<<<grid, 256>>>(d_ptrs, d_lens, d_dir, n, tile0, ntiles, counts, ecounts);
@@ -720,14 +720,14 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     const size_t o_meta = (o_ord + (size_t)ntiles * 4 + 63) / 64 * 64;
     const size_t bytes = o_meta + (size_t)ntiles * sizeof(TileMeta);
     char *m = nullptr, *tmpl = nullptr;  // tmpl: literals and positions as emitted, slice by slice
-    e = cudaMalloc(&m, bytes);
-    if (e == cudaSuccess && ne) e = cudaMalloc(&evsrc, ne * kEvVec * 2);  // event positions as emitted, slice by slice
-    if (e == cudaSuccess) e = cudaMalloc(&tmpl, nl * 10 + 16);
+    e = pool_alloc(reinterpret_cast<void **>(&m), bytes);
+    if (e == cudaSuccess && ne) e = pool_alloc(reinterpret_cast<void **>(&evsrc), ne * kEvVec * 2);  // event positions as emitted, slice by slice
+    if (e == cudaSuccess) e = pool_alloc(reinterpret_cast<void **>(&tmpl), nl * 10 + 16);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        if (m) cudaFree(m);
-        if (evsrc) cudaFree(evsrc);
-        cudaFree(scratch);
+        if (m) pool_free(m);
+        if (evsrc) pool_free(evsrc);
+        pool_free(scratch);
         return BQ_OK;
     }
     SlicedLayout l;
@@ -759,11 +759,11 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    cudaFree(scratch);
-    cudaFree(tmpl);
-    if (evsrc) cudaFree(evsrc);
+    pool_free(scratch);
+    pool_free(tmpl);
+    if (evsrc) pool_free(evsrc);
     if (e != cudaSuccess) {
-        cudaFree(m);
+        pool_free(m);
         return cuda_error(e, "slice_emit_kernel / sort_literals_kernel / arrange_events_kernel");
     }
     // tile order: a reach-only pass of K4s, then tiles sorted by descending reach
@@ -773,9 +773,9 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         size_t sort_bytes = 0;
         e = cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                                       (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)ntiles);
-        if (e == cudaSuccess) e = cudaMalloc(&ss, (size_t)ntiles * 12 + 16 + sort_bytes);
+        if (e == cudaSuccess) e = pool_alloc(reinterpret_cast<void **>(&ss), (size_t)ntiles * 12 + 16 + sort_bytes);
         if (e != cudaSuccess) {
-            cudaFree(m);
+            pool_free(m);
             return cuda_error(e, "tile order scratch");
         }
         uint32_t *reach = reinterpret_cast<uint32_t *>(ss), *reach_sorted = reach + ntiles, *ids = reach_sorted + ntiles;
@@ -795,8 +795,8 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
         re.reach_out = reach;
         int rc = launch_sliced(tmp, re, 0);
         if (rc) {
-            cudaFree(ss);
-            cudaFree(m);
+            pool_free(ss);
+            pool_free(m);
             return rc;
         }
         iota_kernel<<<(ntiles + 255) / 256, 256>>>(ids, ntiles);
@@ -809,9 +809,9 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        cudaFree(ss);
+        pool_free(ss);
         if (e != cudaSuccess) {
-            cudaFree(m);
+            pool_free(m);
             return cuda_error(e, "tile order");
         }
     }
@@ -832,7 +832,7 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
 }
 
 void free_sliced(SlicedLayout *l) {
-    if (l->mem) cudaFree(l->mem);
+    if (l->mem) pool_free(l->mem);
     *l = SlicedLayout();
 }
 

@@ -263,6 +263,13 @@ class RleQuery:
             pass
 
 
+def release_cached_memory() -> None:
+    """Return the device memory libbq keeps for later queries (RLE directories,
+    tile-sliced layouts and their build scratch come from a pool that retains up
+    to 16 GiB after frees) to the driver (bq_release_cached_memory)."""
+    _lib.check(_lib.load().bq_release_cached_memory(), "bq_release_cached_memory")
+
+
 def accept_bytes(accept, n: int) -> np.ndarray:
     """SymmetricSpec (``.accept``) or a bool sequence -> n + 1 bytes (oracle.py:17-31)."""
     acc = getattr(accept, "accept", accept)

@@ -497,3 +497,20 @@ def test_max_inputs_rle(bq):
             exp = O.cdom_threshold(streams, r, t)
             assert np.array_equal(host(out, nw), exp), t
             assert int(pc.item()) == popcount(exp)
+
+
+def test_release_cached_memory_between_queries(bq):
+    """Queries take their directory and layout from libbq's memory pool; returning
+    the cached memory to the driver between queries leaves later queries correct."""
+    lib = bq._lib.load()
+    n, r = 40, 1 << 19
+    streams = [markov(lib, 9, i, r, 64.0, 2000.0) for i in range(n)]
+    nw = r // 64
+    for _ in range(2):
+        q = bq.RleQuery(dev(streams), r)
+        for t in (2, 5):
+            out, pc = q.threshold(t)
+            exp = O.cdom_threshold(streams, r, t)
+            assert np.array_equal(host(out, nw), exp), t
+        q.close()
+        bq.release_cached_memory()
