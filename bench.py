@@ -470,6 +470,10 @@ def run_c1(args, torch, bq, lib, dev, stream, ctx):
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     ms = _timed_launches(torch, lambda: q.threshold(t, out, pc, stream=stream), args.steps, args.warmup, stream,
                          flush=lambda: _l2_flush(scratch))
+    # the floor of this timing method: a one-element kernel between the same events after the same flush
+    one = torch.zeros(1, dtype=torch.int64, device=dev)
+    floor_ms = _timed_launches(torch, lambda: one.add_(1), args.steps, args.warmup, stream,
+                               flush=lambda: _l2_flush(scratch))
     in_bytes = n * nw * 8
     from oracle import oracle as O
     host = [data[i].cpu().numpy().view(np.uint64) for i in range(n)]
@@ -484,6 +488,9 @@ def run_c1(args, torch, bq, lib, dev, stream, ctx):
                  {"workload": "C1: N=8, r=2^20 bits, p=0.1 (q=6554), T=3; L2 flushed (256 MB read) between launches",
                   "n_bitmaps": n, "r_bits": 64 * nw, "t": t},
                  {"matches_oracle": bool(exact),
+                  "timing_floor_ms": round(statistics.median(floor_ms), 5),
+                  "timing_floor_note": "median of a one-element kernel timed the same way (events around one "
+                                       "launch after a 256 MB L2 flush): C1 is launch/latency bound",
                   "cpu_baseline": {"value": round(cpu_gbs, 3), "unit": "GB/s", "cores": host_threads(), "kind": "port",
                                    "sample": "full C1, orc_threshold_port (csv_threshold port), 2 s"}})
     line["_rank_bytes"] = in_bytes  # replicas at N > 1
