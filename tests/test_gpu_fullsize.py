@@ -187,3 +187,20 @@ def test_c4_full_size_low_t_and_symmetric(bq):
     exp = O.cdom_symmetric(streams, r, acc)
     assert np.array_equal(_host(out[:nw]), exp)
     assert int(pc.item()) == _popcount(exp)
+    # thresholds where phase C runs in most tiles: K4s against the per-stream K4, whole
+    import os
+
+    for t in (10, 20, 30):
+        out, pc = q.threshold(t)
+        sliced, pc_sliced = _host(out[:nw]).copy(), int(pc.item())
+        prev = os.environ.get("BQ_RLE_SLICED")
+        os.environ["BQ_RLE_SLICED"] = "0"
+        try:
+            out, pc = q.threshold(t)
+        finally:
+            if prev is None:
+                del os.environ["BQ_RLE_SLICED"]
+            else:
+                os.environ["BQ_RLE_SLICED"] = prev
+        assert np.array_equal(sliced, _host(out[:nw])), t
+        assert pc_sliced == int(pc.item()) == _popcount(sliced), t
