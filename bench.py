@@ -142,22 +142,18 @@ def physical_gpu_index(local: int) -> int:
 # CPU side (oracle port): used for cpu_baseline and --impl reference
 
 def cpu_windows(nwin: int, win_words: int, world_rank_offset: int = 0):
-    """Host copies of ``nwin`` distinct C2 windows (N x win_words each), from the
-    same generator as the GPU inputs (bitmap i, global words)."""
-    from paper_1402_4073_b200 import _lib
+    """Host copies of ``nwin`` distinct C2 windows (N x win_words each) of the same
+    seeded inputs as the GPU arm (bitmap i, global words), generated by the oracle's
+    independent restatement of the generator (oracle/bq_oracle.c orc_gen_*), so the
+    CPU legs never load libbq.so."""
+    from oracle import oracle as O
 
-    lib = _lib.load()
-    qs = [lib.bq_gen_density_q16(SEED, i, DENS_LO, DENS_HI) for i in range(C2_N)]
+    qs = [O.gen_density_q16(SEED, i, DENS_LO, DENS_HI) for i in range(C2_N)]
     wins = []
     stride = C2_WORDS // nwin
     for k in range(nwin):
         w0 = world_rank_offset + k * stride
-        rows = []
-        for i in range(C2_N):
-            a = np.empty(win_words, dtype=np.uint64)
-            _lib.check(lib.bq_gen_bernoulli(SEED, i, qs[i], w0, win_words, a.ctypes.data, 0, None))
-            rows.append(a)
-        wins.append(rows)
+        wins.append([O.gen_bernoulli(SEED, i, qs[i], w0, win_words) for i in range(C2_N)])
     return wins
 
 
@@ -203,7 +199,7 @@ def cpu_baseline(budget_s: float = 12.0):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(max(1, args.gpus))))
     if rank != 0:
         return 0
     threads = host_threads()
@@ -217,7 +213,11 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (bq_gen Bernoulli, seed 1402)",
         "config": {"workload": "C2 sample: N=64 bitmaps, 16 distinct windows of 2^16 words (512 MiB), "
                                "T sweep {1,2,16,32,64}; one step = 5 queries over one window",
-                   "n_bitmaps": C2_N, "ts": list(C2_TS)},
+                   "n_bitmaps": C2_N, "ts": list(C2_TS),
+                   "same_config_as_gpu_arm": False,
+                   "sample_note": "bounded sample of the GPU arm's C2 workload (same seeded bitmaps, same metric and "
+                                  "T sweep): word windows instead of the full 2 GiB, since cost is linear in words "
+                                  "(PAPER.md:283-298); the windows (512 MiB) exceed the host caches"},
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": "reference algorithms (wide_or / wide_and / csv_threshold) restated in C "
                                    "(oracle/bq_oracle.c), OpenMP over word batches, on C2 windows"},
@@ -362,6 +362,31 @@ def run_ours(args):
                "api": "paper_1402_4073_b200.sweep_host -> bq_sweep_host (pinned host in/out)",
                "matches_device_result": bool(ok)}
 
+    # --- C5 strong scaling (BASELINE configs[4]): the sharded majority query --------
+    c5 = None
+    if not args.no_c5:
+        import types
+
+        ctx = types.SimpleNamespace(world=world, rank=rank, dist=dist, cpu=False)
+        l5 = run_c5(args, torch, bq, lib, dev, stream, ctx)
+        red = torch.tensor([l5["_rank_ms"], float(l5["_rank_bytes"]), float(l5["popcount"])], dtype=torch.float64,
+                           device=dev)
+        mx = red.clone()
+        if world > 1:
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(red, op=dist.ReduceOp.SUM)
+        job_ms, job_bytes = float(mx[0]), float(red[1])
+        c5 = {"value": round(job_bytes / (job_ms / 1e3) / 1e9, 3), "unit": "GB/s", "scaling": "strong",
+              "query_ms": round(job_ms, 4), "n_gpus": world, "input_bytes": int(job_bytes),
+              "waves_per_rank": l5["config"]["waves_per_rank"], "popcount": int(red[2]),
+              "roofline_frac": l5["roofline"]["frac"],
+              "workload": "C5: N=511, r=2^32 bits, p=0.5, T=256 (256 GiB) split by word range over the ranks; "
+                          "each rank runs its shard as waves of <= 32 GiB (8 waves at N=1, 1 at N=8); query_ms = "
+                          "max over ranks of the summed per-wave query times, each query followed by the popcount "
+                          "all-reduce (inside the timed launches)"}
+        del l5
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_budget)
@@ -391,6 +416,7 @@ def run_ours(args):
             "gpu_launches": len(C2_TS) * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "c5_strong_scaling": c5,
         }
         cl = clocks.summary()
         line["clocks"] = cl
@@ -552,6 +578,16 @@ def _markov_streams(lib, n, r, m1, m0, threads):
         return list(ex.map(one, range(n)))
 
 
+def _oracle_markov_streams(n, r, m1, m0, threads):
+    """The same C4 streams from the oracle's generator restatement (CPU legs only)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        return list(ex.map(lambda i: O.gen_markov_rle(SEED, i, r, m1, m0), range(n)))
+
+
 def run_c4(args, torch, bq, lib, dev, stream, ctx):
     """Config 4: N=1024 RLE bitmaps, r=2^30, one-runs mean 256 bits, zero-runs mean
     12544 (density 0.02, interpretation A of SURVEY App. B), T=50; output uncompressed."""
@@ -653,7 +689,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
     # run with r = 2^26 reproduces exactly the prefix of the full stream); rank 0 holds it.  The
     # same window is the CPU baseline's sample (~1-2 s of the single-threaded cdom sweep).
     wr = min(1 << 26, q.out_words * 64) if ctx.rank == 0 else 1 << 12
-    wstreams = _markov_streams(lib, n, wr, m1, m0, host_threads())
+    wstreams = _oracle_markov_streams(n, wr, m1, m0, host_threads())
     t0 = time.perf_counter()
     wexp = O.cdom_threshold(wstreams, wr, t)
     cpu_s = time.perf_counter() - t0
@@ -741,6 +777,7 @@ def run_c5(args, torch, bq, lib, dev, stream, ctx):
                               "processed as generate->compute waves of <= 2^23 words (32 GiB, one GPU's shard at 8 "
                               "GPUs); kernels (+ popcount all-reduce) timed only",
                   "n_bitmaps": n, "r_bits": 64 * total, "t": t, "wave_words": wave,
+                  "waves_per_rank": (e - b + wave - 1) // wave,
                   "parallelism": f"word-range shards x{ctx.world}" if ctx.world > 1 else "1 GPU, 8 waves"},
                  {"full_query_ms": round(rank_ms, 3), "popcount": pc_total})
     line["_rank_bytes"] = n * (e - b) * 8
@@ -799,6 +836,29 @@ def run_extra(args):
     return 0
 
 
+def self_launch(n: int) -> int:
+    """``--gpus N`` outside torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and the same arguments; rank 0 prints the
+    line.  The ranks need N visible GPUs (or BQ_BENCH_SHARE_GPU=1, a functional
+    check that is not a measurement)."""
+    import socket
+
+    if os.environ.get("BQ_BENCH_SHARE_GPU") != "1":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c2",
@@ -812,10 +872,13 @@ def main():
     ap.add_argument("--e2e-chunk-mib", type=int, default=0, help="host streaming chunk (MiB of input; 0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 strong-scaling fields of the default line")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return self_launch(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload != "c2":

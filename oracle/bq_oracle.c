@@ -694,3 +694,111 @@ int orc_num_threads(void) {
     return 1;
 #endif
 }
+
+/* ---------------------------------------------------------------------------
+ * Benchmark input generators, restated independently of the product's
+ * csrc/bq_gen.h so that bench.py's CPU legs (cpu_baseline, --impl reference)
+ * and the tests can build inputs without loading libbq.so.  Pinned by
+ * tests/golden/kat.json (Bernoulli / density KATs from an independent
+ * pure-Python statement in tests/golden/make_golden.py) and checked equal to
+ * the product generator in tests/test_oracle.py.  The reference has no
+ * generator for BASELINE.json's configs (its bench/datagen.py draws
+ * fixed-cardinality sets), so there is no reference line to cite.
+ *
+ *   SplitMix64 finaliser; per-bitmap key = mix(mix(seed ^ K0) + (i+1)*GAMMA);
+ *   word w of Bernoulli(q/2^16) composes 16 random words, LSB digit of q first.
+ */
+#include <math.h>
+
+#define ORC_GAMMA 0x9E3779B97F4A7C15ull
+
+static inline uint64_t orc_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static inline uint64_t orc_key(uint64_t seed, uint64_t i) {
+    return orc_mix(orc_mix(seed ^ 0x5851F42D4C957F2Dull) + (i + 1) * ORC_GAMMA);
+}
+
+static inline uint64_t orc_rand(uint64_t key, uint64_t ctr) { return orc_mix(key + (ctr + 1) * ORC_GAMMA); }
+
+static uint64_t orc_bernoulli_word(uint64_t key, uint64_t w, uint32_t q) {
+    if (q == 0) return 0;
+    if (q >= 65536u) return ~0ull;
+    int k0 = __builtin_ctz(q);
+    uint64_t x = 0;
+    for (int k = k0; k < 16; ++k) {
+        uint64_t r = orc_rand(key, w * 16 + (uint64_t)k);
+        x = ((q >> k) & 1) ? (x | r) : (x & r);
+    }
+    return x;
+}
+
+/* Words [w0, w0 + nw) of bitmap i, each bit Bernoulli(q16 / 2^16). */
+int orc_gen_bernoulli(uint64_t seed, uint32_t bitmap, uint32_t q16, uint64_t w0, uint64_t nw, uint64_t *out) {
+    const uint64_t key = orc_key(seed, bitmap);
+#pragma omp parallel for schedule(static) if (nw > (1u << 16))
+    for (int64_t k = 0; k < (int64_t)nw; ++k) out[k] = orc_bernoulli_word(key, w0 + (uint64_t)k, q16);
+    return ORC_OK;
+}
+
+/* Per-bitmap density lo + U * (hi - lo) in q16 units (U: 24 bits of the key). */
+uint32_t orc_gen_density_q16(uint64_t seed, uint32_t bitmap, uint32_t lo, uint32_t hi) {
+    uint64_t u = orc_mix(orc_key(seed, bitmap) ^ 0xD1B54A32D192ED03ull) >> 40;
+    return lo + (uint32_t)((u * (uint64_t)(hi - lo)) >> 24);
+}
+
+/* Geometric length >= 1 with the given mean, by inverting a 53-bit uniform in (0, 1]. */
+static uint64_t orc_geometric(uint64_t key, uint64_t ctr, double mean) {
+    if (mean <= 1.0) return 1;
+    double u = ((double)(orc_rand(key, ctr) >> 11) + 1.0) * (1.0 / 9007199254740992.0);
+    double l = floor(log(u) / log1p(-1.0 / mean));
+    if (l > 1e18) l = 1e18;
+    return 1 + (uint64_t)l;
+}
+
+/* C4 streams: alternating runs of zeros and ones with geometric lengths of the
+ * given means (bits), stationary start, encoded canonically with the RleBuilder
+ * above (bitmaps.py:351-404).  ORC_ERESOURCE if cap is too small; *out_len is
+ * the needed length either way. */
+int orc_gen_markov_rle(uint64_t seed, uint32_t bitmap, uint64_t r, double m1, double m0, uint64_t *out,
+                       uint64_t cap, uint64_t *out_len) {
+    if (m1 < 1.0 || m0 < 1.0) return ORC_EINPUT;
+    const uint64_t key = orc_key(seed ^ 0xC4C4C4C4ull, bitmap);
+    rle_builder b = {out, cap, 0, 0, 0, NULL, 0, 0, 0};
+    const double p1 = m1 / (m1 + m0);
+    uint64_t bit = ((double)(orc_rand(key, 0) >> 11) * (1.0 / 9007199254740992.0)) < p1 ? 1 : 0;
+    uint64_t pos = 0, cur = 0, ctr = 1;
+    int rc = ORC_OK;
+    while (pos < r && rc == ORC_OK) {
+        uint64_t len = orc_geometric(key, ctr++, bit ? m1 : m0);
+        if (len > r - pos) len = r - pos;
+        while (len && rc == ORC_OK) {
+            uint64_t off = pos & 63;
+            if (off == 0 && len >= 64) {
+                uint64_t nfull = len >> 6;
+                rb_append_fill(&b, bit, nfull);
+                pos += nfull << 6;
+                len -= nfull << 6;
+                continue;
+            }
+            uint64_t k = len < 64 - off ? len : 64 - off;
+            if (bit) cur |= (k == 64 ? ~0ull : ((1ull << k) - 1)) << off;
+            pos += k;
+            len -= k;
+            if ((pos & 63) == 0) {
+                rc = rb_append_word(&b, cur);
+                cur = 0;
+            }
+        }
+        bit ^= 1;
+    }
+    if (rc == ORC_OK && (pos & 63)) rc = rb_append_word(&b, cur);
+    if (rc == ORC_OK) rb_finish(&b);
+    free(b.dirty);
+    *out_len = b.len;
+    if (rc != ORC_OK) return rc;
+    return b.overflow ? ORC_ERESOURCE : ORC_OK;
+}

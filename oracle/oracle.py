@@ -67,9 +67,14 @@ def lib():
         L.orc_cdom_threshold.argtypes = [P, P, I, U64, I, P, P]
         L.orc_cdom_symmetric.argtypes = [P, P, I, U64, P, P, P]
         L.orc_num_threads.argtypes = []
+        L.orc_gen_bernoulli.argtypes = [U64, ctypes.c_uint32, ctypes.c_uint32, U64, U64, P]
+        L.orc_gen_density_q16.argtypes = [U64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+        L.orc_gen_density_q16.restype = ctypes.c_uint32
+        L.orc_gen_markov_rle.argtypes = [U64, ctypes.c_uint32, U64, ctypes.c_double, ctypes.c_double, P, U64, P]
         for name in ("orc_scan_count", "orc_scan_count_symmetric", "orc_threshold_port",
                      "orc_symmetric_port", "orc_rle_decompress", "orc_rle_compress",
-                     "orc_cdom_threshold", "orc_cdom_symmetric", "orc_num_threads"):
+                     "orc_cdom_threshold", "orc_cdom_symmetric", "orc_num_threads", "orc_gen_bernoulli",
+                     "orc_gen_markov_rle"):
             getattr(L, name).restype = I
         _lib = L
     return _lib
@@ -225,3 +230,33 @@ def trim(words: np.ndarray) -> np.ndarray:
     w = np.asarray(words, dtype=np.uint64)
     nz = np.flatnonzero(w)
     return w[: (nz[-1] + 1) if nz.size else 0]
+
+
+# ---------------------------------------------------------------------------
+# benchmark input generators (independent restatement of csrc/bq_gen.h; used by
+# bench.py's CPU legs so they never load libbq.so)
+
+def gen_bernoulli(seed: int, bitmap: int, q16: int, w0: int, nw: int) -> np.ndarray:
+    """Words [w0, w0 + nw) of bitmap ``bitmap``, each bit Bernoulli(q16 / 2^16)."""
+    out = np.empty(max(nw, 1), dtype=np.uint64)
+    _check(lib().orc_gen_bernoulli(seed, bitmap, q16, w0, nw, out.ctypes.data), "gen_bernoulli")
+    return out[:nw]
+
+
+def gen_density_q16(seed: int, bitmap: int, lo: int, hi: int) -> int:
+    return int(lib().orc_gen_density_q16(seed, bitmap, lo, hi))
+
+
+def gen_markov_rle(seed: int, bitmap: int, r: int, mean_one: float, mean_zero: float) -> np.ndarray:
+    """C4 stream: geometric one / zero runs of the given means, canonical RLE."""
+    cap = max(4096, r // 64 // 4)
+    while True:
+        out = np.empty(cap, dtype=np.uint64)
+        n = ctypes.c_uint64(0)
+        rc = lib().orc_gen_markov_rle(seed, bitmap, r, float(mean_one), float(mean_zero), out.ctypes.data, cap,
+                                      ctypes.byref(n))
+        if rc == ERESOURCE:
+            cap = int(n.value) + 16
+            continue
+        _check(rc, "gen_markov_rle")
+        return out[: n.value].copy()

@@ -66,3 +66,23 @@ def test_bench_without_gpu_fails_loudly():
     p = _run(["--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"], timeout=300)
     assert p.returncode != 0
     assert not _json_lines(p.stdout)
+
+
+def test_reference_arm_never_loads_the_product_library():
+    """The reference arm (and its input generation) runs on the oracle only: no
+    libbq.so in the process after a full run."""
+    code = ("import sys; sys.argv=['bench.py','--impl','reference','--steps','3','--warmup','3']; "
+            "sys.path.insert(0, %r); import bench; bench.main(); "
+            "maps=open('/proc/self/maps').read(); "
+            "assert 'libbq.so' not in maps, 'libbq.so loaded'; assert 'liboracle.so' in maps" % ROOT)
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600,
+                       env=dict(os.environ, OMP_NUM_THREADS="2"))
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert len(_json_lines(p.stdout)) == 1
+
+
+def test_reference_arm_gpus_flag_reports_world():
+    p = _run(["--impl", "reference", "--gpus", "4", "--steps", "3", "--warmup", "3"])
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 4

@@ -44,6 +44,9 @@ def test_default_line_contract():
     c = d["cpu_baseline"]
     assert c["value"] > 0 and c["cores"] >= 1 and c["kind"] == "port"
     assert "workload" in d["config"] and "sm_mhz" in d["clocks"]
+    c5 = d["c5_strong_scaling"]
+    assert c5["scaling"] == "strong" and c5["n_gpus"] == 1 and c5["waves_per_rank"] == 8
+    assert c5["value"] > 0 and c5["input_bytes"] == 511 * (1 << 26) * 8 and c5["popcount"] > 0
 
 
 def test_c4_line_contract():
@@ -80,3 +83,22 @@ def test_two_ranks_under_torchrun(workload):
         assert d["e2e"]["matches_device_result"]
     else:
         assert d["matches_oracle_window"] and d["popcount"] > 0
+
+
+def test_gpus_flag_launches_its_own_ranks():
+    """``bench.py --gpus 2`` outside torchrun starts two ranks itself (here sharing
+    the one GPU over gloo: a functional check, not a measurement) and rank 0 prints
+    one line with n_gpus = 2, including the C5 strong-scaling fields."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, BQ_BENCH_BACKEND="gloo", BQ_BENCH_SHARE_GPU="1", OMP_NUM_THREADS="2")
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup",
+                        "3", "--e2e-steps", "1"], capture_output=True, text=True, cwd=ROOT, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["matches_device_result"]
+    c5 = d["c5_strong_scaling"]
+    assert c5["n_gpus"] == 2 and c5["waves_per_rank"] == 4 and c5["input_bytes"] == 511 * (1 << 26) * 8

@@ -85,3 +85,34 @@ def test_complement_identity():
         rhs = ~O.scan_count(neg, r, n - t + 1)
         rhs[-1] &= mask
         assert np.array_equal(lhs, rhs)
+
+
+def test_oracle_generator_matches_pin():
+    """The oracle's generator restatement (bench.py's CPU legs use it instead of
+    libbq.so) reproduces the independent pure-Python KATs."""
+    kat = load_kat()["generator"]
+    for c in kat["cases"]:
+        got = O.gen_bernoulli(kat["seed"], c["bitmap"], c["q"], c["word"], 1)
+        assert int(got[0]) == int(c["value"])
+    assert [O.gen_density_q16(kat["seed"], i, 655, 32768) for i in range(64)] == kat["density_q"]
+
+
+def test_oracle_generator_matches_product_generator():
+    """Same words as csrc/bq_gen.h (Bernoulli windows) and bq_gen_markov_rle (C4 streams)."""
+    import ctypes
+
+    from paper_1402_4073_b200 import _lib
+
+    lib = _lib.load()
+    for i in (0, 9, 63):
+        q = lib.bq_gen_density_q16(1402, i, 655, 32768)
+        a = np.empty(777, dtype=np.uint64)
+        assert lib.bq_gen_bernoulli(1402, i, q, 99991, 777, a.ctypes.data, 0, None) == 0
+        assert np.array_equal(a, O.gen_bernoulli(1402, i, q, 99991, 777))
+    r = (1 << 21) + 37
+    for i in (0, 3):
+        cap = 1 << 16
+        buf = np.empty(cap, dtype=np.uint64)
+        n = ctypes.c_uint64(0)
+        assert lib.bq_gen_markov_rle(1402, i, r, 256.0, 12544.0, buf.ctypes.data, cap, ctypes.byref(n)) == 0
+        assert np.array_equal(buf[: n.value], O.gen_markov_rle(1402, i, r, 256.0, 12544.0))
