@@ -109,15 +109,28 @@ class _QueryCache:
     directory) keyed by the identities of their input objects.  Bitmaps are
     immutable after construction (reference bitmaps.py:12-13), so a query stays
     valid as long as its inputs live; entries hold strong references to them so
-    ids cannot be reused.  LRU-bounded."""
+    ids cannot be reused.  LRU-bounded by entry count and by the device bytes of
+    the uploaded host inputs the cached queries keep alive (the upload cache's
+    bound, BQ_UPLOAD_CACHE_BYTES): a query holds its inputs' device copies, so
+    without the second bound evicted uploads would outlive the upload cache."""
 
-    def __init__(self, maxsize: int = 32):
+    def __init__(self, maxsize: int = 32, max_bytes: int | None = None):
         from collections import OrderedDict
         import threading
 
         self.maxsize = maxsize
+        self._max_bytes = max_bytes
         self._d = OrderedDict()
+        self._bytes = 0
         self._lock = threading.Lock()
+
+    @property
+    def max_bytes(self) -> int:
+        return UPLOADS.max_bytes if self._max_bytes is None else self._max_bytes
+
+    @property
+    def held_bytes(self) -> int:
+        return self._bytes
 
     def get(self, kind: str, bitmaps, r: int, device):
         key = (kind, tuple(id(b) for b in bitmaps), r, device.index)
@@ -128,15 +141,27 @@ class _QueryCache:
                 return hit[1]
         dev = _dev_inputs(bitmaps, device)
         q = ThresholdQuery(dev, r, device=device) if kind == "u" else RleQuery(dev, r, device=device)
+        # device bytes of uploaded host inputs (device-resident inputs belong to the caller)
+        seen, nbytes = set(), 0
+        for b, d in zip(bitmaps, dev):
+            if kind_of(b) in ("u", "r") and id(d.data) not in seen:
+                seen.add(id(d.data))
+                nbytes += d.data.numel() * 8
         with self._lock:
-            self._d[key] = (list(bitmaps), q)
-            while len(self._d) > self.maxsize:
-                self._d.popitem(last=False)
+            old = self._d.pop(key, None)
+            if old is not None:
+                self._bytes -= old[2]
+            self._d[key] = (list(bitmaps), q, nbytes)
+            self._bytes += nbytes
+            while self._d and (len(self._d) > self.maxsize or (self._bytes > self.max_bytes and len(self._d) > 1)):
+                _, (_, _, nb) = self._d.popitem(last=False)
+                self._bytes -= nb
         return q
 
     def clear(self):
         with self._lock:
             self._d.clear()
+            self._bytes = 0
 
 
 QUERIES = _QueryCache()

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -82,9 +83,54 @@ cudaError_t pool_alloc(void **p, size_t bytes) {
 
 void pool_free(void *p) {
     if (!p) return;
-    cudaDeviceSynchronize();  // no evaluation may still be reading it (cudaFree's implicit sync)
     if (cudaFreeAsync(p, 0) != cudaSuccess) cudaGetLastError();
-    cudaStreamSynchronize(0);
+}
+
+void StreamUses::note(cudaStream_t s) {
+    for (int i = 0; i < n; ++i)
+        if (streams[i] == s) {
+            cudaEventRecord(events[i], s);
+            return;
+        }
+    if (n == kMax) {
+        overflow = true;
+        return;
+    }
+    if (cudaEventCreateWithFlags(&events[n], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        overflow = true;
+        return;
+    }
+    streams[n] = s;
+    cudaEventRecord(events[n], s);
+    ++n;
+}
+
+void StreamUses::release() {
+    for (int i = 0; i < n; ++i) cudaEventDestroy(events[i]);
+    n = 0;
+}
+
+static cudaStream_t free_stream() {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 0;
+    std::lock_guard<std::mutex> g(mu);
+    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        streams[dev] = 0;
+    }
+    return streams[dev];
+}
+
+void pool_free_after(void *p, const StreamUses &uses) {
+    if (!p) return;
+    if (uses.overflow) cudaDeviceSynchronize();
+    cudaStream_t fs = free_stream();
+    for (int i = 0; i < uses.n; ++i) cudaStreamWaitEvent(fs, uses.events[i], 0);
+    if (cudaFreeAsync(p, fs) != cudaSuccess) cudaGetLastError();
 }
 
 int sm_count() {
@@ -171,6 +217,10 @@ struct bq_query {
     const uint64_t **d_ptrs;
     uint64_t *d_lens;
     std::vector<const uint64_t *> h_ptrs;  // host copy (small N: passed by value to the kernel)
+    // device LUTs of MODE_LUT symmetric specs, uploaded once per distinct table
+    std::map<std::vector<uint32_t>, void *> luts;
+    StreamUses uses;  // caller streams that evaluated this query (destroy waits on them)
+    std::mutex mu;    // guards luts / uses
 };
 
 extern "C" {
@@ -202,7 +252,8 @@ BQ_API int bq_query_create(const bq_span *inputs, int n, uint64_t r_bits, uint64
         return set_error(BQ_EINPUT, "word range [%llu, %llu) outside [0, %llu)", (unsigned long long)w_begin,
                          (unsigned long long)w_end, (unsigned long long)total);
     if (w_begin & 1) return set_error(BQ_EINPUT, "w_begin must be even");
-    int rc = use_device(device);
+    DeviceGuard dg;
+    int rc = dg.set(device);
     if (rc) return rc;
     const uint64_t nwords = w_end - w_begin;
     std::vector<const uint64_t *> ptrs(n);
@@ -232,17 +283,19 @@ BQ_API int bq_query_create(const bq_span *inputs, int n, uint64_t r_bits, uint64
     q->full_words = full;
     q->last_mask = (w_end == total && (r_bits % W)) ? ((1ull << (r_bits % W)) - 1) : ~0ull;
     void *buf = nullptr;
-    cudaError_t e = cudaMalloc(&buf, (size_t)n * 16);
+    cudaError_t e = pool_alloc(&buf, (size_t)n * 16);
     if (e != cudaSuccess) {
         delete q;
         return cuda_error(e, "cudaMalloc(query table)");
     }
     q->d_ptrs = reinterpret_cast<const uint64_t **>(buf);
     q->d_lens = reinterpret_cast<uint64_t *>(static_cast<char *>(buf) + (size_t)n * 8);
-    e = cudaMemcpy(q->d_ptrs, ptrs.data(), (size_t)n * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(q->d_lens, lens.data(), (size_t)n * 8, cudaMemcpyHostToDevice);
+    // the tables are complete before any stream (including non-blocking ones) can use them
+    e = cudaMemcpyAsync(q->d_ptrs, ptrs.data(), (size_t)n * 8, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(q->d_lens, lens.data(), (size_t)n * 8, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) {
-        cudaFree(buf);
+        pool_free(buf);
         delete q;
         return cuda_error(e, "cudaMemcpy(query table)");
     }
@@ -253,8 +306,11 @@ BQ_API int bq_query_create(const bq_span *inputs, int n, uint64_t r_bits, uint64
 
 BQ_API void bq_query_destroy(bq_query *q) {
     if (!q) return;
-    if (q->device >= 0) cudaSetDevice(q->device);
-    cudaFree(q->d_ptrs);
+    DeviceGuard dg;
+    dg.set(q->device);
+    pool_free_after(q->d_ptrs, q->uses);  // after the evaluations enqueued so far; no device sync
+    for (auto &kv : q->luts) pool_free_after(kv.second, q->uses);
+    q->uses.release();
     delete q;
 }
 
@@ -296,7 +352,12 @@ static int base_args(bq_query *q, uint64_t *d_out, unsigned long long *d_popcnt,
     a.out = d_out;
     a.popcnt = d_popcnt;
     a.last_nz = d_last_nz;
-    return use_device(q->device);
+    return BQ_OK;
+}
+
+static void note_use(bq_query *q, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(q->mu);
+    q->uses.note(s);
 }
 
 BQ_API int bq_query_threshold(bq_query *q, int t, uint64_t *d_out, unsigned long long *d_popcnt,
@@ -305,6 +366,8 @@ BQ_API int bq_query_threshold(bq_query *q, int t, uint64_t *d_out, unsigned long
     int rc = base_args(q, d_out, d_popcnt, d_last_nz, a);
     if (rc) return rc;
     if (t < 1 || t > q->n) return set_error(BQ_EINPUT, "threshold %d outside [1, %d]", t, q->n);  // counters.py:40-43
+    DeviceGuard dg;
+    if ((rc = dg.set(q->device))) return rc;
     int mode;
     if (t == 1) mode = MODE_OR;
     else if (t == q->n) mode = MODE_AND;
@@ -314,7 +377,9 @@ BQ_API int bq_query_threshold(bq_query *q, int t, uint64_t *d_out, unsigned long
         a.nbreak = 1;
         a.breaks[0] = (uint32_t)t;
     }
-    return launch_count(a, q->m, mode, static_cast<cudaStream_t>(stream));
+    rc = launch_count(a, q->m, mode, static_cast<cudaStream_t>(stream));
+    if (rc == BQ_OK) note_use(q, static_cast<cudaStream_t>(stream));
+    return rc;
 }
 
 BQ_API int bq_query_symmetric(bq_query *q, const uint8_t *h_accept, uint64_t *d_out,
@@ -323,22 +388,56 @@ BQ_API int bq_query_symmetric(bq_query *q, const uint8_t *h_accept, uint64_t *d_
     int rc = base_args(q, d_out, d_popcnt, d_last_nz, a);
     if (rc) return rc;
     if (!h_accept) return set_error(BQ_EINPUT, "accept vector is NULL");
+    DeviceGuard dg;
+    if ((rc = dg.set(q->device))) return rc;
     AcceptPlan p;
     plan_accept(h_accept, q->n, p);
     a.accept0 = p.accept0;
     a.nbreak = p.nbreak;
     memcpy(a.breaks, p.breaks, sizeof(uint32_t) * (size_t)p.nbreak);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (p.mode == MODE_BREAK) return launch_count(a, p.m, MODE_BREAK, s);
-    void *d_lut = nullptr;
-    size_t bytes = p.lut.size() * 4;
-    cudaError_t e = cudaMallocAsync(&d_lut, bytes, s);
-    if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(lut)");
-    e = cudaMemcpyAsync(d_lut, p.lut.data(), bytes, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync(lut)");
-    a.lut = static_cast<const uint32_t *>(d_lut);
-    rc = launch_count(a, p.m, MODE_LUT, s);
-    cudaFreeAsync(d_lut, s);
+    if (p.mode == MODE_LUT) {
+        // the table of each distinct spec is uploaded once per query (repeated
+        // evaluations: no allocation or copy), complete before any stream reads it
+        constexpr size_t kMaxLuts = 64;
+        void *d_lut = nullptr;
+        bool owned = false;
+        {
+            std::lock_guard<std::mutex> g(q->mu);
+            auto it = q->luts.find(p.lut);
+            if (it != q->luts.end()) d_lut = it->second;
+            else if (q->luts.size() >= kMaxLuts) owned = true;
+        }
+        if (!d_lut) {
+            const size_t bytes = p.lut.size() * 4;
+            cudaError_t e = pool_alloc(&d_lut, bytes);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(d_lut, p.lut.data(), bytes, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) {
+                if (d_lut) pool_free(d_lut);
+                return cuda_error(e, "lut upload");
+            }
+            if (!owned) {
+                std::lock_guard<std::mutex> g(q->mu);
+                auto ins = q->luts.emplace(p.lut, d_lut);
+                if (!ins.second) {  // another thread uploaded the same table meanwhile
+                    pool_free(d_lut);
+                    d_lut = ins.first->second;
+                }
+            }
+        }
+        a.lut = static_cast<const uint32_t *>(d_lut);
+        rc = launch_count(a, p.m, MODE_LUT, s);
+        if (owned) {
+            StreamUses once;
+            once.note(s);
+            pool_free_after(d_lut, once);
+            once.release();
+        }
+    } else {
+        rc = launch_count(a, p.m, MODE_BREAK, s);
+    }
+    if (rc == BQ_OK) note_use(q, s);
     return rc;
 }
 
@@ -418,7 +517,8 @@ BQ_API int bq_sweep_host(const uint64_t *const *h_inputs, const uint64_t *n_word
     }
     int dev = device;
     if (dev < 0) cudaGetDevice(&dev);
-    int rc = use_device(dev);
+    DeviceGuard dg;
+    int rc = dg.set(dev);
     if (rc) return rc;
     if (dev >= 64) return set_error(BQ_EINPUT, "device ordinal too large");
     SweepWorkspace &ws = g_sweep[dev];
@@ -490,6 +590,9 @@ BQ_API int bq_sweep_host(const uint64_t *const *h_inputs, const uint64_t *n_word
         if (modes[k] == MODE_LUT)
             BQ_CUDA_TRY(cudaMemcpy(d_lut + lut_off[k], plans[k].lut.data(), plans[k].lut.size() * 4,
                                    cudaMemcpyHostToDevice));
+    // pageable copies may return before their DMA lands, and s_comp does not order
+    // after the legacy stream: wait for the tables before the kernels read them
+    BQ_CUDA_TRY(cudaStreamSynchronize(0));
     BQ_CUDA_TRY(cudaMemsetAsync(d_pop, 0, (size_t)nq * 8, ws.s_comp));
 
     // rows of one strided host array (the common layout) allow 2-D copies

@@ -26,10 +26,48 @@ int cuda_error(cudaError_t e, const char *what);
     } while (0)
 
 int use_device(int device);  // cudaSetDevice when device >= 0
+// Makes `device` current for a scope and restores the caller's current device at
+// exit, so a call (or a GC-triggered destroy) never changes the device the caller
+// -- e.g. torch -- had selected.
+struct DeviceGuard {
+    int prev = -1;
+    int set(int device) {
+        if (device < 0) return BQ_OK;
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess) {
+            cudaGetLastError();
+            cur = -1;
+        }
+        if (cur == device) return BQ_OK;
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+        prev = cur;
+        return BQ_OK;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 // The library's stream-ordered memory pool (query directories, tile-sliced layouts
 // and their build scratch): freed blocks are kept for the next query.
 cudaError_t pool_alloc(void **p, size_t bytes);
+// Free into the pool in legacy-stream order (no host synchronisation): for memory
+// that only legacy-stream work (the synchronous builds) has used.
 void pool_free(void *p);
+// Evaluations on caller streams that a query's memory must outlive: one event per
+// stream, re-recorded after each launch; freeing waits on them on a library stream
+// instead of synchronising the device.
+struct StreamUses {
+    static constexpr int kMax = 16;
+    cudaStream_t streams[kMax];
+    cudaEvent_t events[kMax];
+    int n = 0;
+    bool overflow = false;  // more streams than tracked: free after a device sync
+    void note(cudaStream_t s);
+    void release();  // destroys the events (call after the frees were enqueued)
+};
+// Free `p` once every evaluation noted in `uses` is done, without a host sync.
+void pool_free_after(void *p, const StreamUses &uses);
 int sm_count();              // SMs of the current device
 
 // ---- K1/K2: uncompressed counting kernel ------------------------------------
@@ -119,7 +157,7 @@ struct SlicedLayout {
 // tiles [tile0, tile0 + ntiles) of the streams; directory rows are relative to tile0
 int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n, uint32_t tile0,
                  uint32_t ntiles, SlicedLayout *out);
-void free_sliced(SlicedLayout *l);
+void free_sliced(SlicedLayout *l, const StreamUses *uses = nullptr);
 struct SlicedEval {
     int n;
     uint64_t total_words;

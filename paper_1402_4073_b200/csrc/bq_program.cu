@@ -21,6 +21,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -150,9 +151,36 @@ using namespace bq;
 struct bq_program {
     int arity, n_slots, result_slot, n_ins;
     std::string source;
-    CUmodule_t module = nullptr;
-    CUfunction_t fn = nullptr;
+    std::vector<char> cubin;
+    // the module is loaded into each device's primary context on first use there: a
+    // function handle from one context cannot be launched in another
+    std::map<int, std::pair<CUmodule_t, CUfunction_t>> per_device;
+    std::mutex mu;
 };
+
+// The program's kernel in the current device's context (loaded on first use).
+static int program_function(bq_program *p, CUfunction_t *fn) {
+    int dev = 0;
+    cudaError_t ce = cudaGetDevice(&dev);
+    if (ce != cudaSuccess) return cuda_error(ce, "cudaGetDevice");
+    std::lock_guard<std::mutex> g(p->mu);
+    auto it = p->per_device.find(dev);
+    if (it != p->per_device.end()) {
+        *fn = it->second.second;
+        return BQ_OK;
+    }
+    cudaFree(0);  // make sure the device's primary context is current for the driver API
+    Jit &j = jit();
+    CUmodule_t mod = nullptr;
+    CUfunction_t f = nullptr;
+    if (j.cuModuleLoadData(&mod, p->cubin.data()) != 0 || j.cuModuleGetFunction(&f, mod, "bq_prog") != 0) {
+        if (mod) j.cuModuleUnload(mod);
+        return set_error(BQ_ECUDA, "cuModuleLoadData/cuModuleGetFunction failed on device %d", dev);
+    }
+    p->per_device.emplace(dev, std::make_pair(mod, f));
+    *fn = f;
+    return BQ_OK;
+}
 
 // Layout of bq_query needed here (defined in bq_api.cu): the public accessor is enough.
 extern "C" {
@@ -199,13 +227,13 @@ BQ_API int bq_program_compile(const int32_t *instr, int n_instr, int arity, int 
     }
     size_t n = 0;
     j.nvrtcGetCUBINSize(prog, &n);
-    std::vector<char> cubin(n);
-    j.nvrtcGetCUBIN(prog, cubin.data());
+    p->cubin.resize(n);
+    j.nvrtcGetCUBIN(prog, p->cubin.data());
     j.nvrtcDestroyProgram(&prog);
-    if (j.cuModuleLoadData(&p->module, cubin.data()) != 0 || j.cuModuleGetFunction(&p->fn, p->module, "bq_prog") != 0) {
-        if (p->module) j.cuModuleUnload(p->module);
+    CUfunction_t fn = nullptr;  // load (and so validate) the module on the current device now
+    if (int rc2 = program_function(p, &fn)) {
         delete p;
-        return set_error(BQ_ECUDA, "cuModuleLoadData/cuModuleGetFunction failed");
+        return rc2;
     }
     *out = p;
     return BQ_OK;
@@ -213,7 +241,16 @@ BQ_API int bq_program_compile(const int32_t *instr, int n_instr, int arity, int 
 
 BQ_API void bq_program_destroy(bq_program *p) {
     if (!p) return;
-    if (p->module && jit().ok) jit().cuModuleUnload(p->module);
+    if (jit().ok) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        for (auto &kv : p->per_device) {  // unload in each module's own context
+            cudaSetDevice(kv.first);
+            cudaFree(0);
+            jit().cuModuleUnload(kv.second.first);
+        }
+        if (prev >= 0) cudaSetDevice(prev);
+    }
     delete p;
 }
 
@@ -248,15 +285,17 @@ extern "C" BQ_API int bq_program_execute(bq_program *p, bq_query *q, uint64_t *d
     if (n != p->arity) return set_error(BQ_EINPUT, "program expects %d inputs, got %d", p->arity, n);  // programs.py:241-242
     if (nwords && !d_out) return set_error(BQ_EINPUT, "d_out is NULL");
     if (!nwords) return BQ_OK;
-    rc = use_device(device);
-    if (rc) return rc;
+    DeviceGuard dg;
+    if ((rc = dg.set(device))) return rc;
+    CUfunction_t fn = nullptr;
+    if ((rc = program_function(p, &fn))) return rc;
     const unsigned threads = 256;
     uint64_t grid = (nwords + threads - 1) / threads;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     if (grid > cap) grid = cap;
     void *args[] = {(void *)&ptrs, (void *)&lens, (void *)&nwords, (void *)&full, (void *)&last_mask,
                     (void *)&d_out, (void *)&d_popcnt, (void *)&d_last_nz};
-    const int r = jit().cuLaunchKernel(p->fn, (unsigned)grid, 1, 1, threads, 1, 1, 0, stream, args, nullptr);
+    const int r = jit().cuLaunchKernel(fn, (unsigned)grid, 1, 1, threads, 1, 1, 0, stream, args, nullptr);
     if (r != 0) return set_error(BQ_ECUDA, "cuLaunchKernel(bq_prog) failed (CUresult %d)", r);
     return BQ_OK;
 }

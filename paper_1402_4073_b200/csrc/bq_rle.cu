@@ -567,8 +567,34 @@ struct bq_rle_query {
     // device accept / const_until / breakpoint tables by accept vector: immutable once
     // uploaded, so repeated evaluations (same T) need no allocation or copy
     std::map<std::vector<uint8_t>, void *> tables;
-    mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced / tables
+    StreamUses uses;              // caller streams that evaluated this query (destroy waits on them)
+    mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced / tables / uses
 };
+
+// Validation of streams over a bit_length-0 universe (host walk; valid streams
+// hold only empty markers, so they are short in practice).
+static int validate_empty_universe(const std::vector<const uint64_t *> &ptrs, const std::vector<uint64_t> &lens) {
+    for (size_t i = 0; i < ptrs.size(); ++i) {
+        if (!lens[i]) continue;
+        std::vector<uint64_t> h(lens[i]);
+        cudaError_t e = cudaMemcpy(h.data(), ptrs[i], lens[i] * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_error(e, "stream copy");
+        uint64_t k = 0, covered = 0;
+        while (k < h.size()) {
+            const uint64_t run = (h[k] >> 1) & 0xFFFFFFFFull, dirty = h[k] >> 33;
+            ++k;
+            covered += run;
+            if (dirty) {
+                if (k + dirty > h.size())
+                    return set_error(BQ_EFORMAT, "stream %zu: marker announces more literal words than present", i);
+                k += dirty;
+                covered += dirty;
+            }
+        }
+        if (covered) return set_error(BQ_EFORMAT, "stream %zu: encoded words exceed bit_length", i);
+    }
+    return BQ_OK;
+}
 
 extern "C" {
 
@@ -597,7 +623,8 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
                                           (unsigned long long)w_begin, (unsigned long long)w_end);
     if (w_begin % kRleTile || (w_end % kRleTile && w_end != total))
         return set_error(BQ_EINPUT, "RLE word range bounds must be multiples of %d words (or the end)", kRleTile);
-    int rc = use_device(device);
+    DeviceGuard dg;
+    int rc = dg.set(device);
     if (rc) return rc;
     const uint32_t tile0 = (uint32_t)(w_begin / kRleTile);
     const uint32_t ntiles = (uint32_t)((w_end - w_begin + kRleTile - 1) / kRleTile);
@@ -697,6 +724,16 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
                 return set_error(BQ_EFORMAT, "stream %llu: set bits at positions >= bit_length", bad);
             return set_error(BQ_EFORMAT, "stream %llu: encoded words exceed bit_length", bad);
         }
+    } else {
+        // bit_length 0: no directory, but the streams are still validated as
+        // iter_word_segments would (bitmaps.py:196-219): a truncated literal group, or
+        // any fill / literal coverage at all (> 0 words), is a FormatError
+        rc = validate_empty_universe(ptrs, lens);
+        if (rc) {
+            pool_free(q->mem);
+            delete q;
+            return rc;
+        }
     }
     *out = q;
     return BQ_OK;
@@ -704,10 +741,14 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
 
 BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     if (!q) return;
-    if (q->device >= 0) cudaSetDevice(q->device);
-    pool_free(q->mem);
-    free_sliced(&q->sliced);
-    for (auto &kv : q->tables) pool_free(kv.second);
+    DeviceGuard dg;
+    dg.set(q->device);
+    // stream-ordered: the memory returns to the pool once the evaluations already
+    // enqueued on the caller's streams are done; no device-wide synchronisation
+    pool_free_after(q->mem, q->uses);
+    free_sliced(&q->sliced, &q->uses);
+    for (auto &kv : q->tables) pool_free_after(kv.second, q->uses);
+    q->uses.release();
     delete q;
 }
 
@@ -734,11 +775,18 @@ BQ_API int bq_rle_query_layout_events(const bq_rle_query *q, uint64_t *n_events)
     return BQ_OK;
 }
 
+static void note_use(bq_rle_query *q, cudaStream_t s) {
+    std::lock_guard<std::mutex> guard(q->build_mu);
+    q->uses.note(s);
+}
+
 static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *d_out, unsigned long long *d_popcnt,
                     void *stream) {
     if (!q) return set_error(BQ_EINPUT, "query is NULL");
     if (q->ntiles && !d_out) return set_error(BQ_EINPUT, "d_out is NULL");
-    int rc = use_device(q->device);
+    if (reinterpret_cast<uintptr_t>(d_out) & 15) return set_error(BQ_EINPUT, "d_out must be 16-byte aligned");
+    DeviceGuard dg;
+    int rc = dg.set(q->device);
     if (rc) return rc;
     if (!q->ntiles) return BQ_OK;
     const int n = q->n;
@@ -771,7 +819,10 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
             d_tab = it->second;
         } else if (q->tables.size() < kMaxTables) {
             e = pool_alloc(reinterpret_cast<void **>(&d_tab), bytes);
-            if (e == cudaSuccess) e = cudaMemcpy(d_tab, host.data(), bytes, cudaMemcpyHostToDevice);
+            // ordered on the consuming stream, and complete before the table is shared
+            // with evaluations on other streams
+            if (e == cudaSuccess) e = cudaMemcpyAsync(d_tab, host.data(), bytes, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) {
                 if (d_tab) pool_free(d_tab);
                 return cuda_error(e, "accept table upload");
@@ -852,6 +903,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         se.debug = a.debug;
         rc = launch_sliced(sliced, se, s);
         release();
+        if (rc == BQ_OK) note_use(q, s);
         return rc;
     } else {
         e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -864,6 +916,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     e = cudaGetLastError();
     release();
     if (e != cudaSuccess) return cuda_error(e, "rle_count_kernel launch");
+    note_use(q, s);
     return BQ_OK;
 }
 

@@ -831,8 +831,13 @@ int build_sliced(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const ui
     return BQ_OK;
 }
 
-void free_sliced(SlicedLayout *l) {
-    if (l->mem) pool_free(l->mem);
+void free_sliced(SlicedLayout *l, const StreamUses *uses) {
+    if (l->mem) {
+        if (uses)
+            pool_free_after(l->mem, *uses);
+        else
+            pool_free(l->mem);
+    }
     *l = SlicedLayout();
 }
 

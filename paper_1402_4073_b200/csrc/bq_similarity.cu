@@ -67,7 +67,8 @@ static int membership(const Span *items, int m, const uint64_t *h_rids, int nr, 
     if (!m || !nr) return BQ_OK;
     for (int j = 1; j < nr && rle; ++j)
         if (h_rids[j] < h_rids[j - 1]) return set_error(BQ_EINPUT, "rids must be ascending");
-    int rc = use_device(device);
+    DeviceGuard dg;
+    int rc = dg.set(device);
     if (rc) return rc;
     std::vector<const uint64_t *> ptrs(m);
     std::vector<uint64_t> lens(m);

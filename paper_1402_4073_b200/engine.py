@@ -94,6 +94,20 @@ class UploadCache:
 UPLOADS = UploadCache()
 
 
+def _check_out(out, out_words: int, device) -> None:
+    """A caller-supplied result buffer: on the query's device, 64-bit words,
+    contiguous, at least ``out_words`` long and 16-byte aligned (the kernels store
+    128-bit vectors; include/bq.h)."""
+    if not isinstance(out, torch.Tensor) or not out.is_cuda or out.device != device:
+        raise InputError(f"output tensor must be a CUDA tensor on {device}")
+    if out.dtype not in (torch.int64, torch.uint64) or not out.is_contiguous():
+        raise InputError("output tensor must be a contiguous int64/uint64 tensor")
+    if out.numel() < out_words:
+        raise InputError(f"output tensor holds {out.numel()} words, the result needs {out_words}")
+    if out.data_ptr() % 16:
+        raise InputError("output tensor must be 16-byte aligned")
+
+
 class ThresholdQuery:
     """A prepared query (``bq_query``) over N device-resident uncompressed inputs.
 
@@ -142,8 +156,8 @@ class ThresholdQuery:
     def _outs(self, out, popcnt, last_nz):
         if out is None:
             out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)
-        elif out.numel() < self.out_words or not out.is_cuda:
-            raise InputError("output tensor too small or not on the device")
+        else:
+            _check_out(out, self.out_words, self.device)
         if popcnt is None:
             popcnt = torch.zeros(1, dtype=torch.int64, device=self.device)
         return out, popcnt, last_nz
@@ -232,6 +246,8 @@ class RleQuery:
     def _outs(self, out, popcnt):
         if out is None:
             out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)
+        else:
+            _check_out(out, self.out_words, self.device)
         if popcnt is None:
             popcnt = torch.zeros(1, dtype=torch.int64, device=self.device)
         return out, popcnt
