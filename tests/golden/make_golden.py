@@ -477,7 +477,125 @@ def kat():
     print(path)
 
 
+# ---------------------------------------------------------------------------
+# BASELINE.json configs, pinned to the reference itself (SURVEY §8(c) protocol,
+# steps 1-3): the exact seeded inputs the GPU tests and bench.py use (the K5
+# Bernoulli generator; the C4 Markov streams), run through the reference's own
+# algorithms.  Inputs are not stored: they regenerate bit-exactly from
+# (seed, bitmap, word window) through the generator, which kat.json pins.  Only
+# the reference's outputs (and popcounts) are committed, in baseline.npz.
+
+SEED = 1402
+C2_DENS = (655, 32768)
+
+
+def _gen_rows(n, q16s, w0, nw):
+    """Input words of bitmaps 0..n-1, words [w0, w0 + nw), via the oracle's C
+    restatement of the generator (checked here against the pure-Python statement
+    above on a sample, so the reference sees exactly the pinned generator's words)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from oracle import oracle as O
+
+    rows = [O.gen_bernoulli(SEED, i, int(q16s[i]), w0, nw) for i in range(n)]
+    for i in (0, n - 1):
+        key = bitmap_key(SEED, i)
+        for k in (0, nw - 1):
+            assert int(rows[i][k]) == bernoulli_word(key, w0 + k, int(q16s[i]))
+    return rows
+
+
+def _ub(words, r):
+    return bm.UncompressedBitmap([int(w) for w in words], r)
+
+
+def baseline_cases():
+    out = {}
+    meta = {}
+
+    def put(name, words, info):
+        out[name] = np.asarray(words, dtype=np.uint64)
+        meta[name] = info
+
+    def padded(res, nw):
+        w = np.zeros(nw, dtype=np.uint64)
+        w[: len(res.words)] = np.asarray(res.words, dtype=np.uint64)
+        return w
+
+    # C1 in full: N=8, r=2^20, p=0.1 (q=6554), T=3
+    n, nw, t = 8, 1 << 14, 3
+    ins = [_ub(r, 64 * nw) for r in _gen_rows(n, [6554] * n, 0, nw)]
+    res = counters.scan_count(ins, t)
+    assert looped_threshold(ins, t) == res and csv_threshold(ins, t) == res
+    put("c1_t3", padded(res, nw), {"n": n, "w0": 0, "nw": nw, "t": t, "q16": 6554, "card": res.cardinality()})
+    print("C1 done", res.cardinality())
+
+    # C2 windows of 2^12 words x 64 bitmaps (first, middle, last window of the 2^22), every T
+    n, nw = 64, 1 << 12
+    q16 = [density_q(SEED, i) for i in range(n)]
+    for w0 in (0, 1 << 21, (1 << 22) - nw):
+        ins = [_ub(r, 64 * nw) for r in _gen_rows(n, q16, w0, nw)]
+        for t in (1, 2, 16, 32, 64):
+            res = counters.scan_count(ins, t)
+            assert looped_threshold(ins, t) == res
+            if 2 <= t < n:
+                assert csv_threshold(ins, t) == res
+            if t == 1:
+                assert bm.wide_or(ins) == res
+            if t == n:
+                assert bm.wide_and(ins) == res
+            if w0 == 0 and t in (2, 32):
+                assert CircuitLibrary(n_max=64, builder="sideways").threshold(ins, t) == res
+            put(f"c2_w{w0}_t{t}", padded(res, nw), {"n": n, "w0": w0, "nw": nw, "t": t, "q16": q16,
+                                                      "card": res.cardinality()})
+        print("C2 window", w0, "done")
+
+    # C3 windows: N=256, p=0.05 (q=3277), accept = [2 <= count <= 10], first and last 2^12 words
+    n, nw = 256, 1 << 12
+    spec = oracle.SymmetricSpec.interval(n, 2, 10)
+    for w0 in (0, (1 << 20) - nw):
+        ins = [_ub(r, 64 * nw) for r in _gen_rows(n, [3277] * n, w0, nw)]
+        res = counters.scan_count_symmetric(ins, spec)
+        put(f"c3_w{w0}", padded(res, nw), {"n": n, "w0": w0, "nw": nw, "accept": "interval(256,2,10)",
+                                            "q16": 3277, "card": res.cardinality()})
+        print("C3 window", w0, "done")
+
+    # C5 windows: N=511, p=0.5 (q=32768), T=256, first and last 2^10 words of 2^26
+    n, nw, t = 511, 1 << 10, 256
+    for w0 in (0, (1 << 26) - nw):
+        ins = [_ub(r, 64 * nw) for r in _gen_rows(n, [32768] * n, w0, nw)]
+        res = csv_threshold(ins, t)
+        if w0 == 0:
+            assert counters.scan_count(ins, t) == res
+        put(f"c5_w{w0}_t{t}", padded(res, nw), {"n": n, "w0": w0, "nw": nw, "t": t, "q16": 32768,
+                                                 "card": res.cardinality()})
+        print("C5 window", w0, "done")
+
+    # C4: the Markov streams over the first 2^20 bits (a prefix of the full 2^30-bit
+    # streams: the generator is sequential), reference RleBitmap -> cdom_threshold
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from oracle import oracle as O
+
+    n, r = 1024, 1 << 20
+    streams = [O.gen_markov_rle(SEED, i, r, 256.0, 12544.0) for i in range(n)]
+    comp = [bm.RleBitmap([int(w) for w in s], r) for s in streams]
+    for c in comp[:16]:  # the generator's streams are canonical reference encodings
+        assert bm.compress(bm.decompress(c)).words == c.words
+    for t in (5, 10, 20, 50):
+        res = runmerge.cdom_threshold(comp, t)
+        u = bm.decompress(res)
+        put(f"c4_t{t}", padded(u, r // 64), {"n": n, "r": r, "t": t, "m1": 256.0, "m0": 12544.0,
+                                              "card": u.cardinality(), "rle_out_len": len(res.words)})
+        print("C4 T", t, "done", u.cardinality())
+    out["meta"] = np.array(json.dumps(meta))
+    path = os.path.join(HERE, "baseline.npz")
+    np.savez_compressed(path, **out)
+    print(path, os.path.getsize(path))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "baseline":
+        baseline_cases()
+        sys.exit(0)
     rng = random.Random(14024073)
     threshold_cases(rng)
     symmetric_cases(rng)
@@ -488,3 +606,4 @@ if __name__ == "__main__":
     similarity_cases()
     serial_cases()
     kat()
+    baseline_cases()

@@ -7,7 +7,10 @@ restatement of runmerge.cdom_threshold.  C5 (256 GiB, eight 32 GiB waves) is
 checked through size-independent properties -- majority over an odd N is
 self-dual, so theta_256(NOT B) = NOT theta_256(B) -- plus oracle windows in
 every wave.  The counting identity sum_T popcount(theta_T) = sum_i popcount(B_i)
-checks C2 across all 64 thresholds."""
+checks C2 across all 64 thresholds.  On top, windows of every full-size result
+are compared with the REFERENCE's own outputs on those exact inputs
+(tests/golden/baseline.npz: C2 first / middle / last windows at every T, C3 and
+C5 first / last windows, C4's first 2^20 bits at T = 10, 20, 50)."""
 
 from __future__ import annotations
 
@@ -16,6 +19,7 @@ import ctypes
 import numpy as np
 import pytest
 
+from conftest import GOLDEN
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -23,6 +27,24 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 SEED = 1402
+
+
+def _baseline():
+    """Reference-run outputs on windows of these exact inputs (make_golden.py baseline_cases)."""
+    import json
+    import os
+
+    z = np.load(os.path.join(GOLDEN, "baseline.npz"))
+    return z, json.loads(str(z["meta"]))
+
+
+def _check_reference_windows(prefix, got_words_at):
+    """Every reference window fixture named prefix*: got_words_at(meta) -> words."""
+    z, meta = _baseline()
+    names = [k for k in meta if k.startswith(prefix)]
+    assert names
+    for k in names:
+        assert np.array_equal(got_words_at(meta[k]), z[k]), k
 
 
 @pytest.fixture(scope="module")
@@ -61,7 +83,7 @@ def test_c2_full_size_bit_exact(bq):
     q = bq.ThresholdQuery([data[i] for i in range(n)], 64 * nw)
     host = _host(data).reshape(n, nw)
     rows = [host[i] for i in range(n)]
-    total_pc, prev = 0, None
+    total_pc, prev, sweep = 0, None, {}
     for t in range(1, n + 1):
         out, pc = q.threshold(t)
         total_pc += int(pc.item())
@@ -72,6 +94,7 @@ def test_c2_full_size_bit_exact(bq):
             got = _host(out[:nw])
             assert np.array_equal(got, exp), t
             assert int(pc.item()) == _popcount(exp)
+            sweep[t] = got
         if t == 1:
             ref = data[0].clone()
             for i in range(1, n):
@@ -84,6 +107,8 @@ def test_c2_full_size_bit_exact(bq):
             assert torch.equal(out[:nw], ref)
         prev = out[:nw].clone()
     assert total_pc == sum(_popcount(r) for r in rows)  # each set bit counted once per T <= its count
+    # the reference's own answers on the first, middle and last 2^12-word windows, every T
+    _check_reference_windows("c2_", lambda m: sweep[m["t"]][m["w0"]:m["w0"] + m["nw"]])
     q.close()
 
 
@@ -97,8 +122,10 @@ def test_c3_full_size_bit_exact(bq):
     out, pc = q.symmetric(acc)
     host = _host(data).reshape(n, nw)
     exp = O.symmetric_port([host[i] for i in range(n)], 64 * nw, acc)
-    assert np.array_equal(_host(out[:nw]), exp)
+    got = _host(out[:nw])
+    assert np.array_equal(got, exp)
     assert int(pc.item()) == _popcount(exp)
+    _check_reference_windows("c3_", lambda m: got[m["w0"]:m["w0"] + m["nw"]])
     q.close()
 
 
@@ -127,6 +154,8 @@ def test_c4_full_size_bit_exact(bq):
     d = [torch.from_numpy(s.view(np.int64)).cuda() for s in streams]
     q = bq.RleQuery(d, r)
     exp = O.cdom_threshold(streams, r, t)
+    z, _ = _baseline()
+    assert np.array_equal(exp[: 1 << 14], z["c4_t50"])  # the reference's answer on the first 2^20 bits
     for _ in range(2):
         out, pc = q.threshold(t)
         assert np.array_equal(_host(out[:nw]), exp)
@@ -154,6 +183,11 @@ def test_c5_full_size_properties(bq):
         for a in (0, int(rng.integers(1, wave // 4096)) * 4096):
             win = [_host(data[i, a:a + 4096]) for i in range(n)]
             assert np.array_equal(_host(out[a:a + 4096]), O.threshold_port(win, 64 * 4096, t)), (w0, a)
+        z, meta = _baseline()
+        for k, m in meta.items():  # the reference's answers on the first and last 2^10 words
+            if k.startswith("c5_") and w0 <= m["w0"] < w0 + wave:
+                a = m["w0"] - w0
+                assert np.array_equal(_host(out[a:a + m["nw"]]), z[k]), k
         res = out[:wave].clone()
         q.close()
         data.bitwise_not_()  # r is a multiple of 64: no tail bits to mask
@@ -187,20 +221,15 @@ def test_c4_full_size_low_t_and_symmetric(bq):
     exp = O.cdom_symmetric(streams, r, acc)
     assert np.array_equal(_host(out[:nw]), exp)
     assert int(pc.item()) == _popcount(exp)
-    # thresholds where phase C runs in most tiles: K4s against the per-stream K4, whole
-    import os
-
+    # thresholds where phase C runs in most tiles: whole results against the oracle's
+    # cdom sweep, and the first 2^20 bits against the reference's own cdom_threshold
+    z, _ = _baseline()
     for t in (10, 20, 30):
         out, pc = q.threshold(t)
-        sliced, pc_sliced = _host(out[:nw]).copy(), int(pc.item())
-        prev = os.environ.get("BQ_RLE_SLICED")
-        os.environ["BQ_RLE_SLICED"] = "0"
-        try:
-            out, pc = q.threshold(t)
-        finally:
-            if prev is None:
-                del os.environ["BQ_RLE_SLICED"]
-            else:
-                os.environ["BQ_RLE_SLICED"] = prev
-        assert np.array_equal(sliced, _host(out[:nw])), t
-        assert pc_sliced == int(pc.item()) == _popcount(sliced), t
+        got = _host(out[:nw])
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(got, exp), t
+        assert int(pc.item()) == _popcount(exp), t
+        if t in (10, 20):
+            assert np.array_equal(got[: 1 << 14], z[f"c4_t{t}"]), t
+    q.close()

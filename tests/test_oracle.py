@@ -3,6 +3,8 @@
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -116,3 +118,42 @@ def test_oracle_generator_matches_product_generator():
         n = ctypes.c_uint64(0)
         assert lib.bq_gen_markov_rle(1402, i, r, 256.0, 12544.0, buf.ctypes.data, cap, ctypes.byref(n)) == 0
         assert np.array_equal(buf[: n.value], O.gen_markov_rle(1402, i, r, 256.0, 12544.0))
+
+
+# ---- BASELINE configs pinned to reference-run outputs (tests/golden/baseline.npz) ----
+
+def _baseline():
+    import json
+
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "baseline.npz"))
+    return z, json.loads(str(z["meta"]))
+
+
+def test_oracle_matches_reference_on_baseline_windows():
+    """The oracle on the exact seeded inputs of C1, C2, C3 and C5 windows reproduces
+    the reference's own outputs (make_golden.py baseline_cases)."""
+    z, meta = _baseline()
+    for name, m in meta.items():
+        if name.startswith("c4"):
+            continue
+        n, w0, nw = m["n"], m["w0"], m["nw"]
+        q16 = m["q16"] if isinstance(m["q16"], list) else [m["q16"]] * n
+        rows = [O.gen_bernoulli(1402, i, q16[i], w0, nw) for i in range(n)]
+        if name.startswith("c3"):
+            acc = [2 <= k <= 10 for k in range(n + 1)]
+            got = O.scan_count_symmetric(rows, 64 * nw, acc)
+        else:
+            got = O.threshold_port(rows, 64 * nw, m["t"], threads=2)
+        assert np.array_equal(got, z[name]), name
+        assert int(np.unpackbits(got.view(np.uint8)).sum()) == m["card"], name
+
+
+def test_oracle_cdom_matches_reference_on_c4_prefix():
+    """C4's 1024 Markov streams over their first 2^20 bits: the oracle's cdom sweep
+    equals the reference's cdom_threshold at T = 5, 10, 20, 50."""
+    z, meta = _baseline()
+    streams = [O.gen_markov_rle(1402, i, 1 << 20, 256.0, 12544.0) for i in range(1024)]
+    for t in (5, 10, 20, 50):
+        m = meta[f"c4_t{t}"]
+        got = O.cdom_threshold(streams, m["r"], t)
+        assert np.array_equal(got, z[f"c4_t{t}"]), t
