@@ -59,5 +59,20 @@ from .errors import (
 from .serial import dumps_bitmap, loads_bitmap_device, read_bitmap_device, write_bitmap
 from .similarity import DeviceDataset, SimilarityQuery, make_similarity
 from .spec import SymmetricSpec
+from . import circuits
+from .circuits import (
+    BitProgram,
+    Circuit,
+    PaddingPlan,
+    build_sideways_sum,
+    build_sop,
+    build_sorter,
+    build_tree_adder,
+    compile_circuit,
+    dumps_program,
+    loads_program,
+    optimize,
+    plan_padding,
+)
 
 __version__ = "0.1.0"

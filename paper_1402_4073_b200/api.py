@@ -23,6 +23,7 @@ without the CUDA library every call raises ``ExtensionMissing``.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Sequence
 
 import numpy as np
@@ -363,32 +364,66 @@ def wide_and(bitmaps: list):
 
 
 class CircuitLibrary:
-    """circuits.CircuitLibrary (circuits/library.py:84-133), threshold side.
+    """circuits.CircuitLibrary (circuits/library.py:84-133).
 
-    The reference pads an (N', T') query to a tabulated (N, T) circuit and
-    interprets it; here every (N, T) is a direct kernel launch, so the plan is
-    only kept for API compatibility (``plan``/``keys``)."""
+    ``keys`` / ``plan`` / ``program`` / ``build_circuit`` and the on-disk program
+    cache behave as the reference's (``circuits.py`` holds this package's own
+    builders, BitProgram layout and BQP1 disk format).  ``threshold`` plans the
+    query exactly as the reference does -- so a request outside the table raises
+    ``NoCoveringCircuit`` (library.py:66-67) and a bad (N, T) ``InputError`` --
+    and then evaluates theta_T of the real inputs with the counting kernel: the
+    padded circuit computes theta_T(B, 1^(T-T'), 0^...) = theta_T'(B), so the pad
+    bitmaps are never materialised.  ``program(n, t)`` gives the tabulated
+    straight-line program, which ``execute`` runs on the GPU (NVRTC)."""
 
     def __init__(self, n_max: int = 64, builder: str = "sideways", cache_dir: str | None = None):
-        if builder not in ("sop", "sorter", "tree", "sideways"):
+        from . import circuits as C
+
+        if builder not in C.BUILDERS:
             raise InputError(f"unknown builder {builder!r}")
         self.n_max = n_max
         self.builder = builder
         self.cache_dir = cache_dir
+        self._programs: dict = {}
+        self._keys = [(n, t) for n in C.tabulation_levels(n_max) for t in range(1, n + 1)]
 
     def keys(self):
-        levels, n = [], 2
-        while n <= self.n_max:
-            levels.append(n)
-            n *= 2
-        if self.n_max >= 2 and self.n_max not in levels:
-            levels.append(self.n_max)
-        return [(n, t) for n in levels for t in range(1, n + 1)]
+        return list(self._keys)
+
+    def build_circuit(self, n: int, t: int):
+        from . import circuits as C
+
+        return C.optimize(C.BUILDERS[self.builder](n, t))
+
+    def program(self, n: int, t: int):
+        """The tabulated (n, t) BitProgram, from memory, the cache directory, or
+        built and compiled (then written to the cache directory)."""
+        from . import circuits as C
+
+        key = (n, t)
+        prog = self._programs.get(key)
+        if prog is not None:
+            return prog
+        path = C.program_path(self.cache_dir, self.builder, n, t)
+        if path and os.path.exists(path):
+            with open(path, "rb") as fp:
+                prog = C.loads_program(fp.read())
+        else:
+            prog = C.compile_circuit(self.build_circuit(n, t))
+            if path:
+                os.makedirs(os.path.dirname(path), exist_ok=True)
+                with open(path, "wb") as fp:
+                    fp.write(C.dumps_program(prog))
+        self._programs[key] = prog
+        return prog
+
+    def plan(self, n_req: int, t_req: int):
+        from . import circuits as C
+
+        return C.plan_padding(n_req, t_req, self._keys)
 
     def threshold(self, inputs: Sequence, t: int):
-        n = len(inputs)
-        if n < 1 or not 1 <= t <= n or n > max(self.n_max, 1):
-            raise InputError(f"bad request ({n}, {t})")
+        self.plan(len(inputs), t)  # the reference's contract: InputError / NoCoveringCircuit
         return _run(inputs, None, t=t)
 
 

@@ -19,7 +19,7 @@ from typing import Iterable, Iterator
 
 import numpy as np
 
-from .errors import InputError
+from .errors import FormatError, InputError
 
 W = 64
 WORD_MASK = (1 << W) - 1
@@ -109,6 +109,48 @@ class UncompressedBitmap:
     def __repr__(self):
         return f"UncompressedBitmap(card={self.cardinality()}, r={self.bit_length})"
 
+    def iter_runs(self) -> Iterator[tuple]:
+        """Maximal ``(start, end_inclusive, bit)`` runs covering [0, bit_length)
+        (bitmaps.py:124-136), found word by word from bit transitions."""
+        yield from _runs_from_words(self.words, self.bit_length)
+
+    # set algebra (bitmaps.py:145-155) on the device: api.and_ / or_ / xor / andnot
+    def __and__(self, other):
+        from .api import and_
+        return and_(self, other)
+
+    def __or__(self, other):
+        from .api import or_
+        return or_(self, other)
+
+    def __xor__(self, other):
+        from .api import xor
+        return xor(self, other)
+
+    def andnot(self, other):
+        from .api import andnot
+        return andnot(self, other)
+
+
+def _runs_from_words(words, r: int) -> Iterator[tuple]:
+    """Runs of a word sequence (missing words zero) over [0, r): each word's bit
+    transitions are located with bit tricks instead of a per-bit loop."""
+    if r == 0:
+        return
+    start, prev = 0, words[0] & 1 if words else 0
+    for wi in range(word_count(r)):
+        w = words[wi] if wi < len(words) else 0
+        base = wi * W
+        nbits = min(W, r - base)
+        # bit k of t is set where bit k differs from bit k-1 (bit -1 = the previous run's bit)
+        t = (w ^ ((w << 1) | prev)) & ((1 << nbits) - 1)
+        while t:
+            k = (t & -t).bit_length() - 1
+            yield start, base + k - 1, prev
+            start, prev = base + k, prev ^ 1
+            t &= t - 1
+    yield start, r - 1, prev
+
 
 class RleBitmap:
     """Word-aligned run-length encoding (reference bitmaps.py:160-345).
@@ -155,6 +197,95 @@ class RleBitmap:
 
     def __repr__(self):
         return f"RleBitmap(r={self.bit_length}, words={len(self.words)})"
+
+    def iter_word_segments(self, total_words: int | None = None) -> Iterator[tuple]:
+        """``('f', bit, count)`` fill and ``('d', start, count)`` literal segments,
+        zero-extended to ``total_words`` (default: the bit length's word count);
+        FormatError on a truncated literal group or coverage beyond it
+        (bitmaps.py:196-219)."""
+        words, n = self.words, len(self.words)
+        i = covered = 0
+        while i < n:
+            mk = words[i]
+            bit, run, dirty = mk & 1, (mk >> 1) & 0xFFFFFFFF, mk >> 33
+            i += 1
+            if run:
+                yield "f", bit, run
+                covered += run
+            if dirty:
+                if i + dirty > n:
+                    raise FormatError("marker announces more literal words than present")
+                yield "d", i, dirty
+                i += dirty
+                covered += dirty
+        limit = word_count(self.bit_length) if total_words is None else total_words
+        if covered > limit:
+            raise FormatError("encoded words exceed bit_length")
+        if covered < limit:
+            yield "f", 0, limit - covered
+
+    def _decoded_words(self) -> list:
+        out = []
+        for kind, a, b in self.iter_word_segments():
+            out.extend([WORD_MASK if a else 0] * b if kind == "f" else self.words[a:a + b])
+        return out
+
+    def cardinality(self) -> int:
+        if self._card is None:
+            total = 0
+            for kind, a, b in self.iter_word_segments():
+                total += a * b * W if kind == "f" else sum(int(w).bit_count() for w in self.words[a:a + b])
+            self._card = total
+        return self._card
+
+    def get(self, position: int) -> bool:
+        if not 0 <= position < self.bit_length:
+            raise InputError("position out of range")
+        target, pos = position >> 6, 0
+        for kind, a, b in self.iter_word_segments():
+            if target < pos + b:
+                return bool(a) if kind == "f" else bool(self.words[a + target - pos] >> (position & 63) & 1)
+            pos += b
+        return False
+
+    __contains__ = get
+
+    def iter_set_bits(self) -> Iterator[int]:
+        pos = 0
+        for kind, a, b in self.iter_word_segments():
+            if kind == "f":
+                if a:
+                    yield from range(pos * W, (pos + b) * W)
+            else:
+                for k in range(b):
+                    yield from _iter_word_bits(self.words[a + k], (pos + k) * W)
+            pos += b
+
+    def positions(self) -> list:
+        return list(self.iter_set_bits())
+
+    def iter_runs(self) -> Iterator[tuple]:
+        """Maximal ``(start, end_inclusive, bit)`` runs over [0, bit_length) (bitmaps.py:221-259)."""
+        yield from _runs_from_words(self._decoded_words(), self.bit_length)
+
+    def run_count(self) -> int:
+        return sum(1 for _ in self.iter_runs())
+
+    def __and__(self, other):
+        from .api import and_
+        return and_(self, other)
+
+    def __or__(self, other):
+        from .api import or_
+        return or_(self, other)
+
+    def __xor__(self, other):
+        from .api import xor
+        return xor(self, other)
+
+    def andnot(self, other):
+        from .api import andnot
+        return andnot(self, other)
 
 
 class DeviceBitmap:
