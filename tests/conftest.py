@@ -13,6 +13,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# The Python reference installed by build() (oracle/install_ref.sh) -- present in
+# the build container and, through the gpurun snapshot, on the GPU box.  Put on
+# the path before the package is imported, so the package's exception classes
+# derive from the reference's (errors.py) as they do in a reference install.
+REF_INSTALL = os.path.join(ROOT, "oracle", "_ref")
+if os.path.isdir(os.path.join(REF_INSTALL, "bitquorum")) and REF_INSTALL not in sys.path:
+    sys.path.append(REF_INSTALL)
 
 
 def pytest_configure(config):
