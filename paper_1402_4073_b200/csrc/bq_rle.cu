@@ -571,6 +571,38 @@ struct bq_rle_query {
     mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced / tables / uses
 };
 
+// The previous K3 (A/B measurements: BQ_RLE_K3=old): K3a walks each stream's chain
+// window by window, K3b fills the directory from every window in parallel.
+static cudaError_t old_directory(const RleDirArgs &a, const std::vector<uint64_t> &lens, int n, int *d_err) {
+    std::vector<uint64_t> wbase(n + 1, 0);
+    uint64_t maxwin = 0;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t nwin = (lens[i] + 31) / 32;
+        wbase[i + 1] = wbase[i] + nwin;
+        maxwin = std::max(maxwin, nwin);
+    }
+    const uint64_t nwin_all = wbase[n];
+    char *scratch = nullptr;
+    cudaError_t e = pool_alloc(reinterpret_cast<void **>(&scratch), (size_t)(n + 1) * 8 + nwin_all * 12 + 16);
+    uint64_t *d_wbase = reinterpret_cast<uint64_t *>(scratch);
+    uint64_t *d_wpos = d_wbase + n + 1;
+    uint32_t *d_wreach = reinterpret_cast<uint32_t *>(d_wpos + nwin_all);
+    if (e == cudaSuccess) e = cudaMemcpy(d_wbase, wbase.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(d_wreach, 0, nwin_all * 4 + 4);
+    if (e == cudaSuccess) {
+        rle_chain_kernel<<<(n + 3) / 4, 128>>>(a, d_wbase, d_wreach, d_wpos);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && nwin_all) {
+        const unsigned gx = (unsigned)std::min<uint64_t>((maxwin + 3) / 4, 64);
+        rle_dirfill_kernel<<<dim3(gx, (unsigned)n), 128>>>(a, d_wbase, d_wreach, d_wpos);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (scratch) pool_free(scratch);
+    return e;
+}
+
 // Validation of streams over a bit_length-0 universe (host walk; valid streams
 // hold only empty markers, so they are short in practice).
 static int validate_empty_universe(const std::vector<const uint64_t *> &ptrs, const std::vector<uint64_t> &lens) {
@@ -610,10 +642,11 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
     if (n > BQ_MAX_INPUTS) return set_error(BQ_EINPUT, "%d inputs exceed BQ_MAX_INPUTS=%d", n, BQ_MAX_INPUTS);
     if (!streams) return set_error(BQ_EINPUT, "streams is NULL");
     const uint64_t total = word_count(r_bits);
-    if (total >= (1ull << 32)) return set_error(BQ_EINPUT, "bit_length too large for the RLE directory (< 2^38 bits)");
+    if (total >= (1ull << 32) - 2)
+        return set_error(BQ_EINPUT, "bit_length too large for the RLE directory (< 2^38 - 128 bits)");
     for (int i = 0; i < n; ++i) {
-        if (streams[i].n_words >= (1ull << 32))
-            return set_error(BQ_EINPUT, "stream %d longer than 2^32 words", i);
+        if (streams[i].n_words >= (1ull << 32) - 2)
+            return set_error(BQ_EINPUT, "stream %d longer than 2^32 - 3 words", i);
         if (streams[i].n_words && !streams[i].words) return set_error(BQ_EINPUT, "stream %d is NULL", i);
         if (reinterpret_cast<uintptr_t>(streams[i].words) & 7)
             return set_error(BQ_EINPUT, "stream %d: device words must be 8-byte aligned", i);
@@ -678,41 +711,27 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
         a.dir = q->d_dir;
         a.err = d_err;
         a.err_stream = d_err_stream;
-        // window bookkeeping for K3a -> K3b: per stream ceil(L / 32) windows
-        std::vector<uint64_t> wbase(n + 1, 0);
-        uint64_t maxwin = 0;
-        for (int i = 0; i < n; ++i) {
-            const uint64_t nwin = (lens[i] + 31) / 32;
-            wbase[i + 1] = wbase[i] + nwin;
-            maxwin = std::max(maxwin, nwin);
-        }
-        const uint64_t nwin_all = wbase[n];
-        char *scratch = nullptr;
-        e = pool_alloc(reinterpret_cast<void **>(&scratch), (size_t)(n + 1) * 8 + nwin_all * 12 + 16);
-        uint64_t *d_wbase = reinterpret_cast<uint64_t *>(scratch);
-        uint64_t *d_wpos = d_wbase + n + 1;
-        uint32_t *d_wreach = reinterpret_cast<uint32_t *>(d_wpos + nwin_all);
-        if (e == cudaSuccess) e = cudaMemcpy(d_wbase, wbase.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemset(d_wreach, 0, nwin_all * 4 + 4);
-        if (e == cudaSuccess) {
-            const int warps_per_block = 4;
-            rle_chain_kernel<<<(n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block>>>(a, d_wbase, d_wreach,
-                                                                                                d_wpos);
-            e = cudaGetLastError();
-        }
-        if (e == cudaSuccess && nwin_all) {
-            const unsigned gx = (unsigned)std::min<uint64_t>((maxwin + 3) / 4, 64);
-            rle_dirfill_kernel<<<dim3(gx, (unsigned)n), 128>>>(a, d_wbase, d_wreach, d_wpos);
-            e = cudaGetLastError();
-        }
-        if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        if (scratch) pool_free(scratch);
         int herr[4] = {0, 0, 0, 0};
-        if (e == cudaSuccess) e = cudaMemcpy(herr, d_err, 16, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) {
-            pool_free(q->mem);
-            delete q;
-            return cuda_error(e, "rle directory (K3)");
+        static const char *k3env = getenv("BQ_RLE_K3");
+        if (k3env && !strcmp(k3env, "old")) {  // the previous two-kernel form (A/B measurements only)
+            e = old_directory(a, lens, n, d_err);
+            if (e == cudaSuccess) e = cudaMemcpy(herr, d_err, 16, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) {
+                pool_free(q->mem);
+                delete q;
+                return cuda_error(e, "rle directory (K3)");
+            }
+        } else {
+            uint64_t bad = 0;
+            rc = build_rle_directory(q->d_ptrs, q->d_lens, lens, total, a.tail_mask, tile0, ntiles + 1, q->d_dir,
+                                     &herr[0], &bad);
+            if (rc) {
+                pool_free(q->mem);
+                delete q;
+                return rc;
+            }
+            herr[2] = (int)(uint32_t)bad;
+            herr[3] = (int)(uint32_t)(bad >> 32);
         }
         if (herr[0]) {
             unsigned long long bad = (unsigned long long)(uint32_t)herr[2] | ((unsigned long long)(uint32_t)herr[3] << 32);
@@ -774,6 +793,7 @@ BQ_API int bq_rle_query_layout_events(const bq_rle_query *q, uint64_t *n_events)
     *n_events = q->sliced.n_events;
     return BQ_OK;
 }
+
 
 static void note_use(bq_rle_query *q, cudaStream_t s) {
     std::lock_guard<std::mutex> guard(q->build_mu);

@@ -1,0 +1,386 @@
+// K3: the tile directory of n RLE streams in one streaming pass (sm_100a).
+//
+// The directory row of tile boundary b for a stream is the marker whose runs
+// cover word b: (its stream index, the word where its fill starts).  Finding it
+// means following the stream's marker chain (bitmaps.py:196-219) -- a marker is
+// only recognisable from the previous one -- so a plain walk is one dependent
+// step per marker, ~142k per C4 stream.  This kernel cuts every stream into
+// segments of kSegWords stream words and walks all segments at once:
+//
+//  * Speculative entry.  A segment's chain enters at the first marker at or
+//    after its first word.  One lane per segment guesses it from the kHalo words
+//    before the segment: each of those words is taken as a marker in turn, its
+//    chain followed to the first position >= the segment start, and the position
+//    most of the eight chains land on (the smallest on a tie) is the guess.  True
+//    markers all land on the true entry, and literal words taken as markers
+//    mostly fall through to it (a literal with a zero dirty field steps to the next
+//    word).  On C4 streams the guess was right for every segment measured.
+//  * Walk.  From its entry, the lane walks its segment in shared memory (the
+//    CTA's block of 32 segments is staged by one TMA bulk copy), summing the words
+//    the markers cover; its exit is the first chain position past the segment.
+//  * Resolution.  A segment's guess is right iff it equals the previous
+//    segment's exit (or, if that exit lies past the segment, the segment holds no
+//    marker start at all).  Within a block this is checked lane by lane; across
+//    blocks by a decoupled look-back: blocks take tickets in (block, stream)
+//    order, each publishes its exit and end position as soon as its own entry is
+//    known, and the next block of the stream spins on that word.  A wrong guess
+//    is repaired by re-walking that segment from the true entry (shared memory,
+//    no second HBM read), so the result is exact whatever the guesses.
+//  * Directory.  With its true entry and absolute word position, every lane
+//    walks its segment once more from shared memory and writes the row of every
+//    tile boundary its markers cover.  Validation is iter_word_segments' /
+//    decompress's: a chain leaving the stream early is a truncated literal group,
+//    coverage past ceil(r/64) words is overlong, set bits >= r are beyond r
+//    (bitmaps.py:210-217, :428-431), in that order of precedence.
+//
+// HBM traffic is one read of the streams plus the directory (8 bytes per tile
+// and stream); the old form (one warp per stream following the chain window by
+// window, then a second pass over all windows) read the streams twice and was
+// latency-bound on the serial chain.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "bq_internal.h"
+
+namespace bq {
+
+#ifndef BQ_DIR_SEG
+#define BQ_DIR_SEG 64
+#endif
+constexpr int kSegWords = BQ_DIR_SEG;                // stream words per segment (one lane)
+constexpr int kBlockWords = kSegWords * 32;          // one warp = one block of 32 segments
+constexpr int kHalo = 8;                             // words before a segment holding its entry guesses
+// a lane's staging slot: halo + segment + 16-byte alignment slack, its stride = 16 bytes
+// mod 128 so the lanes' slots start in different shared-memory banks
+constexpr int kSlotWords = ((kHalo + kSegWords + 2 + 15) / 16) * 16 + 2;
+
+struct DirArgs {
+    const uint64_t *const *ptrs;
+    const uint64_t *lens;
+    int n;
+    uint64_t total_words;        // ceil(r / 64)
+    uint64_t tail_mask;          // valid bits of word total_words - 1 when r % 64 != 0, else 0
+    uint32_t tile0, nrows;       // directory rows: tile boundaries tile0 .. tile0 + nrows - 1
+    uint2 *dir;                  // [nrows][n] (marker index, fill start word)
+    const uint2 *jobs;           // ticket -> (stream, block), block-major
+    const uint32_t *link_base;   // per stream: index of its block 0 in `link`
+    const uint32_t *nblocks;     // per stream
+    unsigned long long *link;    // per (stream, block): exit | end position << 32, ~0 until published
+    unsigned int *ticket;
+    unsigned long long *err;     // min over (stream << 32 | precedence): the first failing stream
+};
+
+enum { DIR_ERR_TRUNCATED = 0, DIR_ERR_OVERLONG = 1, DIR_ERR_BEYOND_R = 2 };
+
+__device__ __forceinline__ void dir_fail(const DirArgs &a, uint32_t code, uint32_t stream) {
+    atomicMin(a.err, ((unsigned long long)stream << 32) | code);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ DirArgs a) {
+    __shared__ __align__(16) uint64_t slots[32 * kSlotWords];
+    __shared__ __align__(8) uint64_t bar;
+    const int lane = threadIdx.x;
+
+    unsigned int t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1u);  // tickets in start order: a block's predecessor started earlier
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const uint2 job = a.jobs[t];
+    const uint32_t stream = job.x, blk = job.y;
+    const uint64_t *s = a.ptrs[stream];
+    const uint32_t L = (uint32_t)a.lens[stream];  // < 2^32 - 2 (bq_rle_query_create)
+    const uint64_t total = a.total_words;
+
+    // ---- this lane's segment [q, qe) and its staging: words [q - kHalo, qe) --------
+    const uint32_t q = blk * (uint32_t)kBlockWords + (uint32_t)lane * kSegWords;
+    const bool active = q < L;
+    const uint32_t qe = active ? min(q + (uint32_t)kSegWords, L) : q;
+    const uint32_t h0 = q >= (uint32_t)kHalo ? q - kHalo : 0;
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + h0) & ~(uintptr_t)15;
+    const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + qe) + 15) & ~(uintptr_t)15;
+    const uint32_t bytes = active ? (uint32_t)(g1 - g0) : 0u;
+    uint64_t *slot = slots + lane * kSlotWords;
+    // stream word p is slot[p - sbase] (sbase = h0 or h0 - 1 after the widening: -1 at a
+    // stream that starts 8 bytes into a 16-byte line)
+    const int64_t sbase = ((intptr_t)g0 - reinterpret_cast<intptr_t>(s)) / 8;
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar_s) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    if (bytes) {
+        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar_s),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(slot)),
+                     "l"(g0), "r"(bytes), "r"(bar_s)
+                     : "memory");
+    } else {
+        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar_s) : "memory");
+    }
+    // the previous block's exit is published by now in the common case: fetch it while
+    // the copies land
+    uint64_t link_prev = 0;
+    if (blk > 0 && lane == 0) link_prev = ld_acquire(a.link + a.link_base[stream] + blk - 1);
+    {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                         : "=r"(done)
+                         : "r"(bar_s)
+                         : "memory");
+    }
+
+    // speculative entry: the landing most of the kHalo hypotheses agree on (smallest on a tie)
+    uint32_t entry = q;
+    if (active && q > 0) {
+        uint64_t land[kHalo];
+#pragma unroll
+        for (int j = kHalo - 1; j >= 0; --j) {
+            const uint32_t h = q - kHalo + j;
+            const uint64_t nx = (uint64_t)h + 1 + (slot[(int64_t)h - sbase] >> 33);
+            uint64_t v = nx;
+#pragma unroll
+            for (int k = j + 1; k < kHalo; ++k)
+                if (nx == (uint64_t)(q - kHalo + k)) v = land[k];
+            land[j] = v;
+        }
+        int best = 0;
+        uint64_t pick = ~0ull;
+#pragma unroll
+        for (int j = 0; j < kHalo; ++j) {
+            int c = 0;
+#pragma unroll
+            for (int k = 0; k < kHalo; ++k) c += land[k] == land[j];
+            if (c > best || (c == best && land[j] < pick)) {
+                best = c;
+                pick = land[j];
+            }
+        }
+        entry = (uint32_t)min(pick, (uint64_t)L + 1);
+    }
+    // walk from slot index i to the first chain position >= qe, summing the words the
+    // markers cover (i stays < 2^32: it is < qe - sbase before a step, dirty < 2^31)
+    const uint32_t iend = (uint32_t)((int64_t)qe - sbase);
+    auto walk = [&](uint32_t from, uint64_t &span) -> uint64_t {
+        span = 0;
+        uint32_t i = (uint32_t)((int64_t)from - sbase);
+        while (i < iend) {
+            const uint64_t w = slot[i];
+            const uint32_t dirty = (uint32_t)(w >> 33);
+            span += (uint64_t)(uint32_t)(w >> 1) + dirty;
+            i += 1 + dirty;
+        }
+        return (uint64_t)((int64_t)i + sbase);
+    };
+    uint64_t span = 0, exit_ = entry;
+    if (active && entry < qe) exit_ = walk(entry, span);
+
+    // ---- the block's entry: the previous block's exit (decoupled look-back) --------
+    uint64_t n_in = 0, p_in = 0;
+    if (blk > 0) {
+        if (lane == 0) {
+            const unsigned long long *lk = a.link + a.link_base[stream] + blk - 1;
+            int spins = 0;
+            while (link_prev == ~0ull) {
+                if (++spins > 4) __nanosleep(64);
+                link_prev = ld_acquire(lk);
+            }
+            n_in = link_prev & 0xFFFFFFFFull;
+            p_in = link_prev >> 32;
+        }
+        n_in = __shfl_sync(0xffffffffu, n_in, 0);
+        p_in = __shfl_sync(0xffffffffu, p_in, 0);
+    }
+    // ---- resolution: every entry must be the previous segment's exit -------------
+    // All lanes check at once; a lane whose predecessor's exit lies past its segment
+    // holds no marker start (it passes the exit through), a lane whose guess differs
+    // re-walks from the true entry.  Repeat while any exit changed (typically never).
+    for (;;) {
+        uint64_t prev = __shfl_up_sync(0xffffffffu, exit_, 1);
+        if (lane == 0) prev = n_in;
+        bool changed = false;
+        if (!active || prev >= qe) {
+            changed = exit_ != prev || span;
+            entry = (uint32_t)min(prev, (uint64_t)L + 1);
+            exit_ = prev;
+            span = 0;
+        } else if (prev != entry) {
+            entry = (uint32_t)prev;
+            exit_ = walk(entry, span);
+            changed = true;
+        }
+        if (!__ballot_sync(0xffffffffu, changed)) break;
+    }
+    // absolute word positions: exclusive prefix of the spans
+    uint64_t incl = span;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint64_t pos0 = p_in + incl - span;
+    const uint64_t p_end = __shfl_sync(0xffffffffu, p_in + incl, 31);
+    const uint64_t x_end = __shfl_sync(0xffffffffu, exit_, 31);
+    // publish this block's exit for the next block of the stream (clamped: > L is a
+    // truncated group, > total overlong; both below the ~0 sentinel)
+    const bool last_block = blk + 1 == a.nblocks[stream];
+    if (lane == 31) {
+        const uint64_t ex = min(x_end, (uint64_t)L + 1), pe = min(p_end, total + 1);
+        if (!last_block) st_release(a.link + a.link_base[stream] + blk, ex | (pe << 32));
+        else {
+            if (x_end > L) dir_fail(a, DIR_ERR_TRUNCATED, stream);
+            else if (p_end > total) dir_fail(a, DIR_ERR_OVERLONG, stream);
+        }
+    }
+
+    // ---- directory rows of the tile boundaries this segment's markers cover ------
+    // nb: the next tile boundary of the query's range (~0 past it), drow its row.  A
+    // marker crossing a boundary costs one store (several only for fills longer than
+    // a tile), so the warp rarely diverges here.
+    const uint64_t r0 = (uint64_t)a.tile0 * kRleTile;
+    const uint64_t rlim = min((uint64_t)(a.tile0 + a.nrows) * kRleTile, total);
+    uint64_t nb = max((pos0 + kRleTile - 1) / kRleTile * kRleTile, r0);
+    uint2 *drow = a.dir + ((nb / kRleTile) - a.tile0) * (uint64_t)a.n + stream;
+    if (nb >= rlim) nb = ~0ull;
+    const uint64_t tail_at = a.tail_mask ? total : ~0ull;  // the marker ending there has its last word checked
+    uint64_t pos = pos0;
+    uint32_t i = active ? (uint32_t)((int64_t)entry - sbase) : iend;
+    while (i < iend) {
+        const uint64_t w = slot[i];
+        const uint32_t dirty = (uint32_t)(w >> 33);
+        const uint64_t end = pos + (uint32_t)(w >> 1) + dirty;
+        if (end > nb) {
+            const uint2 v = make_uint2((uint32_t)((int64_t)i + sbase), (uint32_t)pos);
+            do {
+                *drow = v;
+                drow += a.n;
+                nb += kRleTile;
+            } while (end > nb && nb < rlim);
+            if (nb >= rlim) nb = ~0ull;
+        }
+        if (end >= tail_at && end == total && end > pos) {
+            // bits >= r in the last word (bitmaps.py:70-72 via decompress :428-431)
+            const uint64_t p = (uint64_t)((int64_t)i + sbase);
+            if (dirty == 0) {
+                if (w & 1) dir_fail(a, DIR_ERR_BEYOND_R, stream);
+            } else if (p + dirty < L && (__ldg(s + p + dirty) & ~a.tail_mask)) {
+                dir_fail(a, DIR_ERR_BEYOND_R, stream);
+            }
+        }
+        pos = end;
+        i += 1 + dirty;
+    }
+    // rows past the stream's coverage: exhausted stream, implicit zero tail
+    if (last_block && p_end <= total) {
+        const uint64_t t0 = max((p_end + kRleTile - 1) / kRleTile, (uint64_t)a.tile0);
+        for (uint64_t tt = t0 + lane; tt < (uint64_t)a.tile0 + a.nrows; tt += 32)
+            a.dir[(tt - a.tile0) * (uint64_t)a.n + stream] = make_uint2(L, (uint32_t)p_end);
+    }
+}
+
+int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const std::vector<uint64_t> &lens,
+                        uint64_t total_words, uint64_t tail_mask, uint32_t tile0, uint32_t nrows, uint2 *d_dir,
+                        int *err_code, uint64_t *err_stream) {
+    const int n = (int)lens.size();
+    *err_code = 0;
+    std::vector<uint32_t> nblk(n), base(n);
+    uint32_t maxb = 0;
+    uint64_t njobs = 0;
+    for (int i = 0; i < n; ++i) {
+        nblk[i] = (uint32_t)std::max<uint64_t>(1, (lens[i] + kBlockWords - 1) / kBlockWords);
+        base[i] = (uint32_t)njobs;
+        njobs += nblk[i];
+        maxb = std::max(maxb, nblk[i]);
+    }
+    // tickets block-major: block k of every stream before block k + 1 of any; the table
+    // is written into a pinned staging buffer (kept between calls) so its upload is a
+    // plain DMA, and the build holds the staging lock until its copy has completed
+    static std::mutex staging_mu;
+    static uint2 *staging = nullptr;
+    static size_t staging_cap = 0;
+    std::lock_guard<std::mutex> staging_guard(staging_mu);
+    if (staging_cap < njobs) {
+        if (staging) cudaFreeHost(staging);
+        staging = nullptr;
+        staging_cap = 0;
+        if (cudaHostAlloc(reinterpret_cast<void **>(&staging), std::max<size_t>(njobs, 1 << 16) * 8,
+                          cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            staging = nullptr;
+            return set_error(BQ_ERESOURCE, "pinned staging for the directory job table");
+        }
+        staging_cap = std::max<size_t>(njobs, 1 << 16);
+    }
+    {
+        size_t k = 0;
+        for (uint32_t b = 0; b < maxb; ++b)
+            for (int i = 0; i < n; ++i)
+                if (b < nblk[i]) staging[k++] = make_uint2((uint32_t)i, b);
+    }
+    const size_t jb = njobs * 8, lb = njobs * 8, tb = (size_t)n * 8;
+    char *scratch = nullptr;
+    cudaError_t e = pool_alloc(reinterpret_cast<void **>(&scratch), jb + lb + tb + 64);
+    if (e != cudaSuccess) return cuda_error(e, "rle directory scratch");
+    uint2 *d_jobs = reinterpret_cast<uint2 *>(scratch);
+    unsigned long long *d_link = reinterpret_cast<unsigned long long *>(scratch + jb);
+    uint32_t *d_base = reinterpret_cast<uint32_t *>(scratch + jb + lb);
+    uint32_t *d_nblk = d_base + n;
+    unsigned int *d_ticket = reinterpret_cast<unsigned int *>(scratch + jb + lb + tb);
+    unsigned long long *d_err = reinterpret_cast<unsigned long long *>(scratch + jb + lb + tb + 8);
+    std::vector<uint32_t> tabs(2 * (size_t)n);
+    std::copy(base.begin(), base.end(), tabs.begin());
+    std::copy(nblk.begin(), nblk.end(), tabs.begin() + n);
+    e = cudaMemcpyAsync(d_jobs, staging, jb, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_base, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, lb, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_ticket, 0, 8, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0xFF, 8, 0);
+    if (e == cudaSuccess) {
+        DirArgs a;
+        a.ptrs = d_ptrs;
+        a.lens = d_lens;
+        a.n = n;
+        a.total_words = total_words;
+        a.tail_mask = tail_mask;
+        a.tile0 = tile0;
+        a.nrows = nrows;
+        a.dir = d_dir;
+        a.jobs = d_jobs;
+        a.link_base = d_base;
+        a.nblocks = d_nblk;
+        a.link = d_link;
+        a.ticket = d_ticket;
+        a.err = d_err;
+        rle_dir_kernel<<<(unsigned)njobs, 32, 0, 0>>>(a);
+        e = cudaGetLastError();
+    }
+    unsigned long long herr = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, 8, cudaMemcpyDeviceToHost, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    pool_free(scratch);
+    if (e != cudaSuccess) return cuda_error(e, "rle directory (K3)");
+    if (herr != ~0ull) {
+        const uint32_t code = (uint32_t)(herr & 0xFFFFFFFFull);
+        *err_code = code == DIR_ERR_TRUNCATED ? 1 : code == DIR_ERR_OVERLONG ? 2 : 3;
+        *err_stream = herr >> 32;
+    }
+    return BQ_OK;
+}
+
+}  // namespace bq

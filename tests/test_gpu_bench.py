@@ -53,7 +53,10 @@ def test_c4_line_contract():
     d = _bench("--workload", "c4", "--steps", "5", "--warmup", "3", "--no-e2e")
     assert {"metric", "value", "roofline", "cpu_baseline", "gpu_launches", "clocks"} <= set(d)
     assert d["matches_oracle_window"] and d["popcount"] > 0
-    assert d["sliced_layout"]["markers"] > 0 and d["direct_ewah_k4"]["mean_launch_ms"] > 0
+    f = d["fresh_query_ms"]
+    assert f["k3_directory"] > 0 and f["k4_first_eval"] > 0 and f["total"] >= f["k3_directory"]
+    assert d["repeated_query"]["layout"]["markers"] > 0 and d["repeated_query"]["mean_launch_ms"] > 0
+    assert d["roofline"]["frac"] < 1.2  # input bytes over the fresh query: never above the HBM peak
 
 
 @pytest.mark.parametrize("workload", ["c2", "c4"])
