@@ -9,6 +9,8 @@ fallback: if the library is missing every entry point raises
 from __future__ import annotations
 
 import ctypes
+
+import numpy as np
 import os
 import threading
 
@@ -107,9 +109,18 @@ def check(rc: int, what: str = ""):
 
 
 def spans(pairs):
-    """Build a ctypes array of bq_span from (device_ptr, n_words) pairs."""
-    arr = (Span * max(len(pairs), 1))()
-    for k, (ptr, n) in enumerate(pairs):
-        arr[k].words = ptr or None
-        arr[k].n_words = n
+    """bq_span array (device_ptr, n_words) for the C ABI: a contiguous (n, 2) uint64
+    numpy array (pass ``.ctypes.data``); built column-wise, no per-element ctypes."""
+    arr = np.zeros((max(len(pairs), 1), 2), dtype=np.uint64)
+    if pairs:
+        arr[: len(pairs)] = np.asarray(pairs, dtype=np.uint64).reshape(-1, 2)
+    return arr
+
+
+def span_columns(ptrs, n_words):
+    """The same from two sequences (pointers, word counts)."""
+    arr = np.zeros((max(len(ptrs), 1), 2), dtype=np.uint64)
+    if len(ptrs):
+        arr[: len(ptrs), 0] = ptrs
+        arr[: len(ptrs), 1] = n_words
     return arr

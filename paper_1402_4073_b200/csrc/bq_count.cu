@@ -354,26 +354,66 @@ int launch_count(const CountArgs &a, int m, int mode, cudaStream_t stream) {
 // Whole-bitmap set algebra (bitmaps.py:438-476, 598-644) with fused popcount.
 namespace bq {
 
-__global__ void __launch_bounds__(256) binop_kernel(int kind, const uint64_t *__restrict__ a, uint64_t na,
+template <int KIND>
+__device__ __forceinline__ uint64_t binop(uint64_t x, uint64_t y) {
+    if (KIND == 0) return x & y;   // _u_and: zero beyond the shorter operand
+    if (KIND == 1) return x | y;   // _u_or: longer tail copied
+    if (KIND == 2) return x ^ y;   // _u_xor
+    if (KIND == 3) return x & ~y;  // _u_andnot: a's tail copied
+    return ~x;                     // _u_not: complement within r
+}
+
+__device__ __forceinline__ ulonglong2 ld_stream2(const uint64_t *p) {
+    ulonglong2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+    return v;
+}
+
+// Two words per thread: 128-bit streaming loads and stores over 16-byte-aligned
+// operands (the host falls back to word loads otherwise); words past an operand's
+// length read as zero; the popcount and last nonzero index are fused.
+template <int KIND, bool VEC>
+__global__ void __launch_bounds__(256) binop_kernel(const uint64_t *__restrict__ a, uint64_t na,
                                                    const uint64_t *__restrict__ b, uint64_t nb, uint64_t nwords,
                                                    uint64_t last_mask, uint64_t *__restrict__ out,
                                                    unsigned long long *popcnt, unsigned long long *last_nz) {
     unsigned long long pc = 0, lnz = 0;
-    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t x = w < na ? __ldg(a + w) : 0ull;
-        const uint64_t y = w < nb ? __ldg(b + w) : 0ull;
-        uint64_t r;
-        switch (kind) {
-            case 0: r = x & y; break;   // _u_and: zero beyond the shorter operand
-            case 1: r = x | y; break;   // _u_or: longer tail copied
-            case 2: r = x ^ y; break;   // _u_xor
-            case 3: r = x & ~y; break;  // _u_andnot: a's tail copied
-            default: r = ~x; break;     // _u_not: complement within r
+    const uint64_t npairs = (nwords + 1) / 2;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = 2 * p;
+        ulonglong2 x, y = make_ulonglong2(0ull, 0ull);
+        if (VEC && w + 1 < na) {
+            x = ld_stream2(a + w);
+        } else {
+            x.x = w < na ? __ldg(a + w) : 0ull;
+            x.y = w + 1 < na ? __ldg(a + w + 1) : 0ull;
         }
-        if (w == nwords - 1) r &= last_mask;
-        out[w] = r;
-        pc += __popcll(r);
-        if (r) lnz = w + 1;
+        if (KIND != 4) {
+            if (VEC && w + 1 < nb) {
+                y = ld_stream2(b + w);
+            } else {
+                y.x = w < nb ? __ldg(b + w) : 0ull;
+                y.y = w + 1 < nb ? __ldg(b + w + 1) : 0ull;
+            }
+        }
+        uint64_t r0 = binop<KIND>(x.x, y.x), r1 = binop<KIND>(x.y, y.y);
+        if (w + 1 < nwords) {
+            if (w + 2 == nwords) r1 &= last_mask;
+            if (VEC) {
+                *reinterpret_cast<ulonglong2 *>(out + w) = make_ulonglong2(r0, r1);
+            } else {
+                out[w] = r0;
+                out[w + 1] = r1;
+            }
+            pc += __popcll(r0) + __popcll(r1);
+            if (r1) lnz = w + 2;
+            else if (r0) lnz = w + 1;
+        } else {  // the odd last word
+            r0 &= last_mask;
+            out[w] = r0;
+            pc += __popcll(r0);
+            if (r0) lnz = w + 1;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -384,6 +424,20 @@ __global__ void __launch_bounds__(256) binop_kernel(int kind, const uint64_t *__
     if ((threadIdx.x & 31) == 0) {
         if (popcnt && pc) atomicAdd(popcnt, pc);
         if (last_nz && lnz) atomicMax(last_nz, lnz);
+    }
+}
+
+typedef void (*BinopFn)(const uint64_t *, uint64_t, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t *,
+                        unsigned long long *, unsigned long long *);
+
+template <bool VEC>
+static BinopFn binop_fn(int kind) {
+    switch (kind) {
+        case 0: return binop_kernel<0, VEC>;
+        case 1: return binop_kernel<1, VEC>;
+        case 2: return binop_kernel<2, VEC>;
+        case 3: return binop_kernel<3, VEC>;
+        default: return binop_kernel<4, VEC>;
     }
 }
 
@@ -400,11 +454,14 @@ extern "C" BQ_API int bq_binary_op(int kind, const uint64_t *d_a, uint64_t na, c
     if (nwords && !d_out) return set_error(BQ_EINPUT, "d_out is NULL");
     if (!nwords) return BQ_OK;
     const uint64_t last_mask = (r_bits % W) ? ((1ull << (r_bits % W)) - 1) : ~0ull;
-    uint64_t grid = (nwords + 255) / 256;
+    const bool vec = !((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_out) |
+                        (kind == 4 ? 0 : reinterpret_cast<uintptr_t>(d_b))) & 15);
+    uint64_t grid = ((nwords + 1) / 2 + 255) / 256;
     const uint64_t cap = (uint64_t)sm_count() * 8;
     if (grid > cap) grid = cap;
-    binop_kernel<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        kind, d_a, na, kind == 4 ? nullptr : d_b, kind == 4 ? 0 : nb, nwords, last_mask, d_out, d_popcnt, d_last_nz);
+    BinopFn fn = vec ? binop_fn<true>(kind) : binop_fn<false>(kind);
+    fn<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_a, na, kind == 4 ? nullptr : d_b, kind == 4 ? 0 : nb, nwords, last_mask, d_out, d_popcnt, d_last_nz);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "binop_kernel launch");
     return BQ_OK;

@@ -51,6 +51,9 @@ namespace bq {
 #ifndef BQ_DIR_SEG
 #define BQ_DIR_SEG 64
 #endif
+#ifndef BQ_DIR_CONTIG
+#define BQ_DIR_CONTIG 0
+#endif
 constexpr int kSegWords = BQ_DIR_SEG;                // stream words per segment (one lane)
 constexpr int kBlockWords = kSegWords * 32;          // one warp = one block of 32 segments
 constexpr int kHalo = 8;                             // words before a segment holding its entry guesses
@@ -80,18 +83,27 @@ __device__ __forceinline__ void dir_fail(const DirArgs &a, uint32_t code, uint32
     atomicMin(a.err, ((unsigned long long)stream << 32) | code);
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+// The link word is self-contained (exit and end position in one 64-bit store), and
+// nothing else the consumer reads depends on the producer: relaxed accesses at gpu
+// scope suffice (no fence on the producer's critical path).
+__device__ __forceinline__ unsigned long long ld_link(const unsigned long long *p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_link(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ DirArgs a) {
+#if BQ_DIR_CONTIG
+    // one contiguous copy of the block [b0 - kHalo, b1): a lane's halo is its left
+    // neighbour's tail (less shared memory per warp, more warps per SM)
+    __shared__ __align__(16) uint64_t slots[kHalo + kBlockWords + 4];
+#else
     __shared__ __align__(16) uint64_t slots[32 * kSlotWords];
+#endif
     __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x;
 
@@ -108,17 +120,29 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const uint32_t q = blk * (uint32_t)kBlockWords + (uint32_t)lane * kSegWords;
     const bool active = q < L;
     const uint32_t qe = active ? min(q + (uint32_t)kSegWords, L) : q;
+#if BQ_DIR_CONTIG
+    const uint32_t b0 = blk * (uint32_t)kBlockWords;
+    const uint32_t h0 = b0 >= (uint32_t)kHalo ? b0 - kHalo : 0;
+    const uint32_t b1 = min(b0 + (uint32_t)kBlockWords, L);
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + h0) & ~(uintptr_t)15;
+    const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + b1) + 15) & ~(uintptr_t)15;
+    const uint32_t bytes = (lane == 0 && b1 > h0) ? (uint32_t)(g1 - g0) : 0u;
+    uint64_t *slot = slots;
+    constexpr uint32_t kArrivals = 1;
+#else
     const uint32_t h0 = q >= (uint32_t)kHalo ? q - kHalo : 0;
     const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + h0) & ~(uintptr_t)15;
     const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + qe) + 15) & ~(uintptr_t)15;
     const uint32_t bytes = active ? (uint32_t)(g1 - g0) : 0u;
     uint64_t *slot = slots + lane * kSlotWords;
+    constexpr uint32_t kArrivals = 32;
+#endif
     // stream word p is slot[p - sbase] (sbase = h0 or h0 - 1 after the widening: -1 at a
     // stream that starts 8 bytes into a 16-byte line)
     const int64_t sbase = ((intptr_t)g0 - reinterpret_cast<intptr_t>(s)) / 8;
     const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
     if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar_s) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_s), "r"(kArrivals) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
@@ -130,13 +154,13 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
                          (uint32_t)__cvta_generic_to_shared(slot)),
                      "l"(g0), "r"(bytes), "r"(bar_s)
                      : "memory");
-    } else {
+    } else if (kArrivals == 32 || lane == 0) {
         asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar_s) : "memory");
     }
     // the previous block's exit is published by now in the common case: fetch it while
     // the copies land
     uint64_t link_prev = 0;
-    if (blk > 0 && lane == 0) link_prev = ld_acquire(a.link + a.link_base[stream] + blk - 1);
+    if (blk > 0 && lane == 0) link_prev = ld_link(a.link + a.link_base[stream] + blk - 1);
     {
         uint32_t done = 0;
         while (!done)
@@ -149,19 +173,21 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     // speculative entry: the landing most of the kHalo hypotheses agree on (smallest on a tie)
     uint32_t entry = q;
     if (active && q > 0) {
-        uint64_t land[kHalo];
+        // landings saturate at 2^32 - 1 (beyond any stream): never a valid entry
+        uint32_t land[kHalo];
 #pragma unroll
         for (int j = kHalo - 1; j >= 0; --j) {
             const uint32_t h = q - kHalo + j;
-            const uint64_t nx = (uint64_t)h + 1 + (slot[(int64_t)h - sbase] >> 33);
-            uint64_t v = nx;
+            const uint64_t nx64 = (uint64_t)h + 1 + (slot[(int64_t)h - sbase] >> 33);
+            const uint32_t nx = nx64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)nx64;
+            uint32_t v = nx;
 #pragma unroll
             for (int k = j + 1; k < kHalo; ++k)
-                if (nx == (uint64_t)(q - kHalo + k)) v = land[k];
+                if (nx == q - kHalo + k) v = land[k];
             land[j] = v;
         }
         int best = 0;
-        uint64_t pick = ~0ull;
+        uint32_t pick = 0xFFFFFFFFu;
 #pragma unroll
         for (int j = 0; j < kHalo; ++j) {
             int c = 0;
@@ -172,7 +198,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
                 pick = land[j];
             }
         }
-        entry = (uint32_t)min(pick, (uint64_t)L + 1);
+        entry = min(pick, L + 1);
     }
     // walk from slot index i to the first chain position >= qe, summing the words the
     // markers cover (i stays < 2^32: it is < qe - sbase before a step, dirty < 2^31)
@@ -199,7 +225,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
             int spins = 0;
             while (link_prev == ~0ull) {
                 if (++spins > 4) __nanosleep(64);
-                link_prev = ld_acquire(lk);
+                link_prev = ld_link(lk);
             }
             n_in = link_prev & 0xFFFFFFFFull;
             p_in = link_prev >> 32;
@@ -242,7 +268,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const bool last_block = blk + 1 == a.nblocks[stream];
     if (lane == 31) {
         const uint64_t ex = min(x_end, (uint64_t)L + 1), pe = min(p_end, total + 1);
-        if (!last_block) st_release(a.link + a.link_base[stream] + blk, ex | (pe << 32));
+        if (!last_block) st_link(a.link + a.link_base[stream] + blk, ex | (pe << 32));
         else {
             if (x_end > L) dir_fail(a, DIR_ERR_TRUNCATED, stream);
             else if (p_end > total) dir_fail(a, DIR_ERR_OVERLONG, stream);
@@ -258,33 +284,42 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     uint64_t nb = max((pos0 + kRleTile - 1) / kRleTile * kRleTile, r0);
     uint2 *drow = a.dir + ((nb / kRleTile) - a.tile0) * (uint64_t)a.n + stream;
     if (nb >= rlim) nb = ~0ull;
-    const uint64_t tail_at = a.tail_mask ? total : ~0ull;  // the marker ending there has its last word checked
     uint64_t pos = pos0;
     uint32_t i = active ? (uint32_t)((int64_t)entry - sbase) : iend;
-    while (i < iend) {
-        const uint64_t w = slot[i];
-        const uint32_t dirty = (uint32_t)(w >> 33);
-        const uint64_t end = pos + (uint32_t)(w >> 1) + dirty;
-        if (end > nb) {
-            const uint2 v = make_uint2((uint32_t)((int64_t)i + sbase), (uint32_t)pos);
-            do {
+    auto dir_walk = [&](auto tail_check) {
+        while (i < iend) {
+            const uint64_t w = slot[i];
+            const uint32_t dirty = (uint32_t)(w >> 33);
+            const uint64_t end = pos + (uint32_t)(w >> 1) + dirty;
+            if (end > nb) {  // the marker covers boundary nb (< rlim)
+                const uint2 v = make_uint2((uint32_t)((int64_t)i + sbase), (uint32_t)pos);
                 *drow = v;
                 drow += a.n;
                 nb += kRleTile;
-            } while (end > nb && nb < rlim);
-            if (nb >= rlim) nb = ~0ull;
-        }
-        if (end >= tail_at && end == total && end > pos) {
-            // bits >= r in the last word (bitmaps.py:70-72 via decompress :428-431)
-            const uint64_t p = (uint64_t)((int64_t)i + sbase);
-            if (dirty == 0) {
-                if (w & 1) dir_fail(a, DIR_ERR_BEYOND_R, stream);
-            } else if (p + dirty < L && (__ldg(s + p + dirty) & ~a.tail_mask)) {
-                dir_fail(a, DIR_ERR_BEYOND_R, stream);
+                if (end > nb || nb >= rlim) {  // rare: a fill longer than a tile, or the range's end
+                    for (; end > nb && nb < rlim; nb += kRleTile, drow += a.n) *drow = v;
+                    if (nb >= rlim) nb = ~0ull;
+                }
             }
+            tail_check(w, dirty, end);
+            pos = end;
+            i += 1 + dirty;
         }
-        pos = end;
-        i += 1 + dirty;
+    };
+    if (a.tail_mask) {
+        dir_walk([&](uint64_t w, uint32_t dirty, uint64_t end) {
+            // bits >= r in the last word (bitmaps.py:70-72 via decompress :428-431)
+            if (end == total && end > pos) {
+                const uint64_t p = (uint64_t)((int64_t)i + sbase);
+                if (dirty == 0) {
+                    if (w & 1) dir_fail(a, DIR_ERR_BEYOND_R, stream);
+                } else if (p + dirty < L && (__ldg(s + p + dirty) & ~a.tail_mask)) {
+                    dir_fail(a, DIR_ERR_BEYOND_R, stream);
+                }
+            }
+        });
+    } else {
+        dir_walk([](uint64_t, uint32_t, uint64_t) {});
     }
     // rows past the stream's coverage: exhausted stream, implicit zero tail
     if (last_block && p_end <= total) {

@@ -140,7 +140,7 @@ class ThresholdQuery:
         begin, end = (0, (1 << 64) - 1) if word_range is None else (int(word_range[0]), int(word_range[1]))
         self._spans = _lib.spans(pairs)
         h = ctypes.c_void_p()
-        _lib.check(self._lib.bq_query_create(self._spans, self.n, self.r_bits, begin, end,
+        _lib.check(self._lib.bq_query_create(self._spans.ctypes.data, self.n, self.r_bits, begin, end,
                                              self.device.index, ctypes.byref(h)), "bq_query_create")
         self._h = h
         self.out_words = int(self._lib.bq_query_out_words(h))
@@ -207,18 +207,45 @@ class RleQuery:
         self.device = _device(device if device is not None else d)
         self.n = len(streams)
         self.r_bits = int(r_bits)
-        self._keep = []
-        pairs = []
-        for s in streams:
-            t, n_words = (s.data, s.n_words) if isinstance(s, DeviceRleBitmap) else (s, s.numel())
-            if not t.is_cuda:
-                raise InputError("RLE streams must be CUDA tensors")
-            self._keep.append(t)
-            pairs.append((t.data_ptr() if n_words else 0, n_words))
-        self._spans = _lib.spans(pairs)
+        # one pass per column (a fresh query over 1024 streams is ~1 ms of device work,
+        # so the marshalling stays vectorised: no per-stream ctypes structs)
+        ts = [s.data if isinstance(s, DeviceRleBitmap) else s for s in streams]
+        nws = [s.n_words if isinstance(s, DeviceRleBitmap) else s.numel() for s in streams]
+        if not all(t.is_cuda for t in ts):
+            raise InputError("RLE streams must be CUDA tensors")
+        self._keep = ts
+        self._spans = _lib.span_columns([t.data_ptr() if n else 0 for t, n in zip(ts, nws)], nws)
+        self._create(word_range)
+
+    @classmethod
+    def from_packed(cls, flat, offsets, lengths, r_bits: int, device=None, word_range=None):
+        """A query over streams packed in one device tensor: stream i is
+        ``flat[offsets[i] : offsets[i] + lengths[i]]`` (words).  No per-stream Python
+        objects: the span table is computed with numpy (a BQDS-style dataset or a
+        batch of uploaded streams)."""
+        if not isinstance(flat, torch.Tensor) or not flat.is_cuda or flat.dtype not in (torch.int64, torch.uint64):
+            raise InputError("packed streams must be an int64/uint64 CUDA tensor")
+        offs = np.asarray(offsets, dtype=np.uint64)
+        lens = np.asarray(lengths, dtype=np.uint64)
+        if offs.shape != lens.shape or offs.ndim != 1:
+            raise InputError("offsets and lengths must be 1-D and of equal length")
+        if offs.size and int((offs + lens).max()) > flat.numel():
+            raise InputError("a packed stream extends past the buffer")
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self.device = _device(device if device is not None else flat.device)
+        self.n = int(offs.size)
+        self.r_bits = int(r_bits)
+        self._keep = [flat]
+        ptrs = np.where(lens > 0, np.uint64(flat.data_ptr()) + offs * np.uint64(8), np.uint64(0))
+        self._spans = _lib.span_columns(ptrs, lens)
+        self._create(word_range)
+        return self
+
+    def _create(self, word_range):
         h = ctypes.c_void_p()
         w0, w1 = word_range if word_range is not None else (0, word_count(self.r_bits))
-        _lib.check(self._lib.bq_rle_query_create_range(self._spans, self.n, self.r_bits, int(w0), int(w1),
+        _lib.check(self._lib.bq_rle_query_create_range(self._spans.ctypes.data, self.n, self.r_bits, int(w0), int(w1),
                                                        self.device.index, ctypes.byref(h)), "bq_rle_query_create")
         self._h = h
         self.word_range = (int(w0), int(w0) + int(self._lib.bq_rle_query_out_words(h)))
