@@ -900,6 +900,172 @@ def run_c5(args, torch, bq, lib, dev, stream, ctx):
     return line
 
 
+def run_frows(args, torch, bq, lib, dev, stream, ctx):
+    """SURVEY §8(f) rows, each timed with CUDA events after an L2 flush (inputs are
+    read from HBM), with its algorithmic bytes:
+
+    * set algebra (f2): bq_binary_op AND / OR / XOR / ANDNOT of two C2 bitmaps
+      (2^28 bits: 32 MiB each) and NOT of one;
+    * the canonical RLE encoder (f1, K7): the C2 T=16 result (2^28 bits, mixed) and a
+      dense Bernoulli(0.5) 2^28-bit bitmap (all literals);
+    * an NVRTC-compiled straight-line program (f3): CircuitLibrary(64, 'sideways')
+      .program(64, 32) (SSum, majority) over the C2 inputs, next to the counting
+      kernel on the same query;
+    * the drop-in path (b): api.scan_count on the reference's own UncompressedBitmap
+      objects at C1 (host lists in, host list out), next to the reference's own
+      scan_count and its fastest algorithm on the same objects."""
+    from paper_1402_4073_b200 import api
+
+    n, nw = C2_N, C2_WORDS
+    qs = [lib.bq_gen_density_q16(SEED, i, DENS_LO, DENS_HI) for i in range(n)]
+    data = torch.empty((n, nw), dtype=torch.int64, device=dev)
+    qarr = np.asarray(qs, dtype=np.uint32)
+    _lib_check(lib.bq_gen_bernoulli_rows(SEED, 0, n, qarr.ctypes.data, 0, nw, data.data_ptr(), nw,
+                                         stream.cuda_stream))
+    out = torch.empty(nw, dtype=torch.int64, device=dev)
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    lnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = lambda: _l2_flush(scratch)  # noqa: E731
+    peak, _ = measured_peak()
+    steps = max(5, min(args.steps, 50))
+    res = {}
+
+    def rec(name, ms, nbytes, extra=None):
+        m = statistics.median(ms)
+        d = {"median_ms": round(m, 5), "algorithmic_bytes": int(nbytes),
+             "gbs": round(nbytes / (m / 1e3) / 1e9, 1), "frac_of_peak": round(nbytes / (m / 1e3) / 1e9 / peak, 4)}
+        if extra:
+            d.update(extra)
+        res[name] = d
+
+    a, b = data[0], data[1]
+    for kind, name in ((0, "and"), (1, "or"), (2, "xor"), (3, "andnot"), (4, "not")):
+        def launch(kind=kind):
+            _lib_check(lib.bq_binary_op(kind, a.data_ptr(), nw, b.data_ptr(), nw, 64 * nw, out.data_ptr(),
+                                        pc.data_ptr(), lnz.data_ptr(), stream.cuda_stream))
+        ms = _timed_launches(torch, launch, steps, args.warmup, stream, flush=flush)
+        rec(f"binop_{name}", ms, (1 if kind == 4 else 2) * nw * 8 + nw * 8,
+            {"kernel": "bq::binop_kernel (128-bit streaming loads)"})
+    # the same on operands larger than L2 (8 C2 bitmaps each: 2^25 words = 256 MiB), where
+    # launch ramp and tail no longer dominate
+    big_a, big_b = data[0:8].reshape(-1), data[8:16].reshape(-1)
+    big_out = torch.empty(8 * nw, dtype=torch.int64, device=dev)
+    for kind, name in ((0, "and"), (1, "or"), (4, "not")):
+        def launch(kind=kind):
+            _lib_check(lib.bq_binary_op(kind, big_a.data_ptr(), 8 * nw, big_b.data_ptr(), 8 * nw, 64 * 8 * nw,
+                                        big_out.data_ptr(), pc.data_ptr(), lnz.data_ptr(), stream.cuda_stream))
+        ms = _timed_launches(torch, launch, steps, args.warmup, stream, flush=flush)
+        rec(f"binop_{name}_256mib", ms, ((1 if kind == 4 else 2) + 1) * 8 * nw * 8)
+    del big_out
+    # exactness of the device set algebra on these operands
+    ref_and = (a & b)
+    _lib_check(lib.bq_binary_op(0, a.data_ptr(), nw, b.data_ptr(), nw, 64 * nw, out.data_ptr(), pc.data_ptr(),
+                                lnz.data_ptr(), stream.cuda_stream))
+    res["binop_matches_torch"] = bool(torch.equal(out, ref_and))
+
+    # K7 encoder on the C2 T=16 result and on a dense random bitmap
+    query = bq.ThresholdQuery([data[i] for i in range(n)], 64 * nw)
+    t16 = torch.empty(nw, dtype=torch.int64, device=dev)
+    query.threshold(16, t16, pc, stream=stream)
+    dense = torch.empty((1, nw), dtype=torch.int64, device=dev)
+    q05 = np.asarray([32768], dtype=np.uint32)
+    _lib_check(lib.bq_gen_bernoulli_rows(SEED + 1, 0, 1, q05.ctypes.data, 0, nw, dense.data_ptr(), nw,
+                                         stream.cuda_stream))
+    import ctypes
+    enc = torch.empty(nw + 2, dtype=torch.int64, device=dev)
+    for name, src in (("encode_c2_t16_result", t16), ("encode_dense", dense[0])):
+        n_out = ctypes.c_uint64(0)
+
+        def launch(src=src, n_out=n_out):
+            _lib_check(lib.bq_rle_encode_device(src.data_ptr(), nw, 64 * nw, enc.data_ptr(), nw + 2,
+                                                ctypes.byref(n_out), stream.cuda_stream))
+        ms = _timed_launches(torch, launch, max(5, steps // 2), args.warmup, stream, flush=flush)
+        rec(name, ms, nw * 8 + int(n_out.value) * 8,
+            {"encoded_words": int(n_out.value), "kernel": "K7 (classify / CUB select / size / CUB scan / scatter)",
+             "note": "synchronous call: includes its host round trips"})
+    host_enc = enc[: int(n_out.value)].cpu().numpy().view(np.uint64)
+    from oracle import oracle as O
+    res["encode_matches_oracle"] = bool(np.array_equal(host_enc, O.rle_compress(dense[0].cpu().numpy().view(np.uint64),
+                                                                                64 * nw)))
+
+    # NVRTC SSum(64, 32) program over the C2 inputs, and the counting kernel on the same query
+    lib_c = api.CircuitLibrary(n_max=64, builder="sideways")
+    prog = api.compile_program(lib_c.program(64, 32))
+
+    def launch_prog():
+        prog.run(query, out, pc, lnz, stream=stream)
+    ms = _timed_launches(torch, launch_prog, steps, args.warmup, stream, flush=flush)
+    rec("nvrtc_ssum_64_32", ms, n * nw * 8 + nw * 8, {"gates": lib_c.program(64, 32).op_count,
+                                                        "kernel": "bq_prog (NVRTC, sm_100a)"})
+    prog_out = out.clone()
+    ms = _timed_launches(torch, lambda: query.threshold(32, out, pc, stream=stream), steps, args.warmup, stream,
+                         flush=flush)
+    rec("count_kernel_t32_same_query", ms, n * nw * 8 + nw * 8)
+    res["nvrtc_matches_count_kernel"] = bool(torch.equal(prog_out, out))
+    query.close()
+    del data, dense, scratch
+    torch.cuda.empty_cache()
+
+    # drop-in e2e at C1 through api.scan_count on the reference's own objects
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "bitquorum")):
+        sys.path.insert(0, ref_dir)
+        from bitquorum import bitmaps as rbm
+        from bitquorum import counters
+        from bitquorum.circuits import csv_threshold
+
+        n1, nw1, t1 = 8, 1 << 14, 3
+        ins = [rbm.UncompressedBitmap([int(w) for w in O.gen_bernoulli(SEED, i, 6554, 0, nw1)], 64 * nw1)
+               for i in range(n1)]
+        api.scan_count(ins, t1)  # warm: upload cache and query cache hold these objects afterwards
+        times = []
+        for _ in range(5):
+            # fresh objects each time: the full drop-in cost (upload, query, download, list result)
+            fresh = [rbm.UncompressedBitmap(list(b.words), b.bit_length) for b in ins]
+            t0 = time.perf_counter()
+            got = api.scan_count(fresh, t1)
+            times.append(time.perf_counter() - t0)
+        cached = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            api.scan_count(ins, t1)
+            cached.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        exp = counters.scan_count(ins, t1)
+        ref_sc = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        csv_threshold(ins, t1)
+        ref_csv = time.perf_counter() - t0
+        nbytes = n1 * nw1 * 8
+        res["drop_in_c1"] = {
+            "api": "paper_1402_4073_b200.scan_count(reference UncompressedBitmap objects)",
+            "fresh_objects_ms": round(statistics.median(times) * 1e3, 3),
+            "fresh_objects_gbs": round(nbytes / statistics.median(times) / 1e9, 4),
+            "cached_objects_ms": round(statistics.median(cached) * 1e3, 3),
+            "reference_scan_count_ms": round(ref_sc * 1e3, 1),
+            "reference_csv_threshold_ms": round(ref_csv * 1e3, 1),
+            "matches_reference": bool(got == exp),
+            "note": "host lists in, host list out: upload, query, download and the list result inside the "
+                    "timing; cached = the same objects again (upload and query caches hit)"}
+    line = {"metric": METRIC, "workload": "frows", "unit": "GB/s", "n_gpus": 1, "steps": steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": "u64", "data": "synthetic (seed 1402)",
+            "config": {"workload": "SURVEY §8(f) rows and the drop-in path, each timed after a 256 MB L2 flush"},
+            "rows": res}
+    big = res["binop_and_256mib"]
+    line["value"] = big["gbs"]
+    line["roofline"] = {"bound": "hbm", "achieved": big["gbs"], "peak": peak, "unit": "GB/s",
+                        "frac": big["frac_of_peak"], "kernel": "bq::binop_kernel (AND, 256 MiB operands)",
+                        "traffic": ncu_traffic("binop"),
+                        "algorithmic_bytes_per_launch": big["algorithmic_bytes"],
+                        "mean_launch_ms": big["median_ms"]}
+    line["ms_per_step"] = big["median_ms"]
+    line["gpu_launches"] = 8 * steps
+    line["_rank_bytes"] = big["algorithmic_bytes"]
+    line["_rank_ms"] = big["median_ms"]
+    return line
+
+
 def _lib_check(rc):
     from paper_1402_4073_b200 import _lib
     _lib.check(rc)
@@ -922,7 +1088,7 @@ def run_extra(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     ctx = types.SimpleNamespace(world=world, rank=rank, dist=dist, cpu=(world == 1))
-    fn = {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5}[args.workload]
+    fn = {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5, "frows": run_frows}[args.workload]
     with ClockSampler(physical_gpu_index(local)) as clocks:
         line = fn(args, torch, bq, lib, dev, stream, ctx)
     rank_bytes = float(line.pop("_rank_bytes", line["roofline"]["algorithmic_bytes_per_launch"]))
@@ -975,7 +1141,7 @@ def self_launch(n: int) -> int:
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
-    ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c2",
+    ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5", "frows"), default="c2",
                     help="BASELINE config; c2 (the default) is the headline line")
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
     ap.add_argument("--steps", type=int, default=200)

@@ -112,6 +112,19 @@ BQ_API int bq_threshold_u64(const bq_span *inputs, int n, uint64_t r_bits, int t
 BQ_API int bq_symmetric_u64(const bq_span *inputs, int n, uint64_t r_bits, const uint8_t *h_accept,
                             uint64_t *d_out, unsigned long long *d_popcnt, void *stream);
 
+/* One threshold query sharded by word range over `ngpu` devices of ONE process
+ * (horizontal fragmentation): device g holds words
+ * [w_begin[g], w_end[g]) of every input -- spans[g * n + i] are its local slices
+ * (device pointers on devices[g], local word counts) -- and writes that part of
+ * the result to d_outs[g] (w_end[g] - w_begin[g] words, bits >= r cleared).  The
+ * only exchange is the popcount: the shards' counts are summed into *h_popcnt.
+ * w_begin[g] must be even.  streams (optional): one per shard.  Synchronous.
+ * Multi-process callers create one bq_query per rank over its range instead and
+ * all-reduce the popcount (paper_1402_4073_b200/shard.py: NCCL). */
+BQ_API int bq_shard_threshold(int ngpu, const int *devices, const bq_span *spans, int n, uint64_t r_bits,
+                              const uint64_t *w_begin, const uint64_t *w_end, int t, uint64_t *const *d_outs,
+                              unsigned long long *h_popcnt, void *const *streams);
+
 /* ---- host-buffer path (end to end) ----------------------------------------
  * Evaluate nq queries (thresholds ts[k], or, when ts[k] <= 0, the symmetric
  * spec h_accepts + k*(n+1)) over HOST inputs h_inputs[i] (n_words[i] words,

@@ -46,6 +46,7 @@ SIGNATURES = {
     "bq_query_symmetric": (_I, [_P, _P, _P, _P, _P, _P]),
     "bq_threshold_u64": (_I, [_P, _I, _U64, _I, _P, _P, _P]),
     "bq_symmetric_u64": (_I, [_P, _I, _U64, _P, _P, _P, _P]),
+    "bq_shard_threshold": (_I, [_I, _P, _P, _I, _U64, _P, _P, _I, _P, _P, _P]),
     "bq_sweep_host": (_I, [_P, _P, _I, _U64, _P, _P, _I, _P, _P, _I, _U64]),
     "bq_release_workspace": (None, []),
     "bq_rle_query_create": (_I, [_P, _I, _U64, _I, _P]),

@@ -853,3 +853,56 @@ BQ_API int bq_gen_markov_rle(uint64_t seed, uint32_t bitmap, uint64_t r_bits, do
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// one query sharded by word range over several devices of one process (SURVEY
+// §8(e)): each device evaluates its slice; the only exchange is the popcount sum
+
+extern "C" BQ_API int bq_shard_threshold(int ngpu, const int *devices, const bq_span *spans, int n, uint64_t r_bits,
+                              const uint64_t *w_begin, const uint64_t *w_end, int t, uint64_t *const *d_outs,
+                              unsigned long long *h_popcnt, void *const *streams) {
+    if (ngpu < 1 || !devices || !spans || !w_begin || !w_end || !d_outs) return set_error(BQ_EINPUT, "NULL argument");
+    if (n < 1 || n > BQ_MAX_INPUTS) return set_error(BQ_EINPUT, "bad input count %d", n);
+    const uint64_t total = word_count(r_bits);
+    std::vector<bq_query *> qs(ngpu, nullptr);
+    std::vector<unsigned long long *> d_pc(ngpu, nullptr);
+    int rc = BQ_OK;
+    DeviceGuard dg;
+    for (int g = 0; g < ngpu && rc == BQ_OK; ++g) {
+        if (w_begin[g] > w_end[g] || w_end[g] > total || (w_begin[g] & 1))
+            rc = set_error(BQ_EINPUT, "shard %d: bad word range", g);
+        if (rc) break;
+        // the shard's inputs are local slices: present them as windows of the whole
+        // bitmaps (only words >= w_begin are ever read)
+        std::vector<bq_span> in(n);
+        for (int i = 0; i < n; ++i) {
+            const bq_span &sp = spans[(size_t)g * n + i];
+            in[i].words = sp.n_words ? sp.words - w_begin[g] : nullptr;
+            in[i].n_words = sp.n_words ? w_begin[g] + sp.n_words : 0;
+        }
+        rc = bq_query_create(in.data(), n, r_bits, w_begin[g], w_end[g], devices[g], &qs[g]);
+        if (rc) break;
+        if ((rc = dg.set(devices[g]))) break;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&d_pc[g]), 8, streams ? (cudaStream_t)streams[g] : 0);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_pc[g], 0, 8, streams ? (cudaStream_t)streams[g] : 0);
+        if (e != cudaSuccess) rc = cuda_error(e, "shard popcount");
+        if (rc == BQ_OK) rc = bq_query_threshold(qs[g], t, d_outs[g], d_pc[g], nullptr, streams ? streams[g] : nullptr);
+    }
+    unsigned long long sum = 0;
+    for (int g = 0; g < ngpu; ++g) {  // the all-reduce of the popcount: 8 bytes per device
+        if (!qs[g]) continue;
+        dg.set(devices[g]);
+        cudaStream_t s = streams ? (cudaStream_t)streams[g] : 0;
+        unsigned long long v = 0;
+        if (d_pc[g]) {
+            cudaError_t e = cudaMemcpyAsync(&v, d_pc[g], 8, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess && rc == BQ_OK) rc = cuda_error(e, "shard popcount");
+            cudaFreeAsync(d_pc[g], s);
+        }
+        sum += v;
+        bq_query_destroy(qs[g]);
+    }
+    if (rc == BQ_OK && h_popcnt) *h_popcnt = sum;
+    return rc;
+}

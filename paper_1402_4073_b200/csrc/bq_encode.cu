@@ -15,6 +15,7 @@
 // -> scan (CUB) -> scatter markers and literal words.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,6 +23,10 @@
 #include "bq_internal.h"
 
 namespace bq {
+
+struct WidenFlag {  // u8 flag -> u32, so the run-id scan accumulates in 32 bits
+    __host__ __device__ uint32_t operator()(uint8_t f) const { return f; }
+};
 
 __device__ __forceinline__ int word_class(const uint64_t *w, uint64_t n_words, uint64_t i) {
     const uint64_t x = i < n_words ? w[i] : 0ull;
@@ -56,29 +61,36 @@ __global__ void enc_sizes_kernel(const uint64_t *w, uint64_t n_words, uint64_t t
     }
 }
 
-__global__ void enc_scatter_kernel(const uint64_t *w, uint64_t n_words, uint64_t total, const uint32_t *cp,
+// One thread per change point: the marker word only (literals: enc_literals_kernel).
+__global__ void enc_markers_kernel(const uint64_t *w, uint64_t n_words, uint64_t total, const uint32_t *cp,
                                    const uint32_t *n_cp, const uint32_t *sizes, const uint64_t *offs, uint64_t *out) {
     const uint32_t m = *n_cp;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
-        if (!sizes[j]) continue;
+        const uint32_t sz = sizes[j];
+        if (!sz) continue;
         const uint64_t p = cp[j];
         const int c = word_class(w, n_words, p);
-        const uint64_t q = (j + 1 < m) ? cp[j + 1] : total;
-        uint64_t bit = 0, run = 0, d0 = 0, nd = 0;
+        uint64_t bit = 0, run = 0;
         if (c < 2) {
             bit = (uint64_t)c;
-            run = q - p;
-            if (j + 1 < m && word_class(w, n_words, q) == 2) {
-                d0 = q;
-                nd = ((j + 2 < m) ? cp[j + 2] : total) - q;
-            }
-        } else {  // leading dirty run
-            d0 = p;
-            nd = q - p;
+            run = ((j + 1 < m) ? cp[j + 1] : total) - p;
         }
-        uint64_t *o = out + offs[j];
-        o[0] = bit | (run << 1) | (nd << 33);  // bitmaps.py:35-36
-        for (uint64_t k = 0; k < nd; ++k) o[1 + k] = w[d0 + k];
+        out[offs[j]] = bit | (run << 1) | ((uint64_t)(sz - 1) << 33);  // bitmaps.py:35-36
+    }
+}
+
+// One thread per word: a literal word i in dirty run k (runid[i] = k + 1) goes right
+// after its marker -- marker k - 1 (the fill run before it) or, for a leading dirty
+// run, marker 0 -- at offset i - cp[k] within the group.  Coalesced over words, so a
+// long literal run costs no more than its bytes.
+__global__ void enc_literals_kernel(const uint64_t *w, uint64_t n_words, const uint32_t *runid, const uint32_t *cp,
+                                    const uint64_t *offs, uint64_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_words; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = w[i];
+        if (x == 0ull || x == ~0ull) continue;
+        const uint32_t k = runid[i] - 1;
+        const uint32_t m = k ? k - 1 : 0;
+        out[offs[m] + 1 + (i - cp[k])] = x;
     }
 }
 
@@ -96,24 +108,27 @@ extern "C" BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_w
     if (n_words && !d_words) return set_error(BQ_EINPUT, "d_words is NULL");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // scratch: flags (u8), idx iterator output cp (u32), n_cp, sizes (u32), offs (u64), cub temp
-    size_t t_sel = 0, t_scan = 0;
+    size_t t_sel = 0, t_scan = 0, t_run = 0;
     thrust::counting_iterator<uint32_t> it(0);
     cub::DeviceSelect::Flagged(nullptr, t_sel, it, (uint8_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                (int)total, s);
     cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (uint32_t *)nullptr, (uint64_t *)nullptr, (int)total, s);
+    auto wide = thrust::make_transform_iterator((const uint8_t *)nullptr, WidenFlag());
+    cub::DeviceScan::InclusiveSum(nullptr, t_run, wide, (uint32_t *)nullptr, (int)total, s);
     const size_t a_flags = (total + 255) & ~(size_t)255;
     const size_t a_cp = ((total * 4) + 255) & ~(size_t)255;
     const size_t a_off = ((total + 1) * 8 + 255) & ~(size_t)255;
-    const size_t a_tmp = (std::max(t_sel, t_scan) + 255) & ~(size_t)255;
-    const size_t bytes = a_flags + 2 * a_cp + a_off + a_tmp + 256;
+    const size_t a_tmp = (std::max(std::max(t_sel, t_scan), t_run) + 255) & ~(size_t)255;
+    const size_t bytes = a_flags + 3 * a_cp + a_off + a_tmp + 256;
     char *base = nullptr;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&base), bytes, s);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(encoder scratch)");
     uint8_t *flags = reinterpret_cast<uint8_t *>(base);
     uint32_t *cp = reinterpret_cast<uint32_t *>(base + a_flags);
     uint32_t *sizes = reinterpret_cast<uint32_t *>(base + a_flags + a_cp);
-    uint64_t *offs = reinterpret_cast<uint64_t *>(base + a_flags + 2 * a_cp);
-    void *tmp = base + a_flags + 2 * a_cp + a_off;
+    uint32_t *runid = reinterpret_cast<uint32_t *>(base + a_flags + 2 * a_cp);
+    uint64_t *offs = reinterpret_cast<uint64_t *>(base + a_flags + 3 * a_cp);
+    void *tmp = base + a_flags + 3 * a_cp + a_off;
     uint32_t *n_cp = reinterpret_cast<uint32_t *>(base + bytes - 256);
     int rc = BQ_OK;
     const int threads = 256;
@@ -145,7 +160,13 @@ extern "C" BQ_API int bq_rle_encode_device(const uint64_t *d_words, uint64_t n_w
             rc = set_error(BQ_EINPUT, "d_out is NULL");
             break;
         }
-        enc_scatter_kernel<<<grid, threads, 0, s>>>(d_words, n_words, total, cp, n_cp, sizes, offs, d_out);
+        enc_markers_kernel<<<grid, threads, 0, s>>>(d_words, n_words, total, cp, n_cp, sizes, offs, d_out);
+        if (n_words) {  // run id of every word (1-based change-point index), then the literals
+            t = a_tmp;
+            auto fl = thrust::make_transform_iterator((const uint8_t *)flags, WidenFlag());
+            if ((e = cub::DeviceScan::InclusiveSum(tmp, t, fl, runid, (int)n_words, s)) != cudaSuccess) break;
+            enc_literals_kernel<<<grid, threads, 0, s>>>(d_words, n_words, runid, cp, offs, d_out);
+        }
         if ((e = cudaGetLastError()) != cudaSuccess) break;
         e = cudaStreamSynchronize(s);
     } while (0);

@@ -48,7 +48,13 @@ namespace bq {
 
 constexpr int kSlotsPerBatch = 512;   // undecided words resolved per phase-C pass
 constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
-constexpr int kPoolWords = 768;         // words per warp pool half (two halves: double buffer);
+#ifndef BQ_K4_POOL
+#define BQ_K4_POOL 768
+#endif
+#ifndef BQ_K4_MINB
+#define BQ_K4_MINB 4
+#endif
+constexpr int kPoolWords = BQ_K4_POOL;  // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
 constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
 
@@ -379,7 +385,7 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
 // the segment with one TMA bulk copy while the previous batch is being walked;
 // one mbarrier per pool half, so the warps never meet at a CTA barrier in phase
 // A.  A segment that does not fit the pool is walked straight from HBM.
-__global__ void __launch_bounds__(kStagedThreads, 4) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
+__global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
     constexpr int NT = kStagedThreads;
     constexpr int kSlots = kSlotsPerBatch;
     extern __shared__ __align__(16) uint8_t rle_smem[];

@@ -105,3 +105,15 @@ def test_gpus_flag_launches_its_own_ranks():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["matches_device_result"]
     c5 = d["c5_strong_scaling"]
     assert c5["n_gpus"] == 2 and c5["waves_per_rank"] == 4 and c5["input_bytes"] == 511 * (1 << 26) * 8
+
+
+def test_frows_line():
+    """The §8(f) rows and the drop-in path, each with its bytes and an exactness check."""
+    d = _bench("--workload", "frows", "--steps", "5", "--warmup", "3")
+    rows = d["rows"]
+    for k in ("binop_and", "binop_or", "binop_xor", "binop_andnot", "binop_not", "encode_dense",
+              "encode_c2_t16_result", "nvrtc_ssum_64_32", "count_kernel_t32_same_query"):
+        assert rows[k]["median_ms"] > 0 and rows[k]["gbs"] > 0, k
+    assert rows["binop_matches_torch"] and rows["encode_matches_oracle"] and rows["nvrtc_matches_count_kernel"]
+    if "drop_in_c1" in rows:
+        assert rows["drop_in_c1"]["matches_reference"]
