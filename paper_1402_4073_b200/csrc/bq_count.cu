@@ -373,46 +373,66 @@ __device__ __forceinline__ ulonglong2 ld_stream2(const uint64_t *p) {
 // operands (the host falls back to word loads otherwise); words past an operand's
 // length read as zero; the popcount and last nonzero index are fused.
 template <int KIND, bool VEC>
+__device__ __forceinline__ void binop_pair(const uint64_t *__restrict__ a, uint64_t na, const uint64_t *__restrict__ b,
+                                           uint64_t nb, uint64_t w, ulonglong2 &x, ulonglong2 &y) {
+    if (VEC && w + 1 < na) {
+        x = ld_stream2(a + w);
+    } else {
+        x.x = w < na ? __ldg(a + w) : 0ull;
+        x.y = w + 1 < na ? __ldg(a + w + 1) : 0ull;
+    }
+    y = make_ulonglong2(0ull, 0ull);
+    if (KIND != 4) {
+        if (VEC && w + 1 < nb) {
+            y = ld_stream2(b + w);
+        } else {
+            y.x = w < nb ? __ldg(b + w) : 0ull;
+            y.y = w + 1 < nb ? __ldg(b + w + 1) : 0ull;
+        }
+    }
+}
+
+// Two words per thread, four pairs in flight: 128-bit streaming loads and stores
+// over 16-byte-aligned operands (the host falls back to word loads otherwise);
+// words past an operand's length read as zero; the popcount and last nonzero
+// index are fused.
+template <int KIND, bool VEC>
 __global__ void __launch_bounds__(256) binop_kernel(const uint64_t *__restrict__ a, uint64_t na,
                                                    const uint64_t *__restrict__ b, uint64_t nb, uint64_t nwords,
                                                    uint64_t last_mask, uint64_t *__restrict__ out,
                                                    unsigned long long *popcnt, unsigned long long *last_nz) {
+    constexpr int U = 4;
     unsigned long long pc = 0, lnz = 0;
     const uint64_t npairs = (nwords + 1) / 2;
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t w = 2 * p;
-        ulonglong2 x, y = make_ulonglong2(0ull, 0ull);
-        if (VEC && w + 1 < na) {
-            x = ld_stream2(a + w);
-        } else {
-            x.x = w < na ? __ldg(a + w) : 0ull;
-            x.y = w + 1 < na ? __ldg(a + w + 1) : 0ull;
-        }
-        if (KIND != 4) {
-            if (VEC && w + 1 < nb) {
-                y = ld_stream2(b + w);
-            } else {
-                y.x = w < nb ? __ldg(b + w) : 0ull;
-                y.y = w + 1 < nb ? __ldg(b + w + 1) : 0ull;
-            }
-        }
-        uint64_t r0 = binop<KIND>(x.x, y.x), r1 = binop<KIND>(x.y, y.y);
-        if (w + 1 < nwords) {
-            if (w + 2 == nwords) r1 &= last_mask;
-            if (VEC) {
-                *reinterpret_cast<ulonglong2 *>(out + w) = make_ulonglong2(r0, r1);
-            } else {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npairs; p0 += U * stride) {
+        ulonglong2 x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (p0 + u * stride < npairs) binop_pair<KIND, VEC>(a, na, b, nb, 2 * (p0 + u * stride), x[u], y[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t p = p0 + u * stride;
+            if (p >= npairs) break;
+            const uint64_t w = 2 * p;
+            uint64_t r0 = binop<KIND>(x[u].x, y[u].x), r1 = binop<KIND>(x[u].y, y[u].y);
+            if (w + 1 < nwords) {
+                if (w + 2 == nwords) r1 &= last_mask;
+                if (VEC) {
+                    *reinterpret_cast<ulonglong2 *>(out + w) = make_ulonglong2(r0, r1);
+                } else {
+                    out[w] = r0;
+                    out[w + 1] = r1;
+                }
+                pc += __popcll(r0) + __popcll(r1);
+                if (r1) lnz = max(lnz, (unsigned long long)(w + 2));
+                else if (r0) lnz = max(lnz, (unsigned long long)(w + 1));
+            } else {  // the odd last word
+                r0 &= last_mask;
                 out[w] = r0;
-                out[w + 1] = r1;
+                pc += __popcll(r0);
+                if (r0) lnz = max(lnz, (unsigned long long)(w + 1));
             }
-            pc += __popcll(r0) + __popcll(r1);
-            if (r1) lnz = w + 2;
-            else if (r0) lnz = w + 1;
-        } else {  // the odd last word
-            r0 &= last_mask;
-            out[w] = r0;
-            pc += __popcll(r0);
-            if (r0) lnz = w + 1;
         }
     }
 #pragma unroll

@@ -180,10 +180,13 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
 // Rows [tile0, tile0 + nrows) of dir[row][stream] = (index of the marker covering
 // tile boundary row * kRleTile, word where its fill starts), streams validated
 // (err_code 1 truncated literal group, 2 coverage beyond total_words, 3 set bits
-// >= r; 0 valid; err_stream the first failing stream).  Synchronous.
+// >= r; 0 valid; err_stream the first failing stream).  d_scratch: device memory of
+// rle_directory_scratch_bytes(lens) bytes.  Synchronous.
 int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const std::vector<uint64_t> &lens,
                         uint64_t total_words, uint64_t tail_mask, uint32_t tile0, uint32_t nrows, uint2 *d_dir,
-                        int *err_code, uint64_t *err_stream);
+                        void *d_scratch, int *err_code, uint64_t *err_stream);
+// device scratch bytes build_rle_directory needs for these stream lengths
+size_t rle_directory_scratch_bytes(const std::vector<uint64_t> &lens);
 
 // ---- K5 generator kernels --------------------------------------------------
 int launch_gen_rows(uint64_t seed, uint32_t first, int count, const uint32_t *d_q16s, uint64_t w0,

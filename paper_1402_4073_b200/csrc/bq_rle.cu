@@ -6,15 +6,10 @@
 // followed by that many literal ("dirty") words; coverage shorter than
 // ceil(r/64) words is an implicit zero tail (bitmaps.py:215-219).
 //
-// K3 the tile directory, once per query object (inputs are immutable):
-//   K3a rle_chain_kernel -- one warp per stream follows the marker chain in
-//   32-word windows (pointer doubling + warp OR-reductions find a window's
-//   markers; windows are cp.async-staged ahead; dirty runs longer than the ring
-//   are skipped unread) and keeps per window only its marker mask and start
-//   position.  K3b rle_dirfill_kernel -- every window in parallel: marker word
-//   positions by a warp prefix sum, the validation of
-//   RleBitmap.iter_word_segments (:210-217; FormatError), and a directory entry
-//   (marker index, run start) for every tile boundary a marker's runs cover.
+// K3 the tile directory, once per query object (inputs are immutable): the marker
+//   covering every tile boundary, found in one streaming pass with speculative
+//   per-segment walks and a decoupled look-back across blocks (bq_rle_dir.cu),
+//   which also validates the streams as RleBitmap.iter_word_segments (:210-217).
 //
 // K4 rle_count_kernel -- one CTA per tile of kTileWords output words, the
 //   per-tile form of cdom's run sweep (runmerge.py:198-299):
@@ -66,217 +61,7 @@ inline size_t rle_smem_bytes() {
     return kCntBytes + kRegionBytes;
 }
 
-enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };
-
-struct RleDirArgs {
-    const uint64_t *const *ptrs;
-    const uint64_t *lens;
-    int n;
-    uint64_t total_words;  // ceil(r/64)
-    uint64_t tail_mask;    // valid bits of the last word when r % 64 != 0, else 0
-    uint32_t tile0;        // first tile of the query's word range
-    uint32_t nrows;        // directory rows: the range's tiles + 1 (the boundary after its last tile)
-    uint2 *dir;            // [nrows][n]: (marker index, run start word); tile-major so a K4 CTA reads one row
-    int *err;              // first error code
-    unsigned long long *err_stream;
-};
-
-__device__ __forceinline__ void rle_fail(const RleDirArgs &a, int code, int stream) {
-    if (atomicCAS(a.err, 0, code) == 0) atomicExch(a.err_stream, (unsigned long long)stream);
-}
-
-// K3: one warp per stream.  The stream is read in 32-word windows aligned to its
-// start, so window loads do not wait for the marker chain: the next window is
-// loaded while the current one is decoded (a dirty group reaching past the next
-// window jumps straight to the window of the next marker, skipping literals
-// unread).  Inside a window, the markers on the chain from every possible entry
-// are found at once by pointer jumping; following the chain is a lookup per
-// window; marker word positions come from a warp prefix sum in K3b.
-constexpr int kDirAhead = 14;  // windows in flight ahead of the one being decoded
-constexpr int kDirRing = 16;  // ring slots per warp (> kDirAhead: consumed slots are reused late)
-#ifndef BQ_CHAIN_GROUP
-#define BQ_CHAIN_GROUP 4
-#endif
-constexpr int kChainGroup = BQ_CHAIN_GROUP;  // K3a: windows whose chain tables are computed together
-
-// K3a: the sequential part of the directory -- one warp per stream follows its
-// marker chain window by window (windows copied into a per-warp ring by per-lane
-// cp.async, kDirAhead ahead; a literal group reaching past the ring restarts it
-// at the next marker, so long dirty runs are skipped unread).  The chain's
-// dependency from window to window is kept short: for every window the warp
-// first computes, for all 32 possible entry lanes at once, where the chain from
-// that entry leaves the window, which markers it passes and the words they cover
-// (pointer jumping: five levels, each combining a lane's aggregate with the one at
-// its successor), which does not depend on the actual entry; several windows'
-// tables are computed interleaved (kChainGroup windows).  Following the chain is then a lookup (a
-// shuffle from the entry lane) per window.  Only two facts per window are kept:
-// its marker mask and the word position where its first marker's fill starts.
-// Everything else -- marker positions, validation, directory rows -- is K3b, in
-// parallel over all windows.
-struct ChainTable {
-    uint32_t m;   // markers on the chain from this lane, within the window
-    uint32_t nx;  // where the chain leaves: window-relative index of its next marker (>= 32, or a lane past L)
-};
-
-// This lane's entry of a window's chain table (word w at index bc + lane, valid:
-// bc + lane < L).
-__device__ __forceinline__ ChainTable chain_table(uint64_t w, bool valid, int lane) {
-    ChainTable t;
-    t.m = valid ? 1u << lane : 0u;
-    t.nx = valid ? (uint32_t)lane + 1u + (uint32_t)(w >> 33) : (uint32_t)lane;  // dirty < 2^31
-    return t;
-}
-
-__device__ __forceinline__ void chain_jump(ChainTable &t, int lane) {
-    const bool on = t.nx < 32u;
-    const int src = on ? (int)t.nx : lane;
-    const uint32_t m = __shfl_sync(0xffffffffu, t.m, src);
-    const uint32_t nx = __shfl_sync(0xffffffffu, t.nx, src);
-    t.m |= on ? m : 0u;
-    t.nx = on ? nx : t.nx;
-}
-
-// Words covered by the fills and literal groups of the window's markers in `reach`
-// (each span < 2^40: the two 24-bit-split sums stay exact).
-__device__ __forceinline__ uint64_t chain_span(uint64_t w, uint32_t reach, int lane) {
-    const uint64_t span = ((reach >> lane) & 1u) ? ((w >> 1) & 0xFFFFFFFFull) + (w >> 33) : 0ull;
-    const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)(span & 0xFFFFFFu));
-    const uint32_t hi = __reduce_add_sync(0xffffffffu, (uint32_t)(span >> 24));
-    return ((uint64_t)hi << 24) + lo;
-}
-
-__global__ void __launch_bounds__(128) rle_chain_kernel(const __grid_constant__ RleDirArgs a, const uint64_t *wbase,
-                                                        uint32_t *wreach, uint64_t *wpos) {
-    __shared__ uint64_t ring_all[4][kDirRing][32];
-    const int lane = threadIdx.x & 31;
-    const int stream = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    if (stream >= a.n) return;
-    uint64_t(*ring)[32] = ring_all[threadIdx.x >> 5];
-    const uint64_t *s = a.ptrs[stream];
-    const uint64_t L = a.lens[stream];
-    uint2 *dir = a.dir + stream;  // stride n between tiles
-    const uint64_t wb = wbase[stream];
-    auto issue = [&](uint64_t q) {
-        const uint64_t idx = q * 32 + lane;
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ring[q % kDirRing][lane]);
-        const uint64_t *src = s + (idx < L ? idx : 0);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(idx < L ? 8u : 0u)
-                     : "memory");
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    constexpr int G = kChainGroup;  // windows whose tables are computed per iteration
-    uint64_t k = 0;     // first window of the group being decoded
-    uint64_t next = 0;  // stream index of the next marker
-    uint64_t pos = 0;   // word position where its fill run starts
-    for (int q = 0; q < kDirAhead; ++q) issue(q);
-    while (next < L) {
-        const uint64_t kk = next / 32;
-        if (kk + G - 1 >= k + kDirAhead) {  // a long literal group: restart the pipeline at the next marker
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-            k = kk;
-            for (int q = 0; q < kDirAhead; ++q) issue(k + q);
-        } else {
-            for (; k < kk; ++k) issue(k + kDirAhead);  // windows of literals only
-        }
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDirAhead - G) : "memory");
-        // tables of windows k .. k + G - 1 (independent of the entry; interleaved)
-        const uint64_t bc0 = k * 32;
-        uint64_t w[G];
-        ChainTable t[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            w[g] = ring[(k + g) % kDirRing][lane];
-            t[g] = chain_table(w[g], bc0 + 32 * g + lane < L, lane);
-        }
-#pragma unroll
-        for (int level = 0; level < 5; ++level)
-#pragma unroll
-            for (int g = 0; g < G; ++g) chain_jump(t[g], lane);
-        // follow the chain through the group while it enters the next window
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const uint64_t bc = bc0 + 32 * g;
-            if (g > 0 && !(next < bc + 32 && next < L)) break;  // g == 0 holds the entry; later ones have next >= bc
-            const int e = (int)(next - bc);
-            const uint32_t reach = __shfl_sync(0xffffffffu, t[g].m, e);
-            const uint32_t nx = __shfl_sync(0xffffffffu, t[g].nx, e);
-            if (lane == 0) {
-                wreach[wb + k + g] = reach;
-                wpos[wb + k + g] = pos;
-            }
-            pos += chain_span(w[g], reach, lane);
-            next = bc + nx;
-        }
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    // tiles past the encoded coverage: stream exhausted, implicit zero tail
-    const uint64_t t0 = max((pos + kRleTile - 1) / kRleTile, (uint64_t)a.tile0);
-    for (uint64_t t = t0 + lane; t < (uint64_t)a.tile0 + a.nrows; t += 32)
-        dir[(t - a.tile0) * a.n] = make_uint2((uint32_t)L, (uint32_t)pos);
-}
-
-// K3b: every window with markers, in parallel (grid.y = stream): marker word
-// positions by a warp prefix sum from the window's start position, validation as
-// RleBitmap.iter_word_segments / decompress (bitmaps.py:196-219, :428-431), and
-// the directory row of every tile boundary a marker's runs cover.
-__global__ void __launch_bounds__(128) rle_dirfill_kernel(const __grid_constant__ RleDirArgs a, const uint64_t *wbase,
-                                                          const uint32_t *wreach, const uint64_t *wpos) {
-    const int lane = threadIdx.x & 31;
-    const int stream = blockIdx.y;
-    const uint64_t *s = a.ptrs[stream];
-    const uint64_t L = a.lens[stream];
-    uint2 *dir = a.dir + stream;
-    const uint64_t nwin = (L + 31) / 32, wb = wbase[stream];
-    const uint64_t r0 = (uint64_t)a.tile0 * kRleTile, r1 = (uint64_t)(a.tile0 + a.nrows) * kRleTile;
-    const uint64_t stride = (uint64_t)gridDim.x * 4;
-    uint64_t k = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    // the next window's mask, position and words are loaded one window ahead
-    auto load = [&](uint64_t q, uint32_t &r, uint64_t &p, uint64_t &w) {
-        if (q < nwin) {
-            r = wreach[wb + q];
-            p = wpos[wb + q];
-            w = q * 32 + lane < L ? __ldg(s + q * 32 + lane) : 0ull;
-        }
-    };
-    uint32_t r_n = 0;
-    uint64_t p_n = 0, w_n = 0;
-    load(k, r_n, p_n, w_n);
-    for (; k < nwin; k += stride) {
-        const uint32_t reach = r_n;
-        const uint64_t pos = p_n, w = w_n;
-        load(k + stride, r_n, p_n, w_n);
-        if (!reach) continue;  // a window inside a literal group
-        const uint64_t idx = k * 32 + lane;
-        const uint64_t run = (w >> 1) & 0xFFFFFFFFull;
-        const uint64_t dirty = w >> 33;
-        const bool is_m = (reach >> lane) & 1u;
-        const uint64_t span = is_m ? run + dirty : 0ull;
-        uint64_t incl = span;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        if (!is_m) continue;
-        const uint64_t start = pos + incl - span;
-        const uint64_t end = start + span;
-        if (idx + 1 + dirty > L) rle_fail(a, RLE_ERR_TRUNCATED, stream);
-        if (end > a.total_words) rle_fail(a, RLE_ERR_OVERLONG, stream);
-        // bits >= r in the last word are invalid (bitmaps.py:70-72 via decompress :428-431)
-        if (a.tail_mask && end == a.total_words && span) {
-            const uint64_t fe = start + run;
-            if (fe == end) {
-                if ((w & 1) && run) rle_fail(a, RLE_ERR_BEYOND_R, stream);
-            } else if (idx + 1 + dirty <= L && (__ldg(s + idx + dirty) & ~a.tail_mask)) {
-                rle_fail(a, RLE_ERR_BEYOND_R, stream);
-            }
-        }
-        // record every tile boundary b with start <= b < end that the range's rows cover
-        uint64_t b = max((start + kRleTile - 1) / kRleTile * kRleTile, r0);
-        for (; b < end && b < a.total_words && b < r1; b += kRleTile)
-            dir[(b / kRleTile - a.tile0) * (uint64_t)a.n] = make_uint2((uint32_t)idx, (uint32_t)start);
-    }
-}
+enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };  // build_rle_directory's codes
 
 struct RleCountArgs {
     const uint64_t *const *ptrs;
@@ -577,38 +362,6 @@ struct bq_rle_query {
     mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced / tables / uses
 };
 
-// The previous K3 (A/B measurements: BQ_RLE_K3=old): K3a walks each stream's chain
-// window by window, K3b fills the directory from every window in parallel.
-static cudaError_t old_directory(const RleDirArgs &a, const std::vector<uint64_t> &lens, int n, int *d_err) {
-    std::vector<uint64_t> wbase(n + 1, 0);
-    uint64_t maxwin = 0;
-    for (int i = 0; i < n; ++i) {
-        const uint64_t nwin = (lens[i] + 31) / 32;
-        wbase[i + 1] = wbase[i] + nwin;
-        maxwin = std::max(maxwin, nwin);
-    }
-    const uint64_t nwin_all = wbase[n];
-    char *scratch = nullptr;
-    cudaError_t e = pool_alloc(reinterpret_cast<void **>(&scratch), (size_t)(n + 1) * 8 + nwin_all * 12 + 16);
-    uint64_t *d_wbase = reinterpret_cast<uint64_t *>(scratch);
-    uint64_t *d_wpos = d_wbase + n + 1;
-    uint32_t *d_wreach = reinterpret_cast<uint32_t *>(d_wpos + nwin_all);
-    if (e == cudaSuccess) e = cudaMemcpy(d_wbase, wbase.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(d_wreach, 0, nwin_all * 4 + 4);
-    if (e == cudaSuccess) {
-        rle_chain_kernel<<<(n + 3) / 4, 128>>>(a, d_wbase, d_wreach, d_wpos);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess && nwin_all) {
-        const unsigned gx = (unsigned)std::min<uint64_t>((maxwin + 3) / 4, 64);
-        rle_dirfill_kernel<<<dim3(gx, (unsigned)n), 128>>>(a, d_wbase, d_wreach, d_wpos);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (scratch) pool_free(scratch);
-    return e;
-}
-
 // Validation of streams over a bit_length-0 universe (host walk; valid streams
 // hold only empty markers, so they are short in practice).
 static int validate_empty_universe(const std::vector<const uint64_t *> &ptrs, const std::vector<uint64_t> &lens) {
@@ -667,9 +420,12 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
     if (rc) return rc;
     const uint32_t tile0 = (uint32_t)(w_begin / kRleTile);
     const uint32_t ntiles = (uint32_t)((w_end - w_begin + kRleTile - 1) / kRleTile);
+    std::vector<uint64_t> lens(n);
+    for (int i = 0; i < n; ++i) lens[i] = streams[i].n_words;
     const size_t tab = (size_t)n * 16;
     const size_t dirb = (size_t)n * (ntiles + 1) * sizeof(uint2);
-    const size_t bytes = tab + dirb + 64;
+    const size_t scr_off = (tab + dirb + 255) & ~(size_t)255;
+    const size_t bytes = scr_off + (total ? rle_directory_scratch_bytes(lens) : 0);
     bq_rle_query *q = new bq_rle_query();
     q->device = device;
     q->n = n;
@@ -689,70 +445,43 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
     q->d_ptrs = reinterpret_cast<const uint64_t **>(m);
     q->d_lens = reinterpret_cast<uint64_t *>(m + (size_t)n * 8);
     q->d_dir = reinterpret_cast<uint2 *>(m + tab);
-    int *d_err = reinterpret_cast<int *>(m + tab + dirb);
-    unsigned long long *d_err_stream = reinterpret_cast<unsigned long long *>(m + tab + dirb + 8);
-    std::vector<const uint64_t *> ptrs(n);
-    std::vector<uint64_t> lens(n);
+    std::vector<uint64_t> ptab(2 * (size_t)n);  // pointer table then lengths: one copy
     for (int i = 0; i < n; ++i) {
-        ptrs[i] = streams[i].words;
-        lens[i] = streams[i].n_words;
+        ptab[i] = reinterpret_cast<uint64_t>(streams[i].words);
+        ptab[(size_t)n + i] = lens[i];
     }
-    e = cudaMemcpy(q->d_ptrs, ptrs.data(), (size_t)n * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(q->d_lens, lens.data(), (size_t)n * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(d_err, 0, 16);
+    // ordered on the legacy stream before the directory kernel, which the build
+    // synchronises before returning: complete before any evaluation reads them
+    e = cudaMemcpyAsync(q->d_ptrs, ptab.data(), tab, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess && !total) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) {
         pool_free(q->mem);
         delete q;
         return cuda_error(e, "rle query setup");
     }
     if (total) {  // the directory walk validates every stream whole, whatever the range
-        RleDirArgs a;
-        a.ptrs = q->d_ptrs;
-        a.lens = q->d_lens;
-        a.n = n;
-        a.total_words = total;
-        a.tail_mask = (r_bits % W) ? ((1ull << (r_bits % W)) - 1) : 0ull;
-        a.tile0 = tile0;
-        a.nrows = ntiles + 1;
-        a.dir = q->d_dir;
-        a.err = d_err;
-        a.err_stream = d_err_stream;
-        int herr[4] = {0, 0, 0, 0};
-        static const char *k3env = getenv("BQ_RLE_K3");
-        if (k3env && !strcmp(k3env, "old")) {  // the previous two-kernel form (A/B measurements only)
-            e = old_directory(a, lens, n, d_err);
-            if (e == cudaSuccess) e = cudaMemcpy(herr, d_err, 16, cudaMemcpyDeviceToHost);
-            if (e != cudaSuccess) {
-                pool_free(q->mem);
-                delete q;
-                return cuda_error(e, "rle directory (K3)");
-            }
-        } else {
-            uint64_t bad = 0;
-            rc = build_rle_directory(q->d_ptrs, q->d_lens, lens, total, a.tail_mask, tile0, ntiles + 1, q->d_dir,
-                                     &herr[0], &bad);
-            if (rc) {
-                pool_free(q->mem);
-                delete q;
-                return rc;
-            }
-            herr[2] = (int)(uint32_t)bad;
-            herr[3] = (int)(uint32_t)(bad >> 32);
-        }
-        if (herr[0]) {
-            unsigned long long bad = (unsigned long long)(uint32_t)herr[2] | ((unsigned long long)(uint32_t)herr[3] << 32);
+        int code = 0;
+        uint64_t bad = 0;
+        const uint64_t tail_mask = (r_bits % W) ? ((1ull << (r_bits % W)) - 1) : 0ull;
+        rc = build_rle_directory(q->d_ptrs, q->d_lens, lens, total, tail_mask, tile0, ntiles + 1, q->d_dir,
+                                 m + scr_off, &code, &bad);
+        if (rc || code) {
             pool_free(q->mem);
             delete q;
-            if (herr[0] == RLE_ERR_TRUNCATED)
-                return set_error(BQ_EFORMAT, "stream %llu: marker announces more literal words than present", bad);
-            if (herr[0] == RLE_ERR_BEYOND_R)
-                return set_error(BQ_EFORMAT, "stream %llu: set bits at positions >= bit_length", bad);
-            return set_error(BQ_EFORMAT, "stream %llu: encoded words exceed bit_length", bad);
+            if (rc) return rc;
+            const unsigned long long b = (unsigned long long)bad;
+            if (code == RLE_ERR_TRUNCATED)
+                return set_error(BQ_EFORMAT, "stream %llu: marker announces more literal words than present", b);
+            if (code == RLE_ERR_BEYOND_R)
+                return set_error(BQ_EFORMAT, "stream %llu: set bits at positions >= bit_length", b);
+            return set_error(BQ_EFORMAT, "stream %llu: encoded words exceed bit_length", b);
         }
     } else {
         // bit_length 0: no directory, but the streams are still validated as
         // iter_word_segments would (bitmaps.py:196-219): a truncated literal group, or
         // any fill / literal coverage at all (> 0 words), is a FormatError
+        std::vector<const uint64_t *> ptrs(n);
+        for (int i = 0; i < n; ++i) ptrs[i] = streams[i].words;
         rc = validate_empty_universe(ptrs, lens);
         if (rc) {
             pool_free(q->mem);

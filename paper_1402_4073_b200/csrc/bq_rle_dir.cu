@@ -40,6 +40,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string.h>
+
 #include <algorithm>
 #include <mutex>
 #include <vector>
@@ -69,10 +71,10 @@ struct DirArgs {
     uint64_t tail_mask;          // valid bits of word total_words - 1 when r % 64 != 0, else 0
     uint32_t tile0, nrows;       // directory rows: tile boundaries tile0 .. tile0 + nrows - 1
     uint2 *dir;                  // [nrows][n] (marker index, fill start word)
-    const uint2 *jobs;           // ticket -> (stream, block), block-major
-    const uint32_t *link_base;   // per stream: index of its block 0 in `link`
+    uint32_t full_levels;        // tickets < full_levels * n: block t / n of stream t % n (every stream has them)
+    const uint2 *jobs;           // later tickets: (stream, block), block-major
     const uint32_t *nblocks;     // per stream
-    unsigned long long *link;    // per (stream, block): exit | end position << 32, ~0 until published
+    unsigned long long *link;    // [block][stream]: exit | end position << 32, ~0 until published
     unsigned int *ticket;
     unsigned long long *err;     // min over (stream << 32 | precedence): the first failing stream
 };
@@ -110,7 +112,8 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     unsigned int t = 0;
     if (lane == 0) t = atomicAdd(a.ticket, 1u);  // tickets in start order: a block's predecessor started earlier
     t = __shfl_sync(0xffffffffu, t, 0);
-    const uint2 job = a.jobs[t];
+    const uint32_t full = a.full_levels * (uint32_t)a.n;
+    const uint2 job = t < full ? make_uint2(t % (uint32_t)a.n, t / (uint32_t)a.n) : a.jobs[t - full];
     const uint32_t stream = job.x, blk = job.y;
     const uint64_t *s = a.ptrs[stream];
     const uint32_t L = (uint32_t)a.lens[stream];  // < 2^32 - 2 (bq_rle_query_create)
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     // the previous block's exit is published by now in the common case: fetch it while
     // the copies land
     uint64_t link_prev = 0;
-    if (blk > 0 && lane == 0) link_prev = ld_link(a.link + a.link_base[stream] + blk - 1);
+    if (blk > 0 && lane == 0) link_prev = ld_link(a.link + (size_t)(blk - 1) * a.n + stream);
     {
         uint32_t done = 0;
         while (!done)
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     uint64_t n_in = 0, p_in = 0;
     if (blk > 0) {
         if (lane == 0) {
-            const unsigned long long *lk = a.link + a.link_base[stream] + blk - 1;
+            const unsigned long long *lk = a.link + (size_t)(blk - 1) * a.n + stream;
             int spins = 0;
             while (link_prev == ~0ull) {
                 if (++spins > 4) __nanosleep(64);
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const bool last_block = blk + 1 == a.nblocks[stream];
     if (lane == 31) {
         const uint64_t ex = min(x_end, (uint64_t)L + 1), pe = min(p_end, total + 1);
-        if (!last_block) st_link(a.link + a.link_base[stream] + blk, ex | (pe << 32));
+        if (!last_block) st_link(a.link + (size_t)blk * a.n + stream, ex | (pe << 32));
         else {
             if (x_end > L) dir_fail(a, DIR_ERR_TRUNCATED, stream);
             else if (p_end > total) dir_fail(a, DIR_ERR_OVERLONG, stream);
@@ -329,61 +332,79 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     }
 }
 
+// Scratch of a directory build (device bytes): links, per-stream block counts, the
+// job table of the partial levels, ticket and error words.
+size_t rle_directory_scratch_bytes(const std::vector<uint64_t> &lens) {
+    const size_t n = lens.size();
+    uint64_t maxb = 1, minb = ~0ull, njobs = 0;
+    for (uint64_t L : lens) {
+        const uint64_t b = std::max<uint64_t>(1, (L + kBlockWords - 1) / kBlockWords);
+        maxb = std::max(maxb, b);
+        minb = std::min(minb, b);
+        njobs += b;
+    }
+    if (!n) minb = 0;
+    const size_t rem = njobs - minb * n;
+    return ((maxb * n * 8 + 255) & ~(size_t)255) + ((n * 4 + 255) & ~(size_t)255) + ((rem * 8 + 255) & ~(size_t)255) +
+           256;
+}
+
 int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const std::vector<uint64_t> &lens,
                         uint64_t total_words, uint64_t tail_mask, uint32_t tile0, uint32_t nrows, uint2 *d_dir,
-                        int *err_code, uint64_t *err_stream) {
+                        void *d_scratch, int *err_code, uint64_t *err_stream) {
     const int n = (int)lens.size();
     *err_code = 0;
-    std::vector<uint32_t> nblk(n), base(n);
-    uint32_t maxb = 0;
+    std::vector<uint32_t> nblk(n);
+    uint32_t maxb = 1, minb = ~0u;
     uint64_t njobs = 0;
     for (int i = 0; i < n; ++i) {
         nblk[i] = (uint32_t)std::max<uint64_t>(1, (lens[i] + kBlockWords - 1) / kBlockWords);
-        base[i] = (uint32_t)njobs;
         njobs += nblk[i];
         maxb = std::max(maxb, nblk[i]);
+        minb = std::min(minb, nblk[i]);
     }
-    // tickets block-major: block k of every stream before block k + 1 of any; the table
-    // is written into a pinned staging buffer (kept between calls) so its upload is a
-    // plain DMA, and the build holds the staging lock until its copy has completed
+    // tickets block-major: block k of every stream before block k + 1 of any.  The
+    // levels every stream has map arithmetically; only the rest need a table, written
+    // with the block counts into a pinned staging buffer (kept between calls) so the
+    // upload is one DMA; the build holds the staging lock until it has completed.
+    const size_t rem = njobs - (uint64_t)minb * n;
+    const size_t a_link = ((size_t)maxb * n * 8 + 255) & ~(size_t)255;
+    const size_t a_nblk = ((size_t)n * 4 + 255) & ~(size_t)255;
+    const size_t a_jobs = (rem * 8 + 255) & ~(size_t)255;
+    const size_t up_bytes = a_nblk + rem * 8;
     static std::mutex staging_mu;
-    static uint2 *staging = nullptr;
+    static char *staging = nullptr;
     static size_t staging_cap = 0;
     std::lock_guard<std::mutex> staging_guard(staging_mu);
-    if (staging_cap < njobs) {
+    if (staging_cap < up_bytes) {
         if (staging) cudaFreeHost(staging);
         staging = nullptr;
         staging_cap = 0;
-        if (cudaHostAlloc(reinterpret_cast<void **>(&staging), std::max<size_t>(njobs, 1 << 16) * 8,
-                          cudaHostAllocDefault) != cudaSuccess) {
+        const size_t cap = std::max<size_t>(up_bytes, 1 << 16);
+        if (cudaHostAlloc(reinterpret_cast<void **>(&staging), cap, cudaHostAllocDefault) != cudaSuccess) {
             cudaGetLastError();
             staging = nullptr;
             return set_error(BQ_ERESOURCE, "pinned staging for the directory job table");
         }
-        staging_cap = std::max<size_t>(njobs, 1 << 16);
+        staging_cap = cap;
     }
+    memcpy(staging, nblk.data(), (size_t)n * 4);
     {
+        uint2 *jt = reinterpret_cast<uint2 *>(staging + a_nblk);
         size_t k = 0;
-        for (uint32_t b = 0; b < maxb; ++b)
+        for (uint32_t b = minb; b < maxb; ++b)
             for (int i = 0; i < n; ++i)
-                if (b < nblk[i]) staging[k++] = make_uint2((uint32_t)i, b);
+                if (b < nblk[i]) jt[k++] = make_uint2((uint32_t)i, b);
     }
-    const size_t jb = njobs * 8, lb = njobs * 8, tb = (size_t)n * 8;
-    char *scratch = nullptr;
-    cudaError_t e = pool_alloc(reinterpret_cast<void **>(&scratch), jb + lb + tb + 64);
-    if (e != cudaSuccess) return cuda_error(e, "rle directory scratch");
-    uint2 *d_jobs = reinterpret_cast<uint2 *>(scratch);
-    unsigned long long *d_link = reinterpret_cast<unsigned long long *>(scratch + jb);
-    uint32_t *d_base = reinterpret_cast<uint32_t *>(scratch + jb + lb);
-    uint32_t *d_nblk = d_base + n;
-    unsigned int *d_ticket = reinterpret_cast<unsigned int *>(scratch + jb + lb + tb);
-    unsigned long long *d_err = reinterpret_cast<unsigned long long *>(scratch + jb + lb + tb + 8);
-    std::vector<uint32_t> tabs(2 * (size_t)n);
-    std::copy(base.begin(), base.end(), tabs.begin());
-    std::copy(nblk.begin(), nblk.end(), tabs.begin() + n);
-    e = cudaMemcpyAsync(d_jobs, staging, jb, cudaMemcpyHostToDevice, 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_base, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice, 0);
-    if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, lb, 0);
+    char *sc = static_cast<char *>(d_scratch);
+    unsigned long long *d_link = reinterpret_cast<unsigned long long *>(sc);
+    uint32_t *d_nblk = reinterpret_cast<uint32_t *>(sc + a_link);
+    uint2 *d_jobs = reinterpret_cast<uint2 *>(sc + a_link + a_nblk);
+    unsigned int *d_ticket = reinterpret_cast<unsigned int *>(sc + a_link + a_nblk + a_jobs);
+    unsigned long long *d_err = reinterpret_cast<unsigned long long *>(sc + a_link + a_nblk + a_jobs + 8);
+    // nblk and the job table are adjacent in both buffers: one copy
+    cudaError_t e = cudaMemcpyAsync(d_nblk, staging, up_bytes, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, (size_t)maxb * n * 8, 0);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_ticket, 0, 8, 0);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0xFF, 8, 0);
     if (e == cudaSuccess) {
@@ -396,8 +417,8 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
         a.tile0 = tile0;
         a.nrows = nrows;
         a.dir = d_dir;
+        a.full_levels = minb;
         a.jobs = d_jobs;
-        a.link_base = d_base;
         a.nblocks = d_nblk;
         a.link = d_link;
         a.ticket = d_ticket;
@@ -408,7 +429,6 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
     unsigned long long herr = ~0ull;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, 8, cudaMemcpyDeviceToHost, 0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(0);
-    pool_free(scratch);
     if (e != cudaSuccess) return cuda_error(e, "rle directory (K3)");
     if (herr != ~0ull) {
         const uint32_t code = (uint32_t)(herr & 0xFFFFFFFFull);

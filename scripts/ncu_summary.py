@@ -1,10 +1,12 @@
 """Summarise an ncu --set full report into profiles/ (run here, no GPU needed).
 
-    python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep c2 r01
+    python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep c2 r01 [sum]
 
 writes profiles/<round>_<workload>_ncu.json (per-launch key metrics) and merges
 the per-launch DRAM traffic into profiles/ncu_traffic.json (read by bench.py
-for roofline.traffic).
+for roofline.traffic): the mean over the captured launches, or with ``sum`` the
+sum of the captured launches (one step made of several kernels, e.g. the C4
+fresh query = K3 + K4).  The warp-stall sample counts of every launch are kept.
 """
 
 from __future__ import annotations
@@ -33,6 +35,14 @@ def summarise(rep: str):
     out = []
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")]}
+        for k, m in enumerate(hdr):
+            if m.startswith("smsp__pcsamp_warps_issue_stalled_") and not m.endswith("_not_issued"):
+                try:
+                    v = float(r[k].replace(",", ""))
+                except ValueError:
+                    continue
+                if v:
+                    d.setdefault("stall_samples", {})[m[len("smsp__pcsamp_warps_issue_stalled_"):]] = v
         for m in RAW:
             if m in hdr:
                 k = hdr.index(m)
@@ -50,6 +60,7 @@ def summarise(rep: str):
 
 def main():
     rep, workload, rnd = sys.argv[1], sys.argv[2], sys.argv[3]
+    mode = sys.argv[4] if len(sys.argv) > 4 else "mean"
     launches = summarise(rep)
     prof = os.path.join(ROOT, "profiles")
     with open(os.path.join(prof, f"{rnd}_{workload}_ncu.json"), "w") as fp:
@@ -59,7 +70,11 @@ def main():
                if "dram__bytes_read.sum" in d]
     tpath = os.path.join(prof, "ncu_traffic.json")
     t = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    if traffic:
+    if traffic and mode == "sum":
+        t[workload] = round(sum(traffic))
+        t[workload + "_source"] = (f"profiles/{rnd}_{workload}_ncu.json: sum over the step's {len(traffic)} "
+                                   "kernels of dram__bytes_read.sum + dram__bytes_write.sum")
+    elif traffic:
         t[workload] = round(sum(traffic) / len(traffic))
         t[workload + "_source"] = (f"profiles/{rnd}_{workload}_ncu.json: mean over {len(traffic)} launch(es) of "
                                    "dram__bytes_read.sum + dram__bytes_write.sum")
