@@ -157,6 +157,13 @@ def cpu_windows(nwin: int, win_words: int, world_rank_offset: int = 0):
     return wins
 
 
+def _oracle_build() -> str:
+    from oracle import oracle as O
+
+    return ("AVX-512 build (x86-64-v4)" if O.library_path().endswith("_avx512.so")
+            else "AVX2 build (x86-64-v3)")
+
+
 def cpu_port_run(wins, steps: int, warmup: int, threads: int):
     """Time the oracle's CPU port of the reference algorithms (wide_or / wide_and /
     csv_threshold, oracle/bq_oracle.c) over the windows, 5 queries per step."""
@@ -194,7 +201,7 @@ def cpu_baseline(budget_s: float = 12.0):
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
             "sample": f"C2 windows: 8 x (N=64 x 2^16 words), T in {list(C2_TS)}, {steps} steps "
                       f"({dt:.1f} s) of oracle/bq_oracle.c orc_threshold_port (wide_or / wide_and / "
-                      f"csv_threshold, OpenMP {threads} threads)"}
+                      f"csv_threshold, OpenMP {threads} threads, {_oracle_build()})"}
 
 
 # ---------------------------------------------------------------------------
@@ -287,7 +294,7 @@ def run_reference(args):
                                   "(PAPER.md:283-298); the windows (512 MiB) exceed the host caches"},
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": "reference algorithms (wide_or / wide_and / csv_threshold) restated in C "
-                                   "(oracle/bq_oracle.c), OpenMP over word batches, on C2 windows"},
+                                   f"(oracle/bq_oracle.c, {_oracle_build()}), OpenMP over word batches, on C2 windows"},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if not args.no_reference_python:

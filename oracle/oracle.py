@@ -31,6 +31,18 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+_LIB_AVX512 = os.path.join(_HERE, "_build", "liboracle_avx512.so")
+
+
+def _has_avx512() -> bool:
+    try:
+        with open("/proc/cpuinfo") as fp:
+            for line in fp:
+                if line.startswith("flags"):
+                    return " avx512f " in line + " "
+    except OSError:
+        pass
+    return False
 _lib = None
 
 OK, EINPUT, ERESOURCE, EFORMAT = 0, -1, -2, -3
@@ -45,7 +57,7 @@ class OracleError(RuntimeError):
 def build(force: bool = False) -> str:
     """Compile bq_oracle.c with the Makefile next to it (gcc, OpenMP)."""
     src = os.path.join(_HERE, "bq_oracle.c")
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+    if force or any(not os.path.exists(f) or os.path.getmtime(f) < os.path.getmtime(src) for f in (_LIB_PATH, _LIB_AVX512)):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
 
@@ -54,7 +66,10 @@ def lib():
     global _lib
     if _lib is None:
         build()
-        L = ctypes.CDLL(_LIB_PATH)
+        path = _LIB_AVX512 if (_has_avx512() and os.path.exists(_LIB_AVX512)
+                               and os.environ.get("BQ_ORACLE_AVX512", "1") != "0") else _LIB_PATH
+        L = ctypes.CDLL(path)
+        L._bq_path = path
         P = ctypes.c_void_p
         U64 = ctypes.c_uint64
         I = ctypes.c_int
@@ -260,3 +275,8 @@ def gen_markov_rle(seed: int, bitmap: int, r: int, mean_one: float, mean_zero: f
             continue
         _check(rc, "gen_markov_rle")
         return out[: n.value].copy()
+
+
+def library_path() -> str:
+    """The oracle library in use (AVX-512 build on hosts with avx512f)."""
+    return lib()._bq_path

@@ -401,7 +401,10 @@ __global__ void __launch_bounds__(256) binop_kernel(const uint64_t *__restrict__
                                                    const uint64_t *__restrict__ b, uint64_t nb, uint64_t nwords,
                                                    uint64_t last_mask, uint64_t *__restrict__ out,
                                                    unsigned long long *popcnt, unsigned long long *last_nz) {
-    constexpr int U = 4;
+#ifndef BQ_BINOP_U
+#define BQ_BINOP_U 2
+#endif
+    constexpr int U = BQ_BINOP_U;
     unsigned long long pc = 0, lnz = 0;
     const uint64_t npairs = (nwords + 1) / 2;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
