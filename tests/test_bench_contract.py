@@ -39,6 +39,9 @@ def test_reference_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+    rp = d.get("reference_python")
+    if rp is not None:  # the stock reference (oracle/_ref) timed as context
+        assert rp["one_core_best"] > 0 and rp["k_processes"]["value"] > 0
 
 
 def test_reference_arm_under_torchrun_prints_once():
@@ -48,7 +51,7 @@ def test_reference_arm_under_torchrun_prints_once():
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus",
-           "2", "--steps", "3", "--warmup", "3"]
+           "2", "--steps", "3", "--warmup", "3", "--no-reference-python"]
     p = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=600,
                        env=dict(os.environ, OMP_NUM_THREADS="2"))
     assert p.returncode == 0, p.stderr[-2000:]
@@ -71,10 +74,11 @@ def test_bench_without_gpu_fails_loudly():
 def test_reference_arm_never_loads_the_product_library():
     """The reference arm (and its input generation) runs on the oracle only: no
     libbq.so in the process after a full run."""
-    code = ("import sys; sys.argv=['bench.py','--impl','reference','--steps','3','--warmup','3']; "
+    code = ("import sys; sys.argv=['bench.py','--impl','reference','--steps','3','--warmup','3',"
+            "'--no-reference-python']; "
             "sys.path.insert(0, %r); import bench; bench.main(); "
             "maps=open('/proc/self/maps').read(); "
-            "assert 'libbq.so' not in maps, 'libbq.so loaded'; assert 'liboracle.so' in maps" % ROOT)
+            "assert 'libbq.so' not in maps, 'libbq.so loaded'; assert 'liboracle' in maps" % ROOT)
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600,
                        env=dict(os.environ, OMP_NUM_THREADS="2"))
     assert p.returncode == 0, p.stderr[-2000:]
@@ -82,7 +86,7 @@ def test_reference_arm_never_loads_the_product_library():
 
 
 def test_reference_arm_gpus_flag_reports_world():
-    p = _run(["--impl", "reference", "--gpus", "4", "--steps", "3", "--warmup", "3"])
+    p = _run(["--impl", "reference", "--gpus", "4", "--steps", "3", "--warmup", "3", "--no-reference-python"])
     assert p.returncode == 0, p.stderr[-2000:]
     lines = _json_lines(p.stdout)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 4
