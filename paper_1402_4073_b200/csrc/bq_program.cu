@@ -4,8 +4,8 @@
 // A BitProgram (programs.py:56-72) is a list of (opcode, dst, a, b) over slots;
 // inputs occupy slots 0..arity-1.  The reference interprets it over whole
 // bitmaps (`execute`, :163-193) or 256-word batches (`execute_horizontal`,
-// :196-237).  Here it is turned into CUDA source -- one thread per output word,
-// every slot a 64-bit register variable -- compiled once with NVRTC for sm_100a
+// :196-237).  Here it is turned into CUDA source -- one thread per 32-bit half word,
+// every slot a 32-bit register variable -- compiled once with NVRTC for sm_100a
 // and launched through the driver API.  Loads are coalesced across a warp
 // (consecutive words of one input), so the program runs at HBM speed until its
 // gate count makes it compute-bound.  Semantics match `execute`: missing
@@ -97,27 +97,33 @@ static Jit &jit() {
     return j;
 }
 
+// One thread per 32-bit half of an output word: every slot is a 32-bit register
+// (the program is bitwise, so the halves are independent), which halves the
+// registers per thread against 64-bit slots (SSum(64,32): 78 instead of 171) and
+// triples the warps an SM can hold to overlap the loads with the gate network.
 static std::string gen_source(const int32_t *ins, int n_ins, int arity, int n_slots, int result) {
     std::ostringstream o;
     o << "// generated from a bitquorum BitProgram: arity=" << arity << " slots=" << n_slots << " ops=" << n_ins << "\n"
       << "typedef unsigned long long u64;\n"
+      << "typedef unsigned int u32;\n"
       << "extern \"C\" __global__ void __launch_bounds__(256) bq_prog(const u64 *const *ptrs, const u64 *lens,\n"
       << "    u64 nwords, u64 full_words, u64 last_mask, u64 *out, u64 *popcnt, u64 *last_nz) {\n"
       << "  u64 pc = 0, lnz = 0;\n"
-      << "  for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (u64)gridDim.x * blockDim.x) {\n"
+      << "  for (u64 h = (u64)blockIdx.x * blockDim.x + threadIdx.x; h < 2 * nwords; h += (u64)gridDim.x * blockDim.x) {\n"
+      << "    const u64 w = h >> 1;\n"
       << "    const bool full = w < full_words;\n";
     for (int i = 0; i < arity; ++i)
-        o << "    u64 s" << i << " = (full || w < lens[" << i << "]) ? __ldg(ptrs[" << i << "] + w) : 0ull;\n";
+        o << "    u32 s" << i << " = (full || w < lens[" << i << "]) ? __ldg((const u32 *)ptrs[" << i << "] + h) : 0u;\n";
     if (n_slots > arity) {
-        o << "    u64";
-        for (int k = arity; k < n_slots; ++k) o << (k > arity ? ", " : " ") << "s" << k << " = 0ull";
+        o << "    u32";
+        for (int k = arity; k < n_slots; ++k) o << (k > arity ? ", " : " ") << "s" << k << " = 0u";
         o << ";\n";
     }
     for (int k = 0; k < n_ins; ++k) {
         const int op = ins[4 * k], d = ins[4 * k + 1], a = ins[4 * k + 2], b = ins[4 * k + 3];
         switch (op) {
-            case OP_ZERO: o << "    s" << d << " = 0ull;\n"; break;
-            case OP_ONE: o << "    s" << d << " = ~0ull;\n"; break;
+            case OP_ZERO: o << "    s" << d << " = 0u;\n"; break;
+            case OP_ONE: o << "    s" << d << " = ~0u;\n"; break;
             case OP_AND: o << "    s" << d << " = s" << a << " & s" << b << ";\n"; break;
             case OP_OR: o << "    s" << d << " = s" << a << " | s" << b << ";\n"; break;
             case OP_XOR: o << "    s" << d << " = s" << a << " ^ s" << b << ";\n"; break;
@@ -126,10 +132,10 @@ static std::string gen_source(const int32_t *ins, int n_ins, int arity, int n_sl
             default: break;  // reclaim: register allocation is the compiler's job
         }
     }
-    o << "    u64 r = s" << result << ";\n"
-      << "    if (w == nwords - 1) r &= last_mask;\n"
-      << "    out[w] = r;\n"
-      << "    pc += __popcll(r);\n"
+    o << "    u32 r = s" << result << ";\n"
+      << "    if (w == nwords - 1) r &= (u32)(last_mask >> (32 * (h & 1)));\n"
+      << "    ((u32 *)out)[h] = r;\n"
+      << "    pc += __popc(r);\n"
       << "    if (r) lnz = w + 1;\n"
       << "  }\n"
       << "  for (int o = 16; o > 0; o >>= 1) {\n"
@@ -290,7 +296,7 @@ extern "C" BQ_API int bq_program_execute(bq_program *p, bq_query *q, uint64_t *d
     CUfunction_t fn = nullptr;
     if ((rc = program_function(p, &fn))) return rc;
     const unsigned threads = 256;
-    uint64_t grid = (nwords + threads - 1) / threads;
+    uint64_t grid = (2 * nwords + threads - 1) / threads;  // a thread per 32-bit half word
     const uint64_t cap = (uint64_t)sm_count() * 8;
     if (grid > cap) grid = cap;
     void *args[] = {(void *)&ptrs, (void *)&lens, (void *)&nwords, (void *)&full, (void *)&last_mask,
