@@ -49,6 +49,9 @@ constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a priva
 #ifndef BQ_K4_MINB
 #define BQ_K4_MINB 4
 #endif
+#ifndef BQ_K4_ZERO_ADDS
+#define BQ_K4_ZERO_ADDS 1
+#endif
 constexpr int kPoolWords = BQ_K4_POOL;  // words per warp pool half (two halves: double buffer);
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
 constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
@@ -152,8 +155,14 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
         const uint32_t at_rel = carry + ones;
         const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
         // byte offsets as index * four (runtime 4): IMAD on the FMA pipe instead of an ALU LEA
+#if BQ_K4_ZERO_ADDS
+        // an empty update adds 0 to its real slot (rare on C4: markers are literal groups)
+        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + rel * four), at_rel);
+        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + fe * four), at_fe);
+#else
         atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_rel ? rel : dummy) * four), at_rel);
         atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_fe ? fe : dummy) * four), at_fe);
+#endif
         carry = lit ? 0xFFFF0000u : 0u;
         if (de_raw >= Wu) return;  // the pending literal end lies past the tile
         rel = de_raw;

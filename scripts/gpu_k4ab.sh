@@ -1,11 +1,10 @@
-# K4 occupancy variants (A/B on the C4 fresh-query line) and the (f)-rows line
+# K4 variants: correctness (RLE tests) and the C4 fresh-query line, two interleaved rounds
 mkdir -p gpurun_out
-timeout 900 python bench.py --workload frows --steps 20 > gpurun_out/bench_frows.log 2>&1; echo "rc=$?" >> gpurun_out/bench_frows.log
 for v in _variants/libbq_*.so; do
   n=$(basename $v .so)
-  BQ_LIB=$PWD/$v timeout 900 python -m pytest tests/test_gpu_rle.py -x -q > gpurun_out/pytest_$n.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_$n.log
+  BQ_LIB=$PWD/$v timeout 900 python -m pytest tests/test_gpu_rle.py tests/test_gpu_stress.py -x -q > gpurun_out/pytest_$n.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_$n.log
 done
-for rep in 1 2; do
+for rep in 1 2 3; do
   timeout 600 python bench.py --workload c4 --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/k4ab_base_$rep.log 2>&1
   for v in _variants/libbq_*.so; do
     n=$(basename $v .so)
