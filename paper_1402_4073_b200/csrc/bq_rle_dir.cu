@@ -98,31 +98,6 @@ __device__ __forceinline__ void st_link(unsigned long long *p, unsigned long lon
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-#ifndef BQ_DIR_WIN
-#define BQ_DIR_WIN 1
-#endif
-// A four-word register window over a lane's slot (two 16-byte shared loads from an
-// even index): the next marker is usually within a few words, so most steps of a
-// walk pick it from registers instead of waiting for a dependent shared load.
-struct SlotWindow {
-    uint32_t base = 0xFFFFFFF0u;
-    ulonglong2 a, b;
-    __device__ __forceinline__ uint64_t get(const uint64_t *slot, uint32_t i) {
-#if BQ_DIR_WIN
-        if (i - base >= 4u) {
-            base = i & ~1u;
-            a = *reinterpret_cast<const ulonglong2 *>(slot + base);
-            b = *reinterpret_cast<const ulonglong2 *>(slot + base + 2);
-        }
-        const uint32_t k = i - base;
-        const uint64_t lo = (k & 1) ? a.y : a.x, hi = (k & 1) ? b.y : b.x;
-        return (k & 2) ? hi : lo;
-#else
-        return slot[i];
-#endif
-    }
-};
-
 __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ DirArgs a) {
 #if BQ_DIR_CONTIG
     // one contiguous copy of the block [b0 - kHalo, b1): a lane's halo is its left
@@ -234,9 +209,8 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     auto walk = [&](uint32_t from, uint64_t &span) -> uint64_t {
         span = 0;
         uint32_t i = (uint32_t)((int64_t)from - sbase);
-        SlotWindow win;
         while (i < iend) {
-            const uint64_t w = win.get(slot, i);
+            const uint64_t w = slot[i];
             const uint32_t dirty = (uint32_t)(w >> 33);
             span += (uint64_t)(uint32_t)(w >> 1) + dirty;
             i += 1 + dirty;
@@ -316,9 +290,8 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     uint64_t pos = pos0;
     uint32_t i = active ? (uint32_t)((int64_t)entry - sbase) : iend;
     auto dir_walk = [&](auto tail_check) {
-        SlotWindow win;
         while (i < iend) {
-            const uint64_t w = win.get(slot, i);
+            const uint64_t w = slot[i];
             const uint32_t dirty = (uint32_t)(w >> 33);
             const uint64_t end = pos + (uint32_t)(w >> 1) + dirty;
             if (end > nb) {  // the marker covers boundary nb (< rlim)
