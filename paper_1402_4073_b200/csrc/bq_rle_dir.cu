@@ -363,6 +363,7 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
         maxb = std::max(maxb, nblk[i]);
         minb = std::min(minb, nblk[i]);
     }
+    if (njobs >= (1ull << 31)) return set_error(BQ_ERESOURCE, "streams too long for one directory launch");
     // tickets block-major: block k of every stream before block k + 1 of any.  The
     // levels every stream has map arithmetically; only the rest need a table, written
     // with the block counts into a pinned staging buffer (kept between calls) so the
