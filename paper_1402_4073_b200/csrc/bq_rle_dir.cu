@@ -56,9 +56,7 @@ namespace bq {
 #ifndef BQ_DIR_CONTIG
 #define BQ_DIR_CONTIG 0
 #endif
-#ifndef BQ_DIR_REC
-#define BQ_DIR_REC 1
-#endif
+
 constexpr int kSegWords = BQ_DIR_SEG;                // stream words per segment (one lane)
 constexpr int kBlockWords = kSegWords * 32;          // one warp = one block of 32 segments
 constexpr int kHalo = 8;                             // words before a segment holding its entry guesses
@@ -110,11 +108,6 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     __shared__ __align__(16) uint64_t slots[32 * kSlotWords];
 #endif
     __shared__ __align__(8) uint64_t bar;
-#if BQ_DIR_REC
-    // per marker of the lane's walk: its end relative to the segment's entry position
-    // (24 bits) and its slot index (8 bits), lane-interleaved (conflict-free)
-    __shared__ uint32_t recs[kSegWords * 32];
-#endif
     const int lane = threadIdx.x;
 
     unsigned int t = 0;
@@ -214,28 +207,15 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     // walk from slot index i to the first chain position >= qe, summing the words the
     // markers cover (i stays < 2^32: it is < qe - sbase before a step, dirty < 2^31)
     const uint32_t iend = (uint32_t)((int64_t)qe - sbase);
-    uint32_t nrec = 0;     // markers recorded by the last walk
-    bool rec_ovf = false;  // a relative end >= 2^24: the directory rows come from a second walk
     auto walk = [&](uint32_t from, uint64_t &span) -> uint64_t {
         span = 0;
         uint32_t i = (uint32_t)((int64_t)from - sbase);
-#if BQ_DIR_REC
-        uint32_t m = 0;
-#endif
         while (i < iend) {
             const uint64_t w = slot[i];
             const uint32_t dirty = (uint32_t)(w >> 33);
             span += (uint64_t)(uint32_t)(w >> 1) + dirty;
-#if BQ_DIR_REC
-            recs[m * 32 + lane] = (span < (1u << 24) ? (uint32_t)span : 0xFFFFFFu) | (i << 24);
-            ++m;
-#endif
             i += 1 + dirty;
         }
-#if BQ_DIR_REC
-        nrec = m;
-        rec_ovf = span >= (1u << 24);
-#endif
         return (uint64_t)((int64_t)i + sbase);
     };
     uint64_t span = 0, exit_ = entry;
@@ -270,8 +250,6 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
             entry = (uint32_t)min(prev, (uint64_t)L + 1);
             exit_ = prev;
             span = 0;
-            nrec = 0;
-            rec_ovf = false;
         } else if (prev != entry) {
             entry = (uint32_t)prev;
             exit_ = walk(entry, span);
@@ -312,45 +290,6 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     if (nb >= rlim) nb = ~0ull;
     uint64_t pos = pos0;
     uint32_t i = active ? (uint32_t)((int64_t)entry - sbase) : iend;
-#if BQ_DIR_REC
-    if (!rec_ovf) {
-        // rows from the records: no second walk (boundaries and marker ends ascend)
-        i = iend;  // the walk below does nothing
-        const uint64_t seg_end = pos0 + span;
-        uint32_t k = 0, start = 0;
-        while (nb < seg_end) {  // nb < rlim, or ~0
-            const uint32_t target = (uint32_t)(nb - pos0);
-            uint32_t r = recs[k * 32 + lane];
-            while ((r & 0xFFFFFFu) <= target) {  // marker k ends at or before the boundary
-                start = r & 0xFFFFFFu;
-                r = recs[++k * 32 + lane];
-            }
-            const uint64_t mend = pos0 + (r & 0xFFFFFFu);
-            const uint2 v = make_uint2((uint32_t)((int64_t)(r >> 24) + sbase), (uint32_t)(pos0 + start));
-            for (; nb < mend && nb < rlim; nb += kRleTile, drow += a.n) *drow = v;
-            if (nb >= rlim) nb = ~0ull;
-        }
-        if (a.tail_mask && seg_end == total && nrec) {
-            // bits >= r in the last word (bitmaps.py:70-72 via decompress :428-431): the
-            // marker ending at total with a nonzero span (trailing empty markers skipped)
-            uint32_t kk = nrec - 1;
-            const uint32_t e = recs[kk * 32 + lane] & 0xFFFFFFu;
-            while (kk > 0 && (recs[(kk - 1) * 32 + lane] & 0xFFFFFFu) == e) --kk;
-            const uint32_t st = kk ? (recs[(kk - 1) * 32 + lane] & 0xFFFFFFu) : 0u;
-            if (e > st) {
-                const uint32_t si = recs[kk * 32 + lane] >> 24;
-                const uint64_t w = slot[si];
-                const uint32_t dirty = (uint32_t)(w >> 33);
-                const uint64_t p = (uint64_t)((int64_t)si + sbase);
-                if (dirty == 0) {
-                    if (w & 1) dir_fail(a, DIR_ERR_BEYOND_R, stream);
-                } else if (p + dirty < L && (__ldg(s + p + dirty) & ~a.tail_mask)) {
-                    dir_fail(a, DIR_ERR_BEYOND_R, stream);
-                }
-            }
-        }
-    }
-#endif
     auto dir_walk = [&](auto tail_check) {
         while (i < iend) {
             const uint64_t w = slot[i];
