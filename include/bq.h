@@ -203,6 +203,15 @@ BQ_API int bq_rle_query_threshold(bq_rle_query *q, int t, uint64_t *d_out,
 BQ_API int bq_rle_query_symmetric(bq_rle_query *q, const uint8_t *h_accept, uint64_t *d_out,
                                   unsigned long long *d_popcnt, void *stream);
 
+/* The counters runmerge.cdom_threshold / cdom_symmetric put in ``stats``
+ * (runmerge.py:237-240, :296-298), recomputed on the device from the merged runs
+ * (_merged_runs, :29-56) through the query's tile directory: h_stats[0] =
+ * segments, [1] = heap_pops, [2..5] = dirty_segment_solver's dispatch counts
+ * or / and / looped / scan (:69-83) for threshold t (t = 0: symmetric, zeros).
+ * The query must cover all words (bq_rle_query_create).  Synchronous on
+ * `stream`; scratch ~20 bytes per word, freed before returning. */
+BQ_API int bq_rle_query_sweep_stats(bq_rle_query *q, int t, uint64_t *h_stats, void *stream);
+
 /* Canonical RLE encoding of host words, RleBuilder rules (bitmaps.py:351-414);
  * used to hand results back as RleBitmap (counters.py:33-37).  Returns
  * BQ_ERESOURCE if cap is too small; *out_len always receives the needed length. */

@@ -554,9 +554,12 @@ static heap_ent heap_pop(heap_ent *h, int *hn) {
     return top;
 }
 
-/* accept == NULL -> threshold t (cdom_threshold); otherwise cdom_symmetric. */
+/* accept == NULL -> threshold t (cdom_threshold); otherwise cdom_symmetric.
+ * stats_out (optional, 6 words): segments, heap_pops (runmerge.py:237-239) and the
+ * dirty_segment_solver dispatch counts or / and / looped / scan (:69-83; threshold
+ * only; cdom_symmetric has no solver). */
 static int cdom_common(const uint64_t *const *s, const uint64_t *lens, int n, uint64_t r, int t,
-                       const uint8_t *accept, uint64_t *out, uint64_t *segments_out) {
+                       const uint8_t *accept, uint64_t *out, uint64_t *stats_out) {
     if (n < 1) return ORC_EINPUT;
     if (!accept && (t < 1 || t > n)) return ORC_EINPUT; /* runmerge.py:201-202 */
     uint64_t total = word_count(r);
@@ -588,7 +591,7 @@ static int cdom_common(const uint64_t *const *s, const uint64_t *lens, int n, ui
         }
         heap_push(heap, &hn, (heap_ent){cur[i].end, i});
     }
-    uint64_t pos = 0, segments = 0;
+    uint64_t pos = 0, segments = 0, pops = 0, br[4] = {0, 0, 0, 0};
     int *dirty_idx = (int *)malloc(sizeof(int) * (size_t)n);
     if (!dirty_idx) {
         rc = ORC_ERESOURCE;
@@ -620,6 +623,22 @@ static int cdom_common(const uint64_t *const *s, const uint64_t *lens, int n, ui
             int nd = 0;
             for (int i = 0; i < n; ++i)
                 if (alive[i] && cur[i].kind == 'd') dirty_idx[nd++] = i;
+            if (!accept) { /* dirty_segment_solver's dispatch (runmerge.py:69-83) */
+                const int te = t - k;
+                int b;
+                if (te == 1) b = 0;
+                else if (te == nd) b = 1;
+                else if (te >= 128) b = 3; /* SCANCOUNT_CUTOFF */
+                else {
+                    uint64_t beta = 0;
+                    for (int d = 0; d < nd; ++d)
+                        for (uint64_t w = pos; w <= end; ++w)
+                            beta += (uint64_t)__builtin_popcountll(s[dirty_idx[d]][cur[dirty_idx[d]].base +
+                                                                                 (w - cur[dirty_idx[d]].start)]);
+                    b = 2 * beta >= (uint64_t)nd * (uint64_t)te ? 2 : 3;
+                }
+                br[b]++;
+            }
             for (uint64_t w = pos; w <= end; ++w) {
                 uint32_t cnt[W];
                 memset(cnt, 0, sizeof cnt);
@@ -644,6 +663,7 @@ static int cdom_common(const uint64_t *const *s, const uint64_t *lens, int n, ui
         while (hn && heap[0].end == end) {
             heap_ent e = heap_pop(heap, &hn);
             int i = e.idx;
+            pops++;
             if (cur[i].kind == 'f') {
                 clean--;
                 ones -= (int)cur[i].bit;
@@ -667,7 +687,11 @@ static int cdom_common(const uint64_t *const *s, const uint64_t *lens, int n, ui
         pos = end + 1;
     }
     free(dirty_idx);
-    if (segments_out) *segments_out = segments;
+    if (stats_out) {
+        stats_out[0] = segments;
+        stats_out[1] = pops;
+        for (int b = 0; b < 4; ++b) stats_out[2 + b] = br[b];
+    }
 done:
     free(it);
     free(cur);
@@ -678,13 +702,13 @@ done:
 }
 
 int orc_cdom_threshold(const uint64_t *const *s, const uint64_t *lens, int n, uint64_t r, int t,
-                       uint64_t *out, uint64_t *segments) {
-    return cdom_common(s, lens, n, r, t, NULL, out, segments);
+                       uint64_t *out, uint64_t *stats) {
+    return cdom_common(s, lens, n, r, t, NULL, out, stats);
 }
 
 int orc_cdom_symmetric(const uint64_t *const *s, const uint64_t *lens, int n, uint64_t r,
-                       const uint8_t *accept, uint64_t *out, uint64_t *segments) {
-    return cdom_common(s, lens, n, r, 0, accept, out, segments);
+                       const uint8_t *accept, uint64_t *out, uint64_t *stats) {
+    return cdom_common(s, lens, n, r, 0, accept, out, stats);
 }
 
 int orc_num_threads(void) {

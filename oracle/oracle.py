@@ -215,24 +215,39 @@ def rle_compress(words: np.ndarray, r: int) -> np.ndarray:
     return out[: n_out.value].copy()
 
 
-def cdom_threshold(streams: Sequence[np.ndarray], r: int, t: int) -> np.ndarray:
-    """cdom_threshold (reference runmerge.py:198-241), output uncompressed."""
+_BRANCHES = ("or", "and", "looped", "scan")
+
+
+def cdom_threshold(streams: Sequence[np.ndarray], r: int, t: int, stats: dict | None = None) -> np.ndarray:
+    """cdom_threshold (reference runmerge.py:198-241), output uncompressed.  ``stats``
+    is filled as the reference fills it: untouched for T = 1 / T = N (wide_or /
+    wide_and, :203-206) and r = 0 (:209-210), else segments, heap_pops and the
+    dirty-segment dispatch counts under ``branches`` (nonzero keys only, :237-240)."""
     arrs, ptrs, lens, n = _as_inputs(streams)
     out = np.zeros(max(word_count(r), 1), dtype=np.uint64)
-    seg = ctypes.c_uint64(0)
-    _check(lib().orc_cdom_threshold(ptrs, lens, n, r, t, out.ctypes.data, ctypes.byref(seg)),
+    st = np.zeros(6, dtype=np.uint64)
+    _check(lib().orc_cdom_threshold(ptrs, lens, n, r, t, out.ctypes.data, st.ctypes.data),
            "cdom_threshold")
+    if stats is not None and 1 < t < n and word_count(r):
+        stats["segments"] = int(st[0])
+        stats["heap_pops"] = int(st[1])
+        stats["branches"] = {b: int(c) for b, c in zip(_BRANCHES, st[2:]) if c}
     return out[: word_count(r)]
 
 
-def cdom_symmetric(streams: Sequence[np.ndarray], r: int, accept: Sequence[bool]) -> np.ndarray:
-    """cdom_symmetric (reference runmerge.py:244-299), output uncompressed."""
+def cdom_symmetric(streams: Sequence[np.ndarray], r: int, accept: Sequence[bool],
+                   stats: dict | None = None) -> np.ndarray:
+    """cdom_symmetric (reference runmerge.py:244-299), output uncompressed; ``stats``
+    gets segments and heap_pops (:296-298) unless r = 0."""
     arrs, ptrs, lens, n = _as_inputs(streams)
     acc = np.asarray([1 if a else 0 for a in accept], dtype=np.uint8)
     out = np.zeros(max(word_count(r), 1), dtype=np.uint64)
-    seg = ctypes.c_uint64(0)
+    st = np.zeros(6, dtype=np.uint64)
     _check(lib().orc_cdom_symmetric(ptrs, lens, n, r, acc.ctypes.data, out.ctypes.data,
-                                    ctypes.byref(seg)), "cdom_symmetric")
+                                    st.ctypes.data), "cdom_symmetric")
+    if stats is not None and word_count(r):
+        stats["segments"] = int(st[0])
+        stats["heap_pops"] = int(st[1])
     return out[: word_count(r)]
 
 

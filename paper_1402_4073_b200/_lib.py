@@ -56,6 +56,7 @@ SIGNATURES = {
     "bq_rle_query_directory_bytes": (_U64, [_P]),
     "bq_rle_query_layout_stats": (_I, [_P, _P, _P]),
     "bq_rle_query_layout_events": (_I, [_P, _P]),
+    "bq_rle_query_sweep_stats": (_I, [_P, _I, _P, _P]),
     "bq_rle_query_threshold": (_I, [_P, _I, _P, _P, _P]),
     "bq_rle_query_symmetric": (_I, [_P, _P, _P, _P, _P]),
     "bq_rle_encode_host": (_I, [_P, _U64, _U64, _P, _U64, _P]),

@@ -15,8 +15,9 @@ All the reference's algorithm variants compute the same function, so they all
 dispatch to the same kernels; they differ only in their argument contracts and
 ``stats`` keys.  Keys that describe the query (counter_width, increments,
 bitmap_ops) are reproduced; cdom's keys count the steps of its CPU heap sweep
-(segments, heap_pops, branches; runmerge.py:238-240), which the device path does
-not take, so its ``stats`` dict is left as passed.  There is no CPU fallback:
+(segments, heap_pops, branches; runmerge.py:238-240): the device path does not
+take that sweep, so they are recomputed from the inputs' merged runs by a
+separate device pass (K8), only when a ``stats`` dict is passed.  There is no CPU fallback:
 without the CUDA library every call raises ``ExtensionMissing``.
 """
 
@@ -282,14 +283,18 @@ def scan_count(bitmaps: Sequence, t: int, r: int | None = None, budget_bytes: in
                stats: dict | None = None):
     """counters.scan_count (counters.py:46-67).
 
-    ``budget_bytes`` bounds the device working set (the result buffer); the
-    kernel keeps its counters in registers, so unlike the reference's CPU
-    counter array it does not grow with r * counter width."""
+    ``budget_bytes`` keeps the reference's contract exactly (counters.py:54-57):
+    r counters of counter_width(N) bits may not exceed it, else ResourceError
+    with the reference's message, although the kernel keeps its counters in
+    registers.  ``threshold`` is the same query without the budget."""
     _check_t(len(bitmaps), t)
     if r is None:
         r = max(b.bit_length for b in bitmaps)
-    if word_count(r) * 8 > budget_bytes:
-        raise ResourceError(f"a {word_count(r) * 8}-byte result exceeds the {budget_bytes}-byte budget")
+    width = counter_width(len(bitmaps))
+    if r * width // 8 > budget_bytes:
+        raise ResourceError(
+            f"{r} counters of {width} bits exceed the {budget_bytes}-byte budget; "
+            "consider hash_count")
     res = _run(bitmaps, r, t=t)
     if stats is not None:
         stats["counter_width"] = counter_width(len(bitmaps))
@@ -325,24 +330,42 @@ def csv_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
     return res
 
 
+def _sweep_stats(bitmaps, t: int, stats: dict):
+    """Fill ``stats`` with cdom's sweep counters, computed on the device (K8) from
+    the cached query's directory; nothing for r = 0, like the reference (:209-210)."""
+    r = max(b.bit_length for b in bitmaps)
+    if word_count(r) == 0:
+        return
+    q = QUERIES.get(_classify(bitmaps), bitmaps, r, _device_for(bitmaps))
+    stats.update(q.sweep_stats(t))
+
+
 def cdom_threshold(bitmaps: Sequence, t: int, stats: dict | None = None):
-    """runmerge.cdom_threshold (runmerge.py:198-241): RLE inputs only.  ``stats`` is
-    accepted for the signature; the heap-sweep counters it would hold
-    (runmerge.py:238-240) have no device counterpart."""
+    """runmerge.cdom_threshold (runmerge.py:198-241): RLE inputs only.  ``stats``
+    receives what the reference's sweep reports (:237-240): segments, heap_pops
+    and the dirty-segment dispatch counts under ``branches``, recomputed on the
+    device (K8) -- except for T = 1 / T = N, which the reference answers with
+    wide_or / wide_and without touching ``stats`` (:203-206)."""
     n = len(bitmaps)
     _check_t(n, t)
     if any(kind_of(b) not in ("r", "dr") for b in bitmaps):
         raise InputError("cdom operates on RLE bitmaps; compress inputs first")
-    return _run(bitmaps, None, t=t)
+    res = _run(bitmaps, None, t=t)
+    if stats is not None and 1 < t < n:
+        _sweep_stats(bitmaps, t, stats)
+    return res
 
 
 def cdom_symmetric(bitmaps: Sequence, spec, stats: dict | None = None):
-    """runmerge.cdom_symmetric (runmerge.py:244-299): RLE inputs only.  ``stats`` as
-    for cdom_threshold."""
+    """runmerge.cdom_symmetric (runmerge.py:244-299): RLE inputs only.  ``stats``
+    receives segments and heap_pops (:296-298), recomputed on the device (K8)."""
     accept_bytes(spec, len(bitmaps))
     if any(kind_of(b) not in ("r", "dr") for b in bitmaps):
         raise InputError("cdom operates on RLE bitmaps; compress inputs first")
-    return _run(bitmaps, None, accept=spec)
+    res = _run(bitmaps, None, accept=spec)
+    if stats is not None:
+        _sweep_stats(bitmaps, 0, stats)
+    return res
 
 
 def wide_or(bitmaps: list):

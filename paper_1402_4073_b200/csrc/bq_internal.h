@@ -188,6 +188,13 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
 // device scratch bytes build_rle_directory needs for these stream lengths
 size_t rle_directory_scratch_bytes(const std::vector<uint64_t> &lens);
 
+// ---- K8: cdom sweep statistics (bq_rle_stats.cu) ------------------------------
+// h_stats[6] = segments, heap_pops, then the dispatch counts or / and / looped / scan
+// of thresholds t > 0 (t = 0: symmetric, no dispatch).  Whole-range directory only.
+// Synchronous on `s`.
+int rle_sweep_stats(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const uint2 *d_dir, int n,
+                    uint32_t ntiles, uint64_t total, int t, uint64_t *h_stats, cudaStream_t s);
+
 // ---- K5 generator kernels --------------------------------------------------
 int launch_gen_rows(uint64_t seed, uint32_t first, int count, const uint32_t *d_q16s, uint64_t w0,
                     uint64_t nw, uint64_t *d_out, uint64_t pitch, cudaStream_t stream);

@@ -684,6 +684,22 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     return BQ_OK;
 }
 
+BQ_API int bq_rle_query_sweep_stats(bq_rle_query *q, int t, uint64_t *h_stats, void *stream) {
+    if (!q || !h_stats) return set_error(BQ_EINPUT, "NULL argument");
+    if (t < 0 || t > q->n) return set_error(BQ_EINPUT, "threshold %d outside [0, %d]", t, q->n);
+    if (q->w_begin != 0 || q->w_end != q->total_words)
+        return set_error(BQ_EINPUT, "sweep stats describe the whole sweep: the query must cover all words");
+    DeviceGuard dg;
+    int rc = dg.set(q->device);
+    if (rc) return rc;
+    for (int k = 0; k < 6; ++k) h_stats[k] = 0;
+    if (!q->total_words) return BQ_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rc = rle_sweep_stats(q->d_ptrs, q->d_lens, q->d_dir, q->n, q->ntiles, q->total_words, t, h_stats, s);
+    if (rc == BQ_OK) note_use(q, s);
+    return rc;
+}
+
 BQ_API int bq_rle_query_threshold(bq_rle_query *q, int t, uint64_t *d_out, unsigned long long *d_popcnt, void *stream) {
     if (!q) return set_error(BQ_EINPUT, "query is NULL");
     if (t < 1 || t > q->n) return set_error(BQ_EINPUT, "threshold %d outside [1, %d]", t, q->n);  // runmerge.py:201-202

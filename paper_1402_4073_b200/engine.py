@@ -270,6 +270,20 @@ class RleQuery:
         _lib.check(self._lib.bq_rle_query_layout_events(self._h, ctypes.byref(e)), "bq_rle_query_layout_events")
         return int(e.value)
 
+    def sweep_stats(self, t: int = 0, stream=None) -> dict:
+        """The counters cdom's CPU sweep reports (runmerge.py:237-240, :296-298),
+        recomputed on the device from the inputs' merged runs (K8): segments,
+        heap_pops and, for a threshold t > 0, the dirty-segment dispatch counts
+        (nonzero keys only, like the reference's ``branches`` dict)."""
+        st = np.zeros(6, dtype=np.uint64)
+        _lib.check(self._lib.bq_rle_query_sweep_stats(self._h, int(t), st.ctypes.data,
+                                                      stream_handle(stream, self.device)),
+                   "bq_rle_query_sweep_stats")
+        res = {"segments": int(st[0]), "heap_pops": int(st[1])}
+        if t > 0:
+            res["branches"] = {b: int(c) for b, c in zip(("or", "and", "looped", "scan"), st[2:]) if c}
+        return res
+
     def _outs(self, out, popcnt):
         if out is None:
             out = torch.empty(max(self.out_words, 1), dtype=torch.int64, device=self.device)

@@ -239,27 +239,30 @@ def rle_cases(rng):
         sets = [positions(b) for b in inputs]
         for t in sorted({1, 2, max(1, n // 4), max(1, n // 2), n}):
             exp = oracle.brute_threshold(sets, t)
-            got = runmerge.cdom_threshold(comp, t)
+            st = {}  # the sweep's counters (runmerge.py:237-240); untouched for T = 1 / N
+            got = runmerge.cdom_threshold(comp, t, stats=st)
             assert got.positions() == exp
             sc = counters.scan_count(comp, t)  # RLE in -> RLE out (counters.py:33-37)
             assert sc.words == got.words
             wr.add([c.words for c in comp], [c.bit_length for c in comp], got.words,
                    {"n": n, "t": t, "r": r_eff, "kind": "cdom_threshold",
-                    "uncompressed": [int(w) for w in bm.decompress(got).words]})
+                    "uncompressed": [int(w) for w in bm.decompress(got).words], "stats": st})
         spec = oracle.SymmetricSpec.interval(n, 1, max(1, n // 3))
         exp = oracle.brute_symmetric(sets, spec, r_eff)
-        got = runmerge.cdom_symmetric(comp, spec)
+        st = {}
+        got = runmerge.cdom_symmetric(comp, spec, stats=st)
         assert got.positions() == exp
         wr.add([c.words for c in comp], [c.bit_length for c in comp], got.words,
                {"n": n, "accept": [int(a) for a in spec.accept], "r": r_eff, "kind": "cdom_symmetric",
-                "uncompressed": [int(w) for w in bm.decompress(got).words]})
+                "uncompressed": [int(w) for w in bm.decompress(got).words], "stats": st})
         spec = oracle.SymmetricSpec((True,) + tuple(rng.random() < 0.5 for _ in range(n)))
         exp = oracle.brute_symmetric(sets, spec, r_eff)
-        got = runmerge.cdom_symmetric(comp, spec)
+        st = {}
+        got = runmerge.cdom_symmetric(comp, spec, stats=st)
         assert got.positions() == exp
         wr.add([c.words for c in comp], [c.bit_length for c in comp], got.words,
                {"n": n, "accept": [int(a) for a in spec.accept], "r": r_eff, "kind": "cdom_symmetric",
-                "uncompressed": [int(w) for w in bm.decompress(got).words]})
+                "uncompressed": [int(w) for w in bm.decompress(got).words], "stats": st})
     wr.save()
 
 
@@ -581,10 +584,12 @@ def baseline_cases():
     for c in comp[:16]:  # the generator's streams are canonical reference encodings
         assert bm.compress(bm.decompress(c)).words == c.words
     for t in (5, 10, 20, 50):
-        res = runmerge.cdom_threshold(comp, t)
+        st = {}
+        res = runmerge.cdom_threshold(comp, t, stats=st)
         u = bm.decompress(res)
         put(f"c4_t{t}", padded(u, r // 64), {"n": n, "r": r, "t": t, "m1": 256.0, "m0": 12544.0,
-                                              "card": u.cardinality(), "rle_out_len": len(res.words)})
+                                              "card": u.cardinality(), "rle_out_len": len(res.words),
+                                              "stats": st})
         print("C4 T", t, "done", u.cardinality())
     out["meta"] = np.array(json.dumps(meta))
     path = os.path.join(HERE, "baseline.npz")

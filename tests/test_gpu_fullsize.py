@@ -153,7 +153,8 @@ def test_c4_full_size_bit_exact(bq):
         streams = list(ex.map(lambda i: _markov(lib, i, r), range(n)))
     d = [torch.from_numpy(s.view(np.int64)).cuda() for s in streams]
     q = bq.RleQuery(d, r)
-    exp = O.cdom_threshold(streams, r, t)
+    st = {}
+    exp = O.cdom_threshold(streams, r, t, stats=st)
     z, _ = _baseline()
     assert np.array_equal(exp[: 1 << 14], z["c4_t50"])  # the reference's answer on the first 2^20 bits
     for _ in range(2):
@@ -161,6 +162,7 @@ def test_c4_full_size_bit_exact(bq):
         assert np.array_equal(_host(out[:nw]), exp)
         assert int(pc.item()) == _popcount(exp)
     assert q.layout_stats[0] > 0
+    assert q.sweep_stats(t) == st  # K8: the sweep's segments / heap_pops / branches at full size
 
 
 def test_c5_full_size_properties(bq):

@@ -120,6 +120,31 @@ def test_api_validates_before_touching_the_device():
         bq.cdom_threshold(ins, 2)
 
 
+@pytest.mark.parametrize("n,r,budget", [(3, 1 << 31, 1 << 30), (200, (1 << 29) + 8, 1 << 30), (3, 1000, 124)])
+def test_scan_count_budget_contract(n, r, budget):
+    """counters.py:54-57: r counters of counter_width(N) bits over the budget raise
+    ResourceError with the reference's message, before any device work."""
+    import paper_1402_4073_b200 as bq
+
+    ins = [bq.UncompressedBitmap([1], r) for _ in range(n)]
+    width = bq.api.counter_width(n)
+    with pytest.raises(bq.ResourceError) as ours:
+        bq.scan_count(ins, 1, budget_bytes=budget)
+    assert str(ours.value) == (f"{r} counters of {width} bits exceed the {budget}-byte budget; "
+                               "consider hash_count")
+    try:
+        import sys
+
+        sys.path.insert(0, os.environ.get("BQ_REFERENCE_SRC", "/root/reference/pkg/src"))
+        from bitquorum import bitmaps as rbm
+        from bitquorum import counters
+    except Exception:
+        return
+    with pytest.raises(Exception) as ref:
+        counters.scan_count([rbm.UncompressedBitmap([1], r) for _ in range(n)], 1, budget_bytes=budget)
+    assert type(ref.value).__name__ == "ResourceError" and str(ref.value) == str(ours.value)
+
+
 def test_op_count_formulas_match_reference():
     import paper_1402_4073_b200 as bq
 

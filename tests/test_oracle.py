@@ -37,11 +37,13 @@ def test_symmetric_matches_reference(case):
 @pytest.mark.parametrize("case", RLE, ids=lambda c: c.id)
 def test_cdom_matches_reference(case):
     exp_u = padded(np.array(case.meta["uncompressed"], dtype=np.uint64), case.r)
+    st = {}
     if case.meta["kind"] == "cdom_threshold":
-        got = O.cdom_threshold(case.inputs, case.r, case.meta["t"])
+        got = O.cdom_threshold(case.inputs, case.r, case.meta["t"], stats=st)
     else:
-        got = O.cdom_symmetric(case.inputs, case.r, case.meta["accept"])
+        got = O.cdom_symmetric(case.inputs, case.r, case.meta["accept"], stats=st)
     assert np.array_equal(got, exp_u)
+    assert st == case.meta["stats"]  # segments, heap_pops, branches (runmerge.py:237-240)
     # the reference returns the canonical encoding of those words
     assert np.array_equal(O.rle_compress(O.trim(got), case.r), case.out)
 
@@ -155,5 +157,7 @@ def test_oracle_cdom_matches_reference_on_c4_prefix():
     streams = [O.gen_markov_rle(1402, i, 1 << 20, 256.0, 12544.0) for i in range(1024)]
     for t in (5, 10, 20, 50):
         m = meta[f"c4_t{t}"]
-        got = O.cdom_threshold(streams, m["r"], t)
+        st = {}
+        got = O.cdom_threshold(streams, m["r"], t, stats=st)
         assert np.array_equal(got, z[f"c4_t{t}"]), t
+        assert st == m["stats"], t
