@@ -25,6 +25,7 @@ from .api import (
     execute,
     execute_horizontal,
     cdom_symmetric,
+    dirty_segment_solver,
     cdom_threshold,
     compress,
     compress_device,

@@ -368,6 +368,51 @@ def cdom_symmetric(bitmaps: Sequence, spec, stats: dict | None = None):
     return res
 
 
+SCANCOUNT_CUTOFF = 128  # runmerge.py:25
+
+
+def dirty_segment_solver(blocks: Sequence[Sequence[int]], t_eff: int, force_branch: str | None = None,
+                         scancount_cutoff: int = SCANCOUNT_CUTOFF, stats: dict | None = None) -> list:
+    """runmerge.dirty_segment_solver (runmerge.py:59-126): per-word threshold over
+    aligned blocks of dirty words, ``blocks[i][w]`` being input i's word at offset w.
+    The dispatch (or / and / scan / looped, :69-83) is reproduced for ``stats`` and
+    ``force_branch`` is validated as the reference does; every branch computes the
+    same function, which is evaluated by the device's counting kernel (K1)."""
+    nd = len(blocks)
+    if not 1 <= t_eff <= nd:
+        raise InputError(f"effective threshold {t_eff} outside [1, {nd}]")
+    width = len(blocks[0])
+    arr = np.array([list(b) for b in blocks], dtype=np.uint64).reshape(nd, width)
+    branch = force_branch
+    if branch is None:
+        if t_eff == 1:
+            branch = "or"
+        elif t_eff == nd:
+            branch = "and"
+        elif t_eff >= scancount_cutoff:
+            branch = "scan"
+        else:
+            beta = int(np.unpackbits(arr.view(np.uint8)).sum()) if arr.size else 0
+            branch = "looped" if 2 * beta >= nd * t_eff else "scan"
+    if stats is not None:
+        stats[branch] = stats.get(branch, 0) + 1
+    if branch not in ("or", "and", "looped", "scan"):
+        raise InputError(f"unknown branch {force_branch!r}")
+    if width == 0:
+        return []
+    device = torch.device("cuda", torch.cuda.current_device())
+    pitch = (width + 1) & ~1  # rows 16-byte aligned (bq.h)
+    padded = np.zeros((nd, pitch), dtype=np.uint64)
+    padded[:, :width] = arr
+    rows = torch.from_numpy(padded.view(np.int64)).to(device)
+    q = ThresholdQuery([DeviceBitmap(rows[i], 64 * width, width) for i in range(nd)], 64 * width, device=device)
+    try:
+        out, _ = q.threshold(t_eff)
+        return [int(w) for w in out[:width].cpu().numpy().view(np.uint64)]
+    finally:
+        q.close()
+
+
 def wide_or(bitmaps: list):
     """bitmaps.wide_or (bitmaps.py:647-667)."""
     if not bitmaps:

@@ -103,3 +103,33 @@ def test_drop_in_entry_points_with_reference_objects(bq, datasets):
         bq.CircuitLibrary(n_max=16).threshold(u, 3)
     with pytest.raises(InputError):  # the harness's DNF class (competitions.py:272-274)
         bq.csv_threshold(u, 24)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_dirty_segment_solver_every_branch(bq, seed):
+    """runmerge.dirty_segment_solver (runmerge.py:59-126): the dispatch counts and
+    the words, with each branch forced (SPEC's cross-branch equality) and unforced,
+    against the reference's own solver on the same blocks."""
+    import random
+
+    from bitquorum import runmerge
+
+    rng = random.Random(seed)
+    nd = rng.choice([1, 2, 5, 40, 130, 200])
+    width = rng.choice([1, 3, 17, 64])
+    dens = rng.choice([0.02, 0.5, 0.95])
+    blocks = [[sum(1 << b for b in range(64) if rng.random() < dens) for _ in range(width)] for _ in range(nd)]
+    for t in sorted({1, nd, max(1, nd // 3), min(nd, 129)}):
+        exp_st, got_st = {}, {}
+        exp = runmerge.dirty_segment_solver(blocks, t, stats=exp_st)
+        assert bq.dirty_segment_solver(blocks, t, stats=got_st) == exp
+        assert got_st == exp_st
+        for br in ("or", "and", "scan", "looped"):
+            # forced branches only compute the threshold when they apply (OR: T=1, AND: T=nd)
+            if (br == "or" and t != 1) or (br == "and" and t != nd):
+                continue
+            assert bq.dirty_segment_solver(blocks, t, force_branch=br) == exp
+    with pytest.raises(bq.InputError):
+        bq.dirty_segment_solver(blocks, nd + 1)
+    with pytest.raises(bq.InputError):
+        bq.dirty_segment_solver(blocks, 1, force_branch="heap")
