@@ -53,6 +53,9 @@ namespace bq {
 #ifndef BQ_DIR_SEG
 #define BQ_DIR_SEG 64
 #endif
+#ifndef BQ_DIR_LDS
+#define BQ_DIR_LDS 1
+#endif
 #ifndef BQ_DIR_CONTIG
 #define BQ_DIR_CONTIG 0
 #endif
@@ -97,6 +100,12 @@ __device__ __forceinline__ unsigned long long ld_link(const unsigned long long *
 
 __device__ __forceinline__ void st_link(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t lds64(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
 }
 
 __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ DirArgs a) {
@@ -144,6 +153,8 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     // stream word p is slot[p - sbase] (sbase = h0 or h0 - 1 after the widening: -1 at a
     // stream that starts 8 bytes into a 16-byte line)
     const int64_t sbase = ((intptr_t)g0 - reinterpret_cast<intptr_t>(s)) / 8;
+    // the walks load through 32-bit shared addresses (no generic-to-shared conversion per step)
+    const uint32_t slot_s = (uint32_t)__cvta_generic_to_shared(slot);
     const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
     if (lane == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_s), "r"(kArrivals) : "memory");
@@ -211,7 +222,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
         span = 0;
         uint32_t i = (uint32_t)((int64_t)from - sbase);
         while (i < iend) {
-            const uint64_t w = slot[i];
+            const uint64_t w = BQ_DIR_LDS ? lds64(slot_s + i * 8u) : slot[i];
             const uint32_t dirty = (uint32_t)(w >> 33);
             span += (uint64_t)(uint32_t)(w >> 1) + dirty;
             i += 1 + dirty;
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     uint32_t i = active ? (uint32_t)((int64_t)entry - sbase) : iend;
     auto dir_walk = [&](auto tail_check) {
         while (i < iend) {
-            const uint64_t w = slot[i];
+            const uint64_t w = BQ_DIR_LDS ? lds64(slot_s + i * 8u) : slot[i];
             const uint32_t dirty = (uint32_t)(w >> 33);
             const uint64_t end = pos + (uint32_t)(w >> 1) + dirty;
             if (end > nb) {  // the marker covers boundary nb (< rlim)

@@ -8,7 +8,7 @@ CS=$ROOT/paper_1402_4073_b200/csrc
 B=$CS/_build_$NAME
 mkdir -p $B $ROOT/_variants
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-for f in bq_api bq_count bq_gen bq_rle bq_rle_dir bq_rle_sliced bq_encode bq_program bq_similarity; do
+for f in $(cd $CS && ls *.cu | sed "s/\.cu$//"); do
   /usr/local/cuda/bin/nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -cudart static \
     --expt-relaxed-constexpr $DEFS -c $CS/$f.cu -o $B/$f.o 2> $B/$f.log &
 done
