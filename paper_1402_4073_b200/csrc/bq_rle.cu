@@ -49,9 +49,6 @@ constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a priva
 #ifndef BQ_K4_MINB
 #define BQ_K4_MINB 4
 #endif
-#ifndef BQ_K4_COPY
-#define BQ_K4_COPY 0  // segment staging: 0 = one TMA bulk copy per lane, 1 = per-lane 16-byte cp.async
-#endif
 #ifndef BQ_K4_ZERO_ADDS
 #define BQ_K4_ZERO_ADDS 1
 #endif
@@ -265,15 +262,6 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
                 sg.staged = true;
                 sg.off = off + (uint32_t)((reinterpret_cast<uintptr_t>(sg.g) >> 3) & 1);
                 const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pool + (size_t)(k & 1) * kPoolWords + off);
-#if BQ_K4_COPY == 1
-                // per-lane 16-byte cp.async (per-thread addresses: one instruction per vector
-                // for the whole warp), completion counted by the mbarrier as this lane's arrival
-                for (uint32_t j = 0; j < len; j += 2)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + j * 8), "l"(b0 + j * 8)
-                                 : "memory");
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-                return;
-#endif
                 const uint32_t bytes = len * 8;
                 asm volatile(
                     "{\n\t.reg .b64 st;\n\t"
