@@ -65,7 +65,11 @@ constexpr int kBlockWords = kSegWords * 32;          // one warp = one block of 
 constexpr int kHalo = 8;                             // words before a segment holding its entry guesses
 // a lane's staging slot: halo + segment + 16-byte alignment slack, its stride = 16 bytes
 // mod 128 so the lanes' slots start in different shared-memory banks
-constexpr int kSlotWords = ((kHalo + kSegWords + 2 + 15) / 16) * 16 + 2;
+#ifndef BQ_DIR_SLOT_HALO
+#define BQ_DIR_SLOT_HALO 0  // 1: each slot also holds its kHalo words (82-word slots, 10 warps/SM)
+#endif
+// 0: the halo is read from the left neighbour's slot (lane 0: from HBM), 66-word slots, 13 warps/SM
+constexpr int kSlotWords = ((BQ_DIR_SLOT_HALO * kHalo + kSegWords + 2 + 15) / 16) * 16 + 2 - 16 * (1 - BQ_DIR_SLOT_HALO);
 
 struct DirArgs {
     const uint64_t *const *ptrs;
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     uint64_t *slot = slots;
     constexpr uint32_t kArrivals = 1;
 #else
-    const uint32_t h0 = q >= (uint32_t)kHalo ? q - kHalo : 0;
+    const uint32_t h0 = BQ_DIR_SLOT_HALO ? (q >= (uint32_t)kHalo ? q - kHalo : 0) : q;
     const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + h0) & ~(uintptr_t)15;
     const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + qe) + 15) & ~(uintptr_t)15;
     const uint32_t bytes = active ? (uint32_t)(g1 - g0) : 0u;
@@ -187,13 +191,24 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
 
     // speculative entry: the landing most of the kHalo hypotheses agree on (smallest on a tie)
     uint32_t entry = q;
+#if !BQ_DIR_SLOT_HALO
+    // the halo words [q - kHalo, q): the end of the left neighbour's slot (its sbase by shuffle;
+    // it is active whenever this lane is), lane 0 reads the previous block's last words
+    const int64_t sbase_left = __shfl_up_sync(0xffffffffu, sbase, 1);
+    const uint32_t halo_s = lane ? slot_s - (uint32_t)kSlotWords * 8u + (uint32_t)((int64_t)q - kHalo - sbase_left) * 8u : 0u;
+#endif
     if (active && q > 0) {
         // landings saturate at 2^32 - 1 (beyond any stream): never a valid entry
         uint32_t land[kHalo];
 #pragma unroll
         for (int j = kHalo - 1; j >= 0; --j) {
             const uint32_t h = q - kHalo + j;
-            const uint64_t nx64 = (uint64_t)h + 1 + (slot[(int64_t)h - sbase] >> 33);
+#if BQ_DIR_SLOT_HALO
+            const uint64_t hw = slot[(int64_t)h - sbase];
+#else
+            const uint64_t hw = lane ? lds64(halo_s + (uint32_t)j * 8u) : __ldg(s + h);
+#endif
+            const uint64_t nx64 = (uint64_t)h + 1 + (hw >> 33);
             const uint32_t nx = nx64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)nx64;
             uint32_t v = nx;
 #pragma unroll
