@@ -51,25 +51,21 @@
 namespace bq {
 
 #ifndef BQ_DIR_SEG
-#define BQ_DIR_SEG 64
+#define BQ_DIR_SEG 48
 #endif
 #ifndef BQ_DIR_LDS
 #define BQ_DIR_LDS 1
-#endif
-#ifndef BQ_DIR_CONTIG
-#define BQ_DIR_CONTIG 0
 #endif
 
 constexpr int kSegWords = BQ_DIR_SEG;                // stream words per segment (one lane)
 constexpr int kBlockWords = kSegWords * 32;          // one warp = one block of 32 segments
 constexpr int kHalo = 8;                             // words before a segment holding its entry guesses
-// a lane's staging slot: halo + segment + 16-byte alignment slack, its stride = 16 bytes
-// mod 128 so the lanes' slots start in different shared-memory banks
-#ifndef BQ_DIR_SLOT_HALO
-#define BQ_DIR_SLOT_HALO 0  // 1: each slot also holds its kHalo words (82-word slots, 10 warps/SM)
-#endif
-// 0: the halo is read from the left neighbour's slot (lane 0: from HBM), 66-word slots, 13 warps/SM
-constexpr int kSlotWords = ((BQ_DIR_SLOT_HALO * kHalo + kSegWords + 2 + 15) / 16) * 16 + 2 - 16 * (1 - BQ_DIR_SLOT_HALO);
+// a lane's staging slot: segment + 16-byte alignment slack (the halo words are read
+// from the left neighbour's slot, lane 0's from HBM), its stride = 16 bytes mod 128 so
+// the lanes' slots start in different shared-memory banks.  48-word segments: 50-word
+// slots, 12.8 KB per warp, 17 warps per SM (C4: 64-word segments with their own halo
+// 0.90 ms, without 0.80, 48-word 0.77, 32-word 0.82)
+constexpr int kSlotWords = ((kSegWords + 15) / 16) * 16 + 2;
 
 struct DirArgs {
     const uint64_t *const *ptrs;
@@ -113,13 +109,7 @@ __device__ __forceinline__ uint64_t lds64(uint32_t addr) {
 }
 
 __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ DirArgs a) {
-#if BQ_DIR_CONTIG
-    // one contiguous copy of the block [b0 - kHalo, b1): a lane's halo is its left
-    // neighbour's tail (less shared memory per warp, more warps per SM)
-    __shared__ __align__(16) uint64_t slots[kHalo + kBlockWords + 4];
-#else
     __shared__ __align__(16) uint64_t slots[32 * kSlotWords];
-#endif
     __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x;
 
@@ -137,31 +127,18 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const uint32_t q = blk * (uint32_t)kBlockWords + (uint32_t)lane * kSegWords;
     const bool active = q < L;
     const uint32_t qe = active ? min(q + (uint32_t)kSegWords, L) : q;
-#if BQ_DIR_CONTIG
-    const uint32_t b0 = blk * (uint32_t)kBlockWords;
-    const uint32_t h0 = b0 >= (uint32_t)kHalo ? b0 - kHalo : 0;
-    const uint32_t b1 = min(b0 + (uint32_t)kBlockWords, L);
-    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + h0) & ~(uintptr_t)15;
-    const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + b1) + 15) & ~(uintptr_t)15;
-    const uint32_t bytes = (lane == 0 && b1 > h0) ? (uint32_t)(g1 - g0) : 0u;
-    uint64_t *slot = slots;
-    constexpr uint32_t kArrivals = 1;
-#else
-    const uint32_t h0 = BQ_DIR_SLOT_HALO ? (q >= (uint32_t)kHalo ? q - kHalo : 0) : q;
-    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + h0) & ~(uintptr_t)15;
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + q) & ~(uintptr_t)15;
     const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + qe) + 15) & ~(uintptr_t)15;
     const uint32_t bytes = active ? (uint32_t)(g1 - g0) : 0u;
     uint64_t *slot = slots + lane * kSlotWords;
-    constexpr uint32_t kArrivals = 32;
-#endif
-    // stream word p is slot[p - sbase] (sbase = h0 or h0 - 1 after the widening: -1 at a
-    // stream that starts 8 bytes into a 16-byte line)
+    // stream word p is slot[p - sbase] (sbase = q or q - 1 after the widening: -1 at a
+    // segment that starts 8 bytes into a 16-byte line)
     const int64_t sbase = ((intptr_t)g0 - reinterpret_cast<intptr_t>(s)) / 8;
     // the walks load through 32-bit shared addresses (no generic-to-shared conversion per step)
     const uint32_t slot_s = (uint32_t)__cvta_generic_to_shared(slot);
     const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
     if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_s), "r"(kArrivals) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_s), "r"(32) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
@@ -173,7 +150,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
                          (uint32_t)__cvta_generic_to_shared(slot)),
                      "l"(g0), "r"(bytes), "r"(bar_s)
                      : "memory");
-    } else if (kArrivals == 32 || lane == 0) {
+    } else {
         asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar_s) : "memory");
     }
     // the previous block's exit is published by now in the common case: fetch it while
@@ -191,23 +168,17 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
 
     // speculative entry: the landing most of the kHalo hypotheses agree on (smallest on a tie)
     uint32_t entry = q;
-#if !BQ_DIR_SLOT_HALO
     // the halo words [q - kHalo, q): the end of the left neighbour's slot (its sbase by shuffle;
     // it is active whenever this lane is), lane 0 reads the previous block's last words
     const int64_t sbase_left = __shfl_up_sync(0xffffffffu, sbase, 1);
     const uint32_t halo_s = lane ? slot_s - (uint32_t)kSlotWords * 8u + (uint32_t)((int64_t)q - kHalo - sbase_left) * 8u : 0u;
-#endif
     if (active && q > 0) {
         // landings saturate at 2^32 - 1 (beyond any stream): never a valid entry
         uint32_t land[kHalo];
 #pragma unroll
         for (int j = kHalo - 1; j >= 0; --j) {
             const uint32_t h = q - kHalo + j;
-#if BQ_DIR_SLOT_HALO
-            const uint64_t hw = slot[(int64_t)h - sbase];
-#else
             const uint64_t hw = lane ? lds64(halo_s + (uint32_t)j * 8u) : __ldg(s + h);
-#endif
             const uint64_t nx64 = (uint64_t)h + 1 + (hw >> 33);
             const uint32_t nx = nx64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)nx64;
             uint32_t v = nx;
