@@ -65,7 +65,11 @@ constexpr int kHalo = 8;                             // words before a segment h
 // the lanes' slots start in different shared-memory banks.  48-word segments: 50-word
 // slots, 12.8 KB per warp, 17 warps per SM (C4: 64-word segments with their own halo
 // 0.90 ms, without 0.80, 48-word 0.77, 32-word 0.82)
-constexpr int kSlotWords = ((kSegWords + 15) / 16) * 16 + 2;
+#ifndef BQ_DIR_GROUP
+#define BQ_DIR_GROUP 4
+#endif
+constexpr int kGroup = BQ_DIR_GROUP;  // consecutive segments staged by one bulk copy into one slot
+constexpr int kSlotWords = ((kGroup * kSegWords + 15) / 16) * 16 + 2;
 
 struct DirArgs {
     const uint64_t *const *ptrs;
@@ -109,7 +113,7 @@ __device__ __forceinline__ uint64_t lds64(uint32_t addr) {
 }
 
 __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ DirArgs a) {
-    __shared__ __align__(16) uint64_t slots[32 * kSlotWords];
+    __shared__ __align__(16) uint64_t slots[(32 / kGroup) * kSlotWords];
     __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x;
 
@@ -127,10 +131,13 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const uint32_t q = blk * (uint32_t)kBlockWords + (uint32_t)lane * kSegWords;
     const bool active = q < L;
     const uint32_t qe = active ? min(q + (uint32_t)kSegWords, L) : q;
-    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + q) & ~(uintptr_t)15;
-    const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + qe) + 15) & ~(uintptr_t)15;
-    const uint32_t bytes = active ? (uint32_t)(g1 - g0) : 0u;
-    uint64_t *slot = slots + lane * kSlotWords;
+    // the lane's group of kGroup segments [gq, gqe), copied by its first lane
+    const uint32_t gq = blk * (uint32_t)kBlockWords + (uint32_t)(lane / kGroup) * (kGroup * kSegWords);
+    const uint32_t gqe = gq < L ? min(gq + (uint32_t)(kGroup * kSegWords), L) : gq;
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(s + gq) & ~(uintptr_t)15;
+    const uintptr_t g1 = (reinterpret_cast<uintptr_t>(s + gqe) + 15) & ~(uintptr_t)15;
+    const uint32_t bytes = (lane % kGroup == 0 && gq < L) ? (uint32_t)(g1 - g0) : 0u;
+    uint64_t *slot = slots + (lane / kGroup) * kSlotWords;
     // stream word p is slot[p - sbase] (sbase = q or q - 1 after the widening: -1 at a
     // segment that starts 8 bytes into a 16-byte line)
     const int64_t sbase = ((intptr_t)g0 - reinterpret_cast<intptr_t>(s)) / 8;
@@ -171,7 +178,8 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     // the halo words [q - kHalo, q): the end of the left neighbour's slot (its sbase by shuffle;
     // it is active whenever this lane is), lane 0 reads the previous block's last words
     const int64_t sbase_left = __shfl_up_sync(0xffffffffu, sbase, 1);
-    const uint32_t halo_s = lane ? slot_s - (uint32_t)kSlotWords * 8u + (uint32_t)((int64_t)q - kHalo - sbase_left) * 8u : 0u;
+    const uint32_t slot_left = __shfl_up_sync(0xffffffffu, slot_s, 1);
+    const uint32_t halo_s = lane ? slot_left + (uint32_t)((int64_t)q - kHalo - sbase_left) * 8u : 0u;
     if (active && q > 0) {
         // landings saturate at 2^32 - 1 (beyond any stream): never a valid entry
         uint32_t land[kHalo];
