@@ -51,7 +51,7 @@
 namespace bq {
 
 #ifndef BQ_DIR_SEG
-#define BQ_DIR_SEG 48
+#define BQ_DIR_SEG 32
 #endif
 #ifndef BQ_DIR_LDS
 #define BQ_DIR_LDS 1
@@ -60,11 +60,15 @@ namespace bq {
 constexpr int kSegWords = BQ_DIR_SEG;                // stream words per segment (one lane)
 constexpr int kBlockWords = kSegWords * 32;          // one warp = one block of 32 segments
 constexpr int kHalo = 8;                             // words before a segment holding its entry guesses
-// a lane's staging slot: segment + 16-byte alignment slack (the halo words are read
-// from the left neighbour's slot, lane 0's from HBM), its stride = 16 bytes mod 128 so
-// the lanes' slots start in different shared-memory banks.  48-word segments: 50-word
-// slots, 12.8 KB per warp, 17 warps per SM (C4: 64-word segments with their own halo
-// 0.90 ms, without 0.80, 48-word 0.77, 32-word 0.82)
+// Staging: a group of kGroup consecutive segments is copied by one TMA bulk copy
+// into one slot (its lanes' words are contiguous there; the halo words of a lane are
+// the end of its left neighbour's segment, in the same slot or the previous one, and
+// lane 0's come from HBM); slot stride = 16 bytes mod 128 so consecutive slots start
+// in different shared-memory banks.  32-word segments in groups of 4: 130-word slots,
+// 8.3 KB per warp, 27 warps per SM.  C4 directory: 64-word segments with per-lane
+// slots holding their own halo 0.90 ms; per-lane slots without the halo 0.80;
+// 48-word per-lane 0.77; 48-word groups of 2 / 4 / 8 0.735 / 0.721 / 0.733;
+// 32-word groups of 2 / 4 / 8 0.748 / 0.687 / 0.711; 24-word groups of 4 0.85.
 #ifndef BQ_DIR_GROUP
 #define BQ_DIR_GROUP 4
 #endif

@@ -1,6 +1,6 @@
 """Edge cases of the one-pass RLE directory (K3, csrc/bq_rle_dir.cu): the
 speculative per-segment entry guesses and their repair, literal groups spanning
-segments (48 words) and blocks (1536 words) and the decoupled look-back between
+segments (32 words) and blocks (1024 words) and the decoupled look-back between
 blocks, streams whose length is exactly a segment / block multiple, streams
 shorter than the guess window, 8-byte-misaligned stream starts, adversarial
 literal words that look like markers, and validation failures (truncated,
@@ -105,8 +105,8 @@ def test_long_literal_groups_cross_segments_and_blocks(bq, seed):
     _check_decode(bq, streams, rmax)
 
 
-@pytest.mark.parametrize("length", [1, 7, 8, 9, 47, 48, 49, 55, 56, 57, 63, 64, 65, 1535, 1536, 1537, 2047, 2048,
-                                    2049, 3072, 3073, 4096, 4097])
+@pytest.mark.parametrize("length", [1, 7, 8, 9, 31, 32, 33, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 2047,
+                                    2048, 2049, 3072, 3073, 4096, 4097])
 def test_stream_lengths_at_segment_and_block_edges(bq, length):
     """Streams of exactly `length` words: one made of markers only (non-canonical
     adjacent fills, which the decoder must accept), one a single marker followed
