@@ -46,6 +46,15 @@ constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a priva
 #ifndef BQ_K4_POOL
 #define BQ_K4_POOL 768
 #endif
+#ifndef BQ_K4_BUFS
+#define BQ_K4_BUFS 2  // staging pool halves per warp (1: single-buffered, more CTAs per SM)
+#endif
+#ifndef BQ_K4_C_ILP
+#define BQ_K4_C_ILP 4  // streams walked at once per thread in phase C
+#endif
+#ifndef BQ_K4_NO_C
+#define BQ_K4_NO_C 0
+#endif
 #ifndef BQ_K4_MINB
 #define BQ_K4_MINB 4
 #endif
@@ -107,7 +116,57 @@ __device__ __forceinline__ void walk_tile(const RleCountArgs &a, int st, uint32_
 }
 
 
-// Marker sweep of one stream over a tile of W words in 32-bit tile-relative
+// walk_tile over every stream st = first, first + stride, ... < n, U streams at a time
+// with their marker loads interleaved (U independent HBM loads in flight per thread
+// instead of one dependent chain): phase C's walks are latency-bound, and a tile that
+// needs them otherwise formed the tail of the grid.
+template <int U, typename Visit>
+__device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int stride, uint32_t tile, uint64_t ts,
+                                           uint64_t te, Visit &&visit) {
+    for (int base = first; base < a.n; base += U * stride) {
+        const uint64_t *sp[U];
+        uint64_t L[U], i[U], pos[U];
+        bool act[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int st = base + u * stride;
+            act[u] = st < a.n;
+            sp[u] = nullptr;
+            L[u] = i[u] = pos[u] = 0;
+            if (act[u]) {
+                sp[u] = a.ptrs[st];
+                L[u] = a.lens[st];
+                const uint2 e = a.dir[(size_t)tile * a.n + st];
+                i[u] = e.x;
+                pos[u] = e.y;
+                act[u] = i[u] < L[u] && pos[u] < te;
+            }
+        }
+        for (;;) {
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < U; ++u) any |= act[u];
+            if (!any) break;
+            uint64_t mk[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) mk[u] = act[u] ? __ldg(sp[u] + i[u]) : 0ull;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!act[u]) continue;
+                const uint64_t run = (mk[u] >> 1) & 0xFFFFFFFFull;
+                const uint64_t dirty = mk[u] >> 33;
+                const uint64_t fe = pos[u] + run, de = fe + dirty;
+                if (de > ts) visit(pos[u], fe, (uint32_t)(mk[u] & 1), fe, de, i[u] + 1, sp[u]);
+                pos[u] = de;
+                i[u] += 1 + dirty;
+                act[u] = i[u] < L[u] && pos[u] < te;
+            }
+        }
+    }
+}
+
+
+// Marker sweep of one stream over a tile of W words// Marker sweep of one stream over a tile of W words in 32-bit tile-relative
 // coordinates.  src[0] is the marker named by the stream's directory entry
 // (its fill run starts at word `pos`, at or before the tile); lim = stream
 // words available from there.  Each marker adds at most three entries to the
@@ -329,16 +388,15 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
 
     // ---- C: read dirty literals only where the fills leave the outcome open ----
     pc += tile_resolve<NT, kSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &&add_bits) {
-        for (int st = tid; st < a.n; st += NT) {
-            walk_tile(a, st, tile, ts, te,
-                      [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit, const uint64_t *s) {
-                          const uint64_t lo = max(ds, ts), hi = min(de, te);
-                          for (uint64_t p = lo; p < hi; ++p) {
-                              const uint16_t u = slot_of[p - ts];
-                              if (u != kNoSlot) add_bits(u, s + lit + (p - ds));
-                          }
-                      });
-        }
+        walk_tiles<BQ_K4_C_ILP>(a, tid, NT, tile, ts, te,
+                                [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit,
+                                    const uint64_t *s) {
+                                    const uint64_t lo = max(ds, ts), hi = min(de, te);
+                                    for (uint64_t p = lo; p < hi; ++p) {
+                                        const uint16_t u = slot_of[p - ts];
+                                        if (u != kNoSlot) add_bits(u, s + lit + (p - ds));
+                                    }
+                                });
     });
 
 #pragma unroll
