@@ -46,14 +46,8 @@ constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a priva
 #ifndef BQ_K4_POOL
 #define BQ_K4_POOL 768
 #endif
-#ifndef BQ_K4_BUFS
-#define BQ_K4_BUFS 2  // staging pool halves per warp (1: single-buffered, more CTAs per SM)
-#endif
 #ifndef BQ_K4_C_ILP
 #define BQ_K4_C_ILP 4  // streams walked at once per thread in phase C
-#endif
-#ifndef BQ_K4_NO_C
-#define BQ_K4_NO_C 0
 #endif
 #ifndef BQ_K4_MINB
 #define BQ_K4_MINB 4
