@@ -81,6 +81,14 @@ cudaError_t pool_alloc(void **p, size_t bytes) {
     return e;
 }
 
+cudaError_t pool_alloc_on(void **p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = device_pool(dev);
+    if (!pool) return cudaMalloc(p, bytes);
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
 void pool_free(void *p) {
     if (!p) return;
     if (cudaFreeAsync(p, 0) != cudaSuccess) cudaGetLastError();
@@ -218,7 +226,7 @@ struct bq_query {
     uint64_t *d_lens;
     std::vector<const uint64_t *> h_ptrs;  // host copy (small N: passed by value to the kernel)
     // device LUTs of MODE_LUT symmetric specs, uploaded once per distinct table
-    std::map<std::vector<uint32_t>, void *> luts;
+    std::map<std::vector<uint32_t>, CachedTable> luts;
     StreamUses uses;  // caller streams that evaluated this query (destroy waits on them)
     std::mutex mu;    // guards luts / uses
 };
@@ -309,7 +317,7 @@ BQ_API void bq_query_destroy(bq_query *q) {
     DeviceGuard dg;
     dg.set(q->device);
     pool_free_after(q->d_ptrs, q->uses);  // after the evaluations enqueued so far; no device sync
-    for (auto &kv : q->luts) pool_free_after(kv.second, q->uses);
+    for (auto &kv : q->luts) cached_table_free(kv.second, q->uses);
     q->uses.release();
     delete q;
 }
@@ -405,25 +413,30 @@ BQ_API int bq_query_symmetric(bq_query *q, const uint8_t *h_accept, uint64_t *d_
         {
             std::lock_guard<std::mutex> g(q->mu);
             auto it = q->luts.find(p.lut);
-            if (it != q->luts.end()) d_lut = it->second;
-            else if (q->luts.size() >= kMaxLuts) owned = true;
+            if (it != q->luts.end()) {
+                d_lut = it->second.p;
+                cudaError_t e = cached_table_use(it->second, s);  // after its upload, on any stream
+                if (e != cudaSuccess) return cuda_error(e, "lut wait");
+            } else if (q->luts.size() < kMaxLuts) {
+                CachedTable t;
+                cudaError_t e = cached_table_upload(t, p.lut.data(), p.lut.size() * 4, s);
+                if (e != cudaSuccess) {
+                    if (t.p) pool_free(t.p);
+                    if (t.ready) cudaEventDestroy(t.ready);
+                    return cuda_error(e, "lut upload");
+                }
+                d_lut = t.p;
+                q->luts.emplace(p.lut, t);
+            } else {
+                owned = true;
+            }
         }
-        if (!d_lut) {
-            const size_t bytes = p.lut.size() * 4;
-            cudaError_t e = pool_alloc(&d_lut, bytes);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(d_lut, p.lut.data(), bytes, cudaMemcpyHostToDevice, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (owned) {
+            cudaError_t e = pool_alloc(&d_lut, p.lut.size() * 4);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(d_lut, p.lut.data(), p.lut.size() * 4, cudaMemcpyHostToDevice, s);
             if (e != cudaSuccess) {
                 if (d_lut) pool_free(d_lut);
                 return cuda_error(e, "lut upload");
-            }
-            if (!owned) {
-                std::lock_guard<std::mutex> g(q->mu);
-                auto ins = q->luts.emplace(p.lut, d_lut);
-                if (!ins.second) {  // another thread uploaded the same table meanwhile
-                    pool_free(d_lut);
-                    d_lut = ins.first->second;
-                }
             }
         }
         a.lut = static_cast<const uint32_t *>(d_lut);

@@ -69,7 +69,32 @@ struct StreamUses {
 };
 // Free `p` once every evaluation noted in `uses` is done, without a host sync.
 void pool_free_after(void *p, const StreamUses &uses);
+// Stream-ordered: usable on `s` (and on other streams ordered after it) with no host sync.
+cudaError_t pool_alloc_on(void **p, size_t bytes, cudaStream_t s);
 int sm_count();              // SMs of the current device
+
+// A small immutable device table cached per query (accept / LUT tables).  Uploaded
+// on the first consuming stream with no host synchronisation; `ready` marks the
+// upload, and evaluations on any stream wait on it (stream-ordered, not host-side).
+struct CachedTable {
+    void *p = nullptr;
+    cudaEvent_t ready = nullptr;
+};
+inline cudaError_t cached_table_upload(CachedTable &t, const void *host, size_t bytes, cudaStream_t s) {
+    cudaError_t e = pool_alloc_on(&t.p, bytes, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(t.p, host, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(t.ready, s);
+    return e;
+}
+inline cudaError_t cached_table_use(const CachedTable &t, cudaStream_t s) {
+    return t.ready ? cudaStreamWaitEvent(s, t.ready, 0) : cudaSuccess;
+}
+inline void cached_table_free(CachedTable &t, const StreamUses &uses) {
+    if (t.p) pool_free_after(t.p, uses);
+    if (t.ready) cudaEventDestroy(t.ready);
+    t = CachedTable();
+}
 
 // ---- K1/K2: uncompressed counting kernel ------------------------------------
 constexpr int kMaxBreaks = 32;

@@ -418,7 +418,7 @@ struct bq_rle_query {
     SlicedLayout sliced;  // tile-sliced layout (K4s), the default derived layout
     // device accept / const_until / breakpoint tables by accept vector: immutable once
     // uploaded, so repeated evaluations (same T) need no allocation or copy
-    std::map<std::vector<uint8_t>, void *> tables;
+    std::map<std::vector<uint8_t>, CachedTable> tables;
     StreamUses uses;              // caller streams that evaluated this query (destroy waits on them)
     mutable std::mutex build_mu;  // guards evals / sliced_tried / sliced / tables / uses
 };
@@ -562,7 +562,7 @@ BQ_API void bq_rle_query_destroy(bq_rle_query *q) {
     // enqueued on the caller's streams are done; no device-wide synchronisation
     pool_free_after(q->mem, q->uses);
     free_sliced(&q->sliced, &q->uses);
-    for (auto &kv : q->tables) pool_free_after(kv.second, q->uses);
+    for (auto &kv : q->tables) cached_table_free(kv.second, q->uses);
     q->uses.release();
     delete q;
 }
@@ -632,18 +632,19 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         std::lock_guard<std::mutex> guard(q->build_mu);
         auto it = q->tables.find(acc);
         if (it != q->tables.end()) {
-            d_tab = it->second;
+            d_tab = it->second.p;
+            e = cached_table_use(it->second, s);  // ordered after its upload, whichever stream did it
+            if (e != cudaSuccess) return cuda_error(e, "accept table wait");
         } else if (q->tables.size() < kMaxTables) {
-            e = pool_alloc(reinterpret_cast<void **>(&d_tab), bytes);
-            // ordered on the consuming stream, and complete before the table is shared
-            // with evaluations on other streams
-            if (e == cudaSuccess) e = cudaMemcpyAsync(d_tab, host.data(), bytes, cudaMemcpyHostToDevice, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            CachedTable t;
+            e = cached_table_upload(t, host.data(), bytes, s);
             if (e != cudaSuccess) {
-                if (d_tab) pool_free(d_tab);
+                if (t.p) pool_free(t.p);
+                if (t.ready) cudaEventDestroy(t.ready);
                 return cuda_error(e, "accept table upload");
             }
-            q->tables.emplace(acc, d_tab);
+            d_tab = t.p;
+            q->tables.emplace(acc, t);
         }
     }
     if (!d_tab) {
