@@ -196,17 +196,20 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
     uint32_t i = 1 + dirty;
     while (i < lim) {
         mk = load(i);
-        dirty = (uint32_t)(mk >> 33);
+        const uint32_t hi = (uint32_t)(mk >> 32);
+        dirty = hi >> 1;
         const uint32_t run = min((uint32_t)(mk >> 1), Wu);
-        const uint32_t ones = (uint32_t)(mk & 1) & (run != 0u);
+        // a zero-length one-fill adds +1 and -1 at the same word; an update at fe = W lands in
+        // the sentinel slot past the tile (both cheaper than testing for them)
+        const uint32_t ones = (uint32_t)mk & 1u;
         const uint32_t fe_raw = rel + run;       // <= 2W
         const uint32_t de_raw = fe_raw + dirty;  // < 2^32: dirty < 2^31
         const uint32_t fe = min(fe_raw, Wu);
-        const bool lit = (dirty != 0u) & (fe < Wu);
+        const uint32_t litv = hi >= 2u ? 0x10000u : 0u;  // the marker has literals
         // two reductions per marker: (previous literals end | this one-fill starts) at rel,
         // (this one-fill ends | this marker's literals start) at fe
         const uint32_t at_rel = carry + ones;
-        const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
+        const uint32_t at_fe = litv - ones;
         // byte offsets as index * four (runtime 4): IMAD on the FMA pipe instead of an ALU LEA
 #if BQ_K4_ZERO_ADDS
         // an empty update adds 0 to its real slot (rare on C4: markers are literal groups)
@@ -216,7 +219,7 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
         atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_rel ? rel : dummy) * four), at_rel);
         atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_fe ? fe : dummy) * four), at_fe);
 #endif
-        carry = lit ? 0xFFFF0000u : 0u;
+        carry = 0u - litv;
         if (de_raw >= Wu) return;  // the pending literal end lies past the tile
         rel = de_raw;
         i += 1 + dirty;
