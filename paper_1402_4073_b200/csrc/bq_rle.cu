@@ -500,7 +500,9 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
     q->tile0 = tile0;
     q->ntiles = ntiles;
     q->dir_bytes = dirb;
-    cudaError_t e = pool_alloc(reinterpret_cast<void **>(&q->mem), bytes);
+    // stream-ordered on the legacy stream, like every use below; the build synchronises
+    // that stream before returning, so the query is usable from any stream afterwards
+    cudaError_t e = pool_alloc_on(reinterpret_cast<void **>(&q->mem), bytes, 0);
     if (e != cudaSuccess) {
         delete q;
         return cuda_error(e, "cudaMalloc(rle directory)");
