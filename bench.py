@@ -674,7 +674,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
     tile-sliced layout derived from the streams (built once, at the second
     evaluation); they are reported separately under ``repeated_query`` with the
     bytes K4s actually moves and the layout build cost."""
-    n, r, t = 1024, 1 << 30, 50
+    n, r, t = 1024, 1 << 30, args.c4_t
     m1, m0 = 256.0, 12544.0
     t_gen = time.perf_counter()
     streams = _markov_streams(lib, n, r, m1, m0, host_threads())
@@ -814,7 +814,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
     line = _line("c4", comp_bytes * out_words / nw / (fresh_mean / 1e3) / 1e9, fresh_ms, fresh_bytes, len(fresh_ms),
                  args.warmup,
                  {"workload": "C4: N=1024 RLE (EWAH-style) bitmaps, r=2^30 bits, Markov runs (ones mean 256, zeros "
-                              "mean 12544 bits; density 0.02), T=50; output uncompressed. One step = one FRESH query "
+                              f"mean 12544 bits; density 0.02), T={t}; output uncompressed. One step = one FRESH query "
                               "over device-resident streams: K3 directory (bq_rle_query_create) + first evaluation "
                               "(K4 reads the streams); CUDA events around both; streams (2.4 GB) > L2",
                   "n_bitmaps": n, "r_bits": r, "t": t, "compressed_bytes": comp_bytes,
@@ -1163,6 +1163,7 @@ def main():
                     help="--impl reference: skip timing the stock reference Python (context numbers)")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 strong-scaling fields of the default line")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--c4-t", type=int, default=50, help="C4 threshold (BASELINE configs[3]: 50; others are diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
