@@ -46,11 +46,14 @@ constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a priva
 #ifndef BQ_K4_POOL
 #define BQ_K4_POOL 768
 #endif
+#ifndef BQ_K4_BUFS
+#define BQ_K4_BUFS 1  // staging pool halves per warp (2: double-buffered, 4 CTAs/SM; 1: 7 CTAs/SM)
+#endif
 #ifndef BQ_K4_C_ILP
 #define BQ_K4_C_ILP 4  // streams walked at once per thread in phase C
 #endif
 #ifndef BQ_K4_MINB
-#define BQ_K4_MINB 4
+#define BQ_K4_MINB 7
 #endif
 #ifndef BQ_K4_ZERO_ADDS
 #define BQ_K4_ZERO_ADDS 1
@@ -59,9 +62,9 @@ constexpr int kPoolWords = BQ_K4_POOL;  // words per warp pool half (two halves:
                                         // C4 needs ~613 words per 32 streams on average, 760 at p99
 constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
 
-constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * 2 * kPoolWords * 8;
-constexpr size_t kPhaseCBytes = tile_resolve_bytes<kSlotsPerBatch>() + (size_t)kRleTile * 2;  // + undecided list
-constexpr size_t kRegionBytes = kPoolBytes > kPhaseCBytes ? kPoolBytes : kPhaseCBytes;
+constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * BQ_K4_BUFS * kPoolWords * 8;
+// phase A's pools; phase B lists the undecided words over them once phase A is done
+constexpr size_t kRegionBytes = kPoolBytes > (size_t)kRleTile * 2 ? kPoolBytes : (size_t)kRleTile * 2;
 
 inline size_t rle_smem_bytes() {
     return kCntBytes + kRegionBytes;
@@ -85,6 +88,11 @@ struct RleCountArgs {
     unsigned long long *popcnt;
     int debug;  // experiment knob (BQ_RLE_DEBUG): 1 = skip marker walks, 2 = also skip copies
     uint32_t four;  // 4 as a runtime value (see sweep_stream)
+    // phase C deferred to rle_resolve_kernel: a tile with undecided words appends itself to
+    // todo[] and leaves its scanned counts in todo_cnt[slot][kRleTile]
+    uint32_t *todo_count;
+    uint32_t *todo;
+    uint32_t *todo_cnt;
 };
 
 
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
                 q.p = a.ptrs[st];
             }
         };
-        uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * 2 * kPoolWords;
+        uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * BQ_K4_BUFS * kPoolWords;
         // one mbarrier per pool half; 32 arrivals (one per lane) + the TMA byte count complete a phase
         uint64_t *bars = reinterpret_cast<uint64_t *>(cnt + kRleTile + 36) + warp * 2;
         const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
@@ -313,11 +321,11 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
                 if (lane >= o) incl += v;
             }
             const uint32_t off = incl - len;
-            const uint32_t bar = bar0 + 8 * (k & 1);
+            const uint32_t bar = bar0 + (BQ_K4_BUFS == 2 ? 8 * (k & 1) : 0);
             if (len && incl <= (uint32_t)kPoolWords && a.debug < 2) {
                 sg.staged = true;
                 sg.off = off + (uint32_t)((reinterpret_cast<uintptr_t>(sg.g) >> 3) & 1);
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pool + (size_t)(k & 1) * kPoolWords + off);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pool + (size_t)(k & (BQ_K4_BUFS - 1)) * kPoolWords + off);
                 const uint32_t bytes = len * 8;
                 asm volatile(
                     "{\n\t.reg .b64 st;\n\t"
@@ -333,8 +341,8 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
             }
         };
         auto wait_batch = [&](int k) {
-            const uint32_t bar = bar0 + 8 * (k & 1);
-            const uint32_t parity = (uint32_t)((k >> 1) & 1);
+            const uint32_t bar = bar0 + (BQ_K4_BUFS == 2 ? 8 * (k & 1) : 0);
+            const uint32_t parity = (uint32_t)((BQ_K4_BUFS == 2 ? k >> 1 : k) & 1);
             uint32_t done = 0;
             while (!done) {
                 asm volatile(
@@ -349,6 +357,26 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
         // two-batch unrolled pipeline: batch k + 2's metadata lands in q while batch k is
         // walked, and the segment plans alternate between sa / sb (no register rotation
         // that would wait on the metadata loads right after issuing them)
+#if BQ_K4_BUFS == 1
+        // single-buffered: batch k is copied and walked before batch k + 1 is planned;
+        // more CTAs per SM hide the copy latency instead of a second pool half
+        Seg sa;
+        Pre q;
+        fetch(my, q);
+        for (int k = 0; k < nk; ++k) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
+            plan(q, k, sa);
+            fetch((k + 1) * NT + my, q);
+            wait_batch(k);
+            if (sa.lim && !a.debug) {
+                if (sa.staged)
+                    sweep_stream<false>(pool + sa.off, sa.lim, sa.pos, ts, width, cnt, a.four);
+                else
+                    sweep_stream<true>(sa.g, sa.lim, sa.pos, ts, width, cnt, a.four);
+            }
+            __syncwarp();
+        }
+#else
         Seg sa, sb;
         Pre q;
         fetch(my, q);
@@ -372,6 +400,7 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
             step(k, sa, sb);
             if (k + 1 < nk) step(k + 1, sb, sa);
         }
+#endif
     }
     __syncthreads();
 
@@ -379,23 +408,89 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
     const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
     TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile,
                  a.breaks, a.nbreak};
-    uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kSlots>());
+    uint16_t *undecided = reinterpret_cast<uint16_t *>(region);
     unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
     __syncthreads();
 
-    // ---- C: read dirty literals only where the fills leave the outcome open ----
-    pc += tile_resolve<NT, kSlots>(d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &&add_bits) {
-        walk_tiles<BQ_K4_C_ILP>(a, tid, NT, tile, ts, te,
-                                [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit,
-                                    const uint64_t *s) {
-                                    const uint64_t lo = max(ds, ts), hi = min(de, te);
-                                    for (uint64_t p = lo; p < hi; ++p) {
-                                        const uint16_t u = slot_of[p - ts];
-                                        if (u != kNoSlot) add_bits(u, s + lit + (p - ds));
-                                    }
-                                });
-    });
+    // ---- C is deferred: hand the counts of a tile with undecided words to K4c --------
+    __shared__ uint32_t todo_slot;
+    if (n_undecided) {  // block-uniform
+        if (tid == 0) {
+            todo_slot = atomicAdd(a.todo_count, 1u);
+            a.todo[todo_slot] = tile;
+        }
+        __syncthreads();
+        uint4 *dst = reinterpret_cast<uint4 *>(a.todo_cnt + (size_t)todo_slot * kRleTile);
+        const uint4 *src = reinterpret_cast<const uint4 *>(cnt);
+        for (int k = tid; k < kRleTile / 4; k += NT) dst[k] = src[k];
+    }
 
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
+    if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
+}
+
+// K4c: phase C of the tiles K4 deferred (the same tile_resolve, one CTA of kResolveThreads
+// per tile, streams walked one per thread four at a time, and a larger literal-address
+// buffer than K4's pools leave room for).  A persistent grid takes the deferred tiles in
+// order; the decided words of these tiles were written by K4.
+#ifndef BQ_K4C_THREADS
+#define BQ_K4C_THREADS 512
+#endif
+#ifndef BQ_K4C_SLOTS
+#define BQ_K4C_SLOTS 1024
+#endif
+constexpr int kResolveThreads = BQ_K4C_THREADS;
+constexpr int kResolveSlots = BQ_K4C_SLOTS;
+#ifndef BQ_K4C_CAP
+#define BQ_K4C_CAP 6144
+#endif
+constexpr int kResolveCapC = BQ_K4C_CAP;  // literal words per batch (8 bytes each)
+constexpr size_t kResolveSmem = (size_t)(kRleTile + 4) * 4 + tile_resolve_bytes<kResolveSlots, kResolveCapC>() +
+                                (size_t)kRleTile * 2;
+
+__global__ void __launch_bounds__(kResolveThreads) rle_resolve_kernel(const __grid_constant__ RleCountArgs a) {
+    constexpr int NT = kResolveThreads;
+    extern __shared__ __align__(16) uint8_t rs_smem[];
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(rs_smem);
+    uint8_t *region = rs_smem + (size_t)(kRleTile + 4) * 4;
+    uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kResolveSlots, kResolveCapC>());
+    __shared__ uint32_t n_undecided;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t ntodo = *a.todo_count;
+    unsigned long long pc = 0;
+    for (uint32_t k = blockIdx.x; k < ntodo; k += gridDim.x) {
+        const uint32_t tile = a.todo[k];
+        const uint64_t ts = (uint64_t)(a.tile0 + tile) * kRleTile;
+        const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
+        const int width = (int)(te - ts);
+        if (tid == 0) n_undecided = 0;
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.todo_cnt + (size_t)k * kRleTile);
+        for (int j = tid; j < kRleTile / 4; j += NT) reinterpret_cast<uint4 *>(cnt)[j] = src[j];
+        __syncthreads();
+        // the undecided words, as phase B classified them
+        for (int j = tid; j < width; j += NT) {
+            const uint32_t c = cnt[j];
+            const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
+            if (ones + dirty > __ldg(a.const_until + ones)) undecided[atomicAdd(&n_undecided, 1u)] = (uint16_t)j;
+        }
+        __syncthreads();
+        TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out,
+                     (uint64_t)a.tile0 * kRleTile, a.breaks, a.nbreak};
+        pc += tile_resolve<NT, kResolveSlots, kResolveCapC>(
+            d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &&add_bits) {
+                walk_tiles<BQ_K4_C_ILP>(a, tid, NT, tile, ts, te,
+                                        [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit,
+                                            const uint64_t *s) {
+                                            const uint64_t lo = max(ds, ts), hi = min(de, te);
+                                            for (uint64_t p = lo; p < hi; ++p) {
+                                                const uint16_t u = slot_of[p - ts];
+                                                if (u != kNoSlot) add_bits(u, s + lit + (p - ds));
+                                            }
+                                        });
+            });
+        __syncthreads();
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
     if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
@@ -728,8 +823,33 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         if (rc == BQ_OK) note_use(q, s);
         return rc;
     } else {
-        e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) rle_count_kernel<<<q->ntiles, kStagedThreads, smem, s>>>(a);
+        // K4 (phases A, B), then K4c over the tiles it deferred (scratch in stream order)
+        const size_t b_todo = (((size_t)q->ntiles + 1) * 4 + 255) & ~(size_t)255;
+        void *scr = nullptr;
+        e = pool_alloc_on(&scr, b_todo + (size_t)q->ntiles * kRleTile * 4, s);
+        if (e == cudaSuccess) {
+            a.todo_count = static_cast<uint32_t *>(scr);
+            a.todo = a.todo_count + 1;
+            a.todo_cnt = reinterpret_cast<uint32_t *>(static_cast<char *>(scr) + b_todo);
+            e = cudaMemsetAsync(a.todo_count, 0, 4, s);
+        }
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) {
+            rle_count_kernel<<<q->ntiles, kStagedThreads, smem, s>>>(a);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(rle_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResolveSmem);
+        if (e == cudaSuccess) {
+            static int per_sm = 0;
+            if (!per_sm) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_resolve_kernel, kResolveThreads, kResolveSmem);
+                per_sm = std::max(per_sm, 1);
+            }
+            const unsigned grid = (unsigned)std::min<uint64_t>(q->ntiles, (uint64_t)sm_count() * per_sm);
+            rle_resolve_kernel<<<grid, kResolveThreads, kResolveSmem, s>>>(a);
+        }
+        if (scr) cudaFreeAsync(scr, s);
     }
     if (e != cudaSuccess) {
         release();

@@ -103,10 +103,9 @@ __device__ __forceinline__ unsigned long long tile_decide(const TileDecide &d, c
 // Phase C shared memory: slot_of[kRleTile] | slot_word[SLOTS] | soff[SLOTS + 1] |
 // sfill[SLOTS] | entries[kResolveCap] (addresses of literal words, grouped by slot).
 constexpr int kResolveCap = 3584;  // literal words per phase-C batch (28 KB)
-template <int SLOTS>
+template <int SLOTS, int CAP = kResolveCap>
 constexpr size_t tile_resolve_bytes() {
-    return (size_t)kRleTile * 2 + (size_t)SLOTS * 2 + (size_t)(SLOTS + 4) * 4 + (size_t)SLOTS * 4 +
-           (size_t)kResolveCap * 8;
+    return (size_t)kRleTile * 2 + (size_t)SLOTS * 2 + (size_t)(SLOTS + 4) * 4 + (size_t)SLOTS * 4 + (size_t)CAP * 8;
 }
 
 template <int M>
@@ -186,7 +185,7 @@ __device__ __forceinline__ uint64_t decide_word(const TileDecide &d, uint32_t on
 // atomics, no per-bit loop) and decides all 64 bits with bit-sliced comparisons
 // against the accept vector's breakpoints.  A word with more dirty inputs than the
 // buffer holds is resolved alone by atomic ripple-adds into shared planes.
-template <int NT, int SLOTS, class CountBits>
+template <int NT, int SLOTS, int CAP = kResolveCap, class CountBits>
 __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, const uint32_t *cnt,
                                                            const uint16_t *undecided, uint32_t nu, uint8_t *region,
                                                            CountBits &&count_bits) {
@@ -223,7 +222,7 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const uint32_t i = tid * kPer + q;
-            if (i < cand && off + dv[q] <= (uint32_t)kResolveCap) {
+            if (i < cand && off + dv[q] <= (uint32_t)CAP) {
                 kk = i + 1;
                 soff[i] = off;
                 sfill[i] = 0;
