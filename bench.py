@@ -847,7 +847,7 @@ def run_c4(args, torch, bq, lib, dev, stream, ctx):
                                              f"thread as the reference) on the first 2^{wr.bit_length() - 1} bits of all 1024 streams "
                                              f"({wbytes} compressed bytes, {cpu_s:.2f} s)"}},
                  traffic_key="c4_fresh")
-    line["gpu_launches"] = len(fresh_ms) * 3  # per fresh query: K3 directory kernel, K4, popcount reset
+    line["gpu_launches"] = len(fresh_ms) * 3  # per fresh query: K3 directory, K4 (phases A, B), K4c (phase C)
     line["_rank_bytes"] = comp_bytes * out_words / nw  # this rank's share of the query
     line["_scaling"] = "strong"
     q.close()

@@ -5,4 +5,4 @@ timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 for w in c4 c2; do
   timeout 900 python bench.py --workload $w > gpurun_out/bench_$w.log 2>&1; echo "bench $w rc=$?" >> gpurun_out/bench_$w.log
 done
-TAG=_r2c bash scripts/gpu_ncu_fresh.sh
+TAG=_r2e bash scripts/gpu_ncu_fresh.sh
