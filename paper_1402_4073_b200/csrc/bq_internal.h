@@ -209,7 +209,9 @@ int launch_sliced(const SlicedLayout &l, const SlicedEval &e, cudaStream_t strea
 // rle_directory_scratch_bytes(lens) bytes.  Synchronous.
 int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const std::vector<uint64_t> &lens,
                         uint64_t total_words, uint64_t tail_mask, uint32_t tile0, uint32_t nrows, uint2 *d_dir,
-                        void *d_scratch, int *err_code, uint64_t *err_stream);
+                        void *d_scratch, int *err_code, uint64_t *err_stream, const void *h_extra = nullptr,
+                        void *d_extra = nullptr, size_t extra_bytes = 0);
+// (h_extra: extra_bytes uploaded to d_extra through the same pinned staging, ordered before the kernel)
 // device scratch bytes build_rle_directory needs for these stream lengths
 size_t rle_directory_scratch_bytes(const std::vector<uint64_t> &lens);
 

@@ -611,21 +611,24 @@ BQ_API int bq_rle_query_create_range(const bq_rle_span *streams, int n, uint64_t
         ptab[i] = reinterpret_cast<uint64_t>(streams[i].words);
         ptab[(size_t)n + i] = lens[i];
     }
-    // ordered on the legacy stream before the directory kernel, which the build
-    // synchronises before returning: complete before any evaluation reads them
-    e = cudaMemcpyAsync(q->d_ptrs, ptab.data(), tab, cudaMemcpyHostToDevice, 0);
-    if (e == cudaSuccess && !total) e = cudaStreamSynchronize(0);
-    if (e != cudaSuccess) {
-        pool_free(q->mem);
-        delete q;
-        return cuda_error(e, "rle query setup");
+    // with a directory to build, the tables go up with its job table (one pinned staging,
+    // ordered on the legacy stream before the kernel; the build synchronises before
+    // returning, so they are complete before any evaluation reads them)
+    if (!total) {
+        e = cudaMemcpyAsync(q->d_ptrs, ptab.data(), tab, cudaMemcpyHostToDevice, 0);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+        if (e != cudaSuccess) {
+            pool_free(q->mem);
+            delete q;
+            return cuda_error(e, "rle query setup");
+        }
     }
     if (total) {  // the directory walk validates every stream whole, whatever the range
         int code = 0;
         uint64_t bad = 0;
         const uint64_t tail_mask = (r_bits % W) ? ((1ull << (r_bits % W)) - 1) : 0ull;
         rc = build_rle_directory(q->d_ptrs, q->d_lens, lens, total, tail_mask, tile0, ntiles + 1, q->d_dir,
-                                 m + scr_off, &code, &bad);
+                                 m + scr_off, &code, &bad, ptab.data(), q->d_ptrs, tab);
         if (rc || code) {
             pool_free(q->mem);
             delete q;

@@ -361,7 +361,8 @@ size_t rle_directory_scratch_bytes(const std::vector<uint64_t> &lens) {
 
 int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, const std::vector<uint64_t> &lens,
                         uint64_t total_words, uint64_t tail_mask, uint32_t tile0, uint32_t nrows, uint2 *d_dir,
-                        void *d_scratch, int *err_code, uint64_t *err_stream) {
+                        void *d_scratch, int *err_code, uint64_t *err_stream, const void *h_extra, void *d_extra,
+                        size_t extra_bytes) {
     const int n = (int)lens.size();
     *err_code = 0;
     std::vector<uint32_t> nblk(n);
@@ -382,7 +383,8 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
     const size_t a_link = ((size_t)maxb * n * 8 + 255) & ~(size_t)255;
     const size_t a_nblk = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t a_jobs = (rem * 8 + 255) & ~(size_t)255;
-    const size_t up_bytes = a_nblk + rem * 8;
+    const size_t a_up = (a_nblk + rem * 8 + 15) & ~(size_t)15;
+    const size_t up_bytes = a_up + extra_bytes;
     static std::mutex staging_mu;
     static char *staging = nullptr;
     static size_t staging_cap = 0;
@@ -414,7 +416,10 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
     unsigned int *d_ticket = reinterpret_cast<unsigned int *>(sc + a_link + a_nblk + a_jobs);
     unsigned long long *d_err = reinterpret_cast<unsigned long long *>(sc + a_link + a_nblk + a_jobs + 8);
     // nblk and the job table are adjacent in both buffers: one copy
-    cudaError_t e = cudaMemcpyAsync(d_nblk, staging, up_bytes, cudaMemcpyHostToDevice, 0);
+    if (extra_bytes) memcpy(staging + a_up, h_extra, extra_bytes);
+    cudaError_t e = cudaMemcpyAsync(d_nblk, staging, a_nblk + rem * 8, cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess && extra_bytes)
+        e = cudaMemcpyAsync(d_extra, staging + a_up, extra_bytes, cudaMemcpyHostToDevice, 0);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, (size_t)maxb * n * 8, 0);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_ticket, 0, 8, 0);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0xFF, 8, 0);
