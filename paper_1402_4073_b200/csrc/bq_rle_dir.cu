@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
                          : "memory");
     }
 
-    // speculative entry: the landing most of the kHalo hypotheses agree on (smallest on a tie)
+    // speculative entry: the landing most of the kHalo hypotheses reach (smallest on a tie)
     uint32_t entry = q;
     // the halo words [q - kHalo, q): the end of the left neighbour's slot (its sbase by shuffle;
     // it is active whenever this lane is), lane 0 reads the previous block's last words
@@ -185,30 +185,32 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const uint32_t slot_left = __shfl_up_sync(0xffffffffu, slot_s, 1);
     const uint32_t halo_s = lane ? slot_left + (uint32_t)((int64_t)q - kHalo - sbase_left) * 8u : 0u;
     if (active && q > 0) {
-        // landings saturate at 2^32 - 1 (beyond any stream): never a valid entry
-        uint32_t land[kHalo];
+        // landings saturate at 2^32 - 1 (beyond any stream): never a valid entry.  A
+        // hypothesis whose next marker is a later halo word shares that word's root (the
+        // halo word whose chain leaves the halo); each root gets the votes of the
+        // hypotheses on it, kept as 4-bit counters in one word (no per-pair comparisons)
+        static_assert(kHalo <= 8, "4-bit root indices and vote counters");
+        uint32_t nxs[kHalo];
+        uint32_t rootp = 0, votes = 0;
 #pragma unroll
         for (int j = kHalo - 1; j >= 0; --j) {
             const uint32_t h = q - kHalo + j;
             const uint64_t hw = lane ? lds64(halo_s + (uint32_t)j * 8u) : __ldg(s + h);
             const uint64_t nx64 = (uint64_t)h + 1 + (hw >> 33);
             const uint32_t nx = nx64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)nx64;
-            uint32_t v = nx;
-#pragma unroll
-            for (int k = j + 1; k < kHalo; ++k)
-                if (nx == q - kHalo + k) v = land[k];
-            land[j] = v;
+            nxs[j] = nx;
+            // nx > h, so a landing inside the halo is a later halo word k > j
+            const uint32_t r = nx < q ? (rootp >> (4u * (nx - (q - kHalo)))) & 15u : (uint32_t)j;
+            rootp |= r << (4 * j);
+            votes += 1u << (4u * r);
         }
-        int best = 0;
-        uint32_t pick = 0xFFFFFFFFu;
+        uint32_t best = 0, pick = 0xFFFFFFFFu;
 #pragma unroll
-        for (int j = 0; j < kHalo; ++j) {
-            int c = 0;
-#pragma unroll
-            for (int k = 0; k < kHalo; ++k) c += land[k] == land[j];
-            if (c > best || (c == best && land[j] < pick)) {
+        for (int r = 0; r < kHalo; ++r) {
+            const uint32_t c = (votes >> (4 * r)) & 15u;
+            if (c > best || (c == best && c && nxs[r] < pick)) {
                 best = c;
-                pick = land[j];
+                pick = nxs[r];
             }
         }
         entry = min(pick, L + 1);
