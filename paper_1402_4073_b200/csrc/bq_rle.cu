@@ -93,6 +93,7 @@ struct RleCountArgs {
     uint32_t *todo_count;
     uint32_t *todo;
     uint32_t *todo_cnt;
+    uint32_t tile_off;  // K4 launches cover directory rows [tile_off, tile_off + gridDim.x)
 };
 
 
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
     __shared__ uint32_t n_undecided;
     __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
 
-    const uint32_t tile = blockIdx.x;  // directory row; the tile's words are global
+    const uint32_t tile = blockIdx.x + a.tile_off;  // directory row; the tile's words are global
     const uint64_t ts = (uint64_t)(a.tile0 + tile) * kRleTile;
     const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
     const int width = (int)(te - ts);
@@ -826,31 +827,40 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         if (rc == BQ_OK) note_use(q, s);
         return rc;
     } else {
-        // K4 (phases A, B), then K4c over the tiles it deferred (scratch in stream order)
-        const size_t b_todo = (((size_t)q->ntiles + 1) * 4 + 255) & ~(size_t)255;
+        // K4 (phases A, B), then K4c over the tiles it deferred (scratch in stream order), in
+        // chunks of at most kChunk tiles so the deferred counts need at most 256 MB
+        const char *chenv = getenv("BQ_K4_CHUNK");  // tests: small chunks
+        const uint32_t kChunk = chenv && atoi(chenv) > 0 ? (uint32_t)atoi(chenv) : 65536u;
+        const uint32_t chunk = std::min<uint32_t>(q->ntiles, kChunk);
+        const size_t b_todo = (((size_t)chunk + 1) * 4 + 255) & ~(size_t)255;
         void *scr = nullptr;
-        e = pool_alloc_on(&scr, b_todo + (size_t)q->ntiles * kRleTile * 4, s);
+        e = pool_alloc_on(&scr, b_todo + (size_t)chunk * kRleTile * 4, s);
         if (e == cudaSuccess) {
             a.todo_count = static_cast<uint32_t *>(scr);
             a.todo = a.todo_count + 1;
             a.todo_cnt = reinterpret_cast<uint32_t *>(static_cast<char *>(scr) + b_todo);
-            e = cudaMemsetAsync(a.todo_count, 0, 4, s);
-        }
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) {
-            rle_count_kernel<<<q->ntiles, kStagedThreads, smem, s>>>(a);
-            e = cudaGetLastError();
+            e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         }
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(rle_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResolveSmem);
-        if (e == cudaSuccess) {
-            static int per_sm = 0;
-            if (!per_sm) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_resolve_kernel, kResolveThreads, kResolveSmem);
-                per_sm = std::max(per_sm, 1);
+        static int per_sm = 0;
+        if (e == cudaSuccess && !per_sm) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_resolve_kernel, kResolveThreads, kResolveSmem);
+            per_sm = std::max(per_sm, 1);
+        }
+        for (uint32_t t0 = 0; e == cudaSuccess && t0 < q->ntiles; t0 += chunk) {
+            const uint32_t nt = std::min<uint32_t>(chunk, q->ntiles - t0);
+            a.tile_off = t0;
+            e = cudaMemsetAsync(a.todo_count, 0, 4, s);
+            if (e == cudaSuccess) {
+                rle_count_kernel<<<nt, kStagedThreads, smem, s>>>(a);
+                e = cudaGetLastError();
             }
-            const unsigned grid = (unsigned)std::min<uint64_t>(q->ntiles, (uint64_t)sm_count() * per_sm);
-            rle_resolve_kernel<<<grid, kResolveThreads, kResolveSmem, s>>>(a);
+            if (e == cudaSuccess) {
+                const unsigned grid = (unsigned)std::min<uint64_t>(nt, (uint64_t)sm_count() * per_sm);
+                rle_resolve_kernel<<<grid, kResolveThreads, kResolveSmem, s>>>(a);
+                e = cudaGetLastError();
+            }
         }
         if (scr) cudaFreeAsync(scr, s);
     }

@@ -514,3 +514,27 @@ def test_release_cached_memory_between_queries(bq):
             assert np.array_equal(host(out, nw), exp), t
         q.close()
         bq.release_cached_memory()
+
+
+@pytest.mark.parametrize("chunk", ["1", "3", "4"])
+def test_first_evaluation_in_chunks(bq, chunk, monkeypatch):
+    """K4 + K4c launched over chunks of tiles (BQ_K4_CHUNK; by default 65536 tiles bound
+    the deferred-count scratch): every chunk's deferred tiles are resolved, on the whole
+    range and on a word-range query, at thresholds where most tiles reach phase C."""
+    monkeypatch.setenv("BQ_K4_CHUNK", chunk)
+    lib = bq._lib.load()
+    n, r = 40, 64 * 9000 - 5
+    nw = (r + 63) // 64
+    streams = [markov(lib, 29, i, r, 48.0, 400.0) for i in range(n)]
+    d = dev(streams)
+    for t in (2, 5, 11):
+        exp = O.cdom_threshold(streams, r, t)
+        q = bq.RleQuery(d, r)
+        out, pc = q.threshold(t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+        q.close()
+        q = bq.RleQuery(d, r, word_range=(2048, 7168))
+        out, pc = q.threshold(t)
+        assert np.array_equal(host(out, 5120), exp[2048:7168]), t
+        q.close()
