@@ -438,6 +438,9 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
 #ifndef BQ_K4C_THREADS
 #define BQ_K4C_THREADS 512
 #endif
+#ifndef BQ_K4C_MINB
+#define BQ_K4C_MINB 2
+#endif
 #ifndef BQ_K4C_SLOTS
 #define BQ_K4C_SLOTS 1024
 #endif
@@ -450,7 +453,7 @@ constexpr int kResolveCapC = BQ_K4C_CAP;  // literal words per batch (8 bytes ea
 constexpr size_t kResolveSmem = (size_t)(kRleTile + 4) * 4 + tile_resolve_bytes<kResolveSlots, kResolveCapC>() +
                                 (size_t)kRleTile * 2;
 
-__global__ void __launch_bounds__(kResolveThreads) rle_resolve_kernel(const __grid_constant__ RleCountArgs a) {
+__global__ void __launch_bounds__(kResolveThreads, BQ_K4C_MINB) rle_resolve_kernel(const __grid_constant__ RleCountArgs a) {
     constexpr int NT = kResolveThreads;
     extern __shared__ __align__(16) uint8_t rs_smem[];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(rs_smem);

@@ -273,6 +273,42 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
         };
         count_bits(static_cast<const uint16_t *>(slot_of), add_entry);
         __syncthreads();
+        if (nb <= (uint32_t)(NT / 32)) {
+            // few undecided words (a high threshold's typical tile): a warp per word, the
+            // lanes loading its literal words 32 at a time and counting each bit position
+            // with a ballot, so the loads are not serialised in one thread
+            if ((uint32_t)warp < nb) {
+                const uint32_t u = (uint32_t)warp;
+                const uint16_t wk = slot_word[u];
+                const uint32_t ones = cnt[wk] & 0xFFFFu, dirty = cnt[wk] >> 16;
+                const uint64_t *lits = entries + soff[u];
+                uint32_t c_lo = 0, c_hi = 0;  // counts of bit `lane` and bit `lane + 32`
+                for (uint32_t b0 = 0; b0 < dirty; b0 += 32) {
+                    const uint64_t x = b0 + lane < dirty ? __ldg(reinterpret_cast<const uint64_t *>(lits[b0 + lane])) : 0ull;
+#pragma unroll
+                    for (int bit = 0; bit < 32; ++bit) {
+                        const uint32_t m_lo = __ballot_sync(0xffffffffu, (x >> bit) & 1u);
+                        const uint32_t m_hi = __ballot_sync(0xffffffffu, (x >> (bit + 32)) & 1u);
+                        if (lane == bit) {
+                            c_lo += __popc(m_lo);
+                            c_hi += __popc(m_hi);
+                        }
+                    }
+                }
+                const uint32_t lo = __ballot_sync(0xffffffffu, accept_at(d.accept_bits, ones + c_lo));
+                const uint32_t hi = __ballot_sync(0xffffffffu, accept_at(d.accept_bits, ones + c_hi));
+                if (lane == 0) {
+                    uint64_t w = ((uint64_t)hi << 32) | lo;
+                    if (d.ts + wk == d.total_words - 1) w &= d.last_mask;
+                    d.out[d.ts - d.out_first + wk] = w;
+                    pc += __popcll(w);
+                    slot_of[wk] = kNoSlot;
+                }
+            }
+            __syncthreads();
+            base += nb;
+            continue;
+        }
         for (uint32_t u = tid; u < nb; u += NT) {
             const uint16_t wk = slot_word[u];
             const uint32_t ones = cnt[wk] & 0xFFFFu, dirty = cnt[wk] >> 16;
