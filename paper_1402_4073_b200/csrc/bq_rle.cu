@@ -11,20 +11,20 @@
 //   per-segment walks and a decoupled look-back across blocks (bq_rle_dir.cu),
 //   which also validates the streams as RleBitmap.iter_word_segments (:210-217).
 //
-// K4 rle_count_kernel -- one CTA per tile of kTileWords output words, the
-//   per-tile form of cdom's run sweep (runmerge.py:198-299):
-//   A. each thread walks whole streams from their directory entry, reading
-//      only marker words; one-fill and dirty runs become +1/-1 entries of a
-//      packed shared-memory difference array (ones in bits 0-15, dirty in
-//      16-31), so a prefix scan yields k_w (one-fills) and d_w (dirty inputs)
-//      for every word w;
+// K4 rle_count_kernel -- a query's first evaluation: the per-tile form of cdom's run
+//   sweep (runmerge.py:198-299) over tiles of kRleTile output words, kWT tiles per CTA:
+//   A. each lane walks one (stream, tile) slice from its directory entry, reading
+//      only marker words (staged by TMA, one bulk copy per stream and kWT tiles);
+//      one-fill and dirty runs become +1/-1 entries of the tile's packed
+//      shared-memory difference array (ones in bits 0-15, dirty in 16-31), so a
+//      prefix scan yields k_w (one-fills) and d_w (dirty inputs) for every word w;
 //   B. w is decided from (k_w, d_w) alone when accept[] is constant on
 //      [k_w, k_w + d_w] (cdom's three cases) -- the common
 //      case -- and written directly;
-//   C. only for undecided words are the dirty literals read: a second walk
-//      adds their bits into per-word shared-memory bit counters, then
-//      accept[k_w + count_b] decides each bit (dirty_segment_solver's "scan"
-//      branch, runmerge.py:99-125).
+//   C. only for undecided words are the dirty literals read (K4c rle_resolve_kernel,
+//      over the tiles K4 lists): a second walk files their addresses, bit-sliced
+//      sums count each bit position, then accept[k_w + count_b] decides each bit
+//      (dirty_segment_solver's "scan" branch, runmerge.py:99-125).
 //   Output is uncompressed (BASELINE config 4), with a fused popcount.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -41,34 +41,9 @@
 
 namespace bq {
 
-constexpr int kSlotsPerBatch = 512;   // undecided words resolved per phase-C pass
-constexpr int kStagedThreads = 128;     // staged K4: 4 warps, each with a private pool
-#ifndef BQ_K4_POOL
-#define BQ_K4_POOL 768
-#endif
-#ifndef BQ_K4_BUFS
-#define BQ_K4_BUFS 1  // staging pool halves per warp (2: double-buffered, 4 CTAs/SM; 1: 7 CTAs/SM)
-#endif
 #ifndef BQ_K4_C_ILP
 #define BQ_K4_C_ILP 4  // streams walked at once per thread in phase C
 #endif
-#ifndef BQ_K4_MINB
-#define BQ_K4_MINB 7
-#endif
-#ifndef BQ_K4_ZERO_ADDS
-#define BQ_K4_ZERO_ADDS 1
-#endif
-constexpr int kPoolWords = BQ_K4_POOL;  // words per warp pool half (two halves: double buffer);
-                                        // C4 needs ~613 words per 32 streams on average, 760 at p99
-constexpr size_t kCntBytes = (size_t)(kRleTile + 36) * 4 + 16 * 16;  // + sentinel, 32 per-lane dummies, mbarriers
-
-constexpr size_t kPoolBytes = (size_t)(kStagedThreads / 32) * BQ_K4_BUFS * kPoolWords * 8;
-// phase A's pools; phase B lists the undecided words over them once phase A is done
-constexpr size_t kRegionBytes = kPoolBytes > (size_t)kRleTile * 2 ? kPoolBytes : (size_t)kRleTile * 2;
-
-inline size_t rle_smem_bytes() {
-    return kCntBytes + kRegionBytes;
-}
 
 enum { RLE_ERR_TRUNCATED = 1, RLE_ERR_OVERLONG = 2, RLE_ERR_BEYOND_R = 3 };  // build_rle_directory's codes
 
@@ -93,7 +68,8 @@ struct RleCountArgs {
     uint32_t *todo_count;
     uint32_t *todo;
     uint32_t *todo_cnt;
-    uint32_t tile_off;  // K4 launches cover directory rows [tile_off, tile_off + gridDim.x)
+    uint32_t tile_off;  // K4 launches cover directory rows [tile_off, tile_off + tile_cnt)
+    uint32_t tile_cnt;
 };
 
 
@@ -177,11 +153,11 @@ __device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int
 // fill ends and the literals begin, -dirty where the literals end.
 template <bool GLOBAL>
 __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, uint32_t pos, uint64_t ts, int W,
-                                             uint32_t *cnt, uint32_t four) {
+                                             uint32_t *cnt, uint32_t four, uint32_t dummy) {
+    // dummy: this lane's slot (> W) for the first marker's empty contributions
     auto load = [src](uint32_t k) { return GLOBAL ? __ldg(src + k) : src[k]; };
     if (lim == 0) return;
     const uint32_t Wu = (uint32_t)W;
-    const uint32_t dummy = Wu + 1 + (threadIdx.x & 31);  // this lane's slot for empty contributions
     // first marker: its fill starts at or before the tile (64-bit positions)
     uint64_t mk = load(0);
     uint32_t dirty = (uint32_t)(mk >> 33);
@@ -220,14 +196,9 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
         const uint32_t at_rel = carry + ones;
         const uint32_t at_fe = litv - ones;
         // byte offsets as index * four (runtime 4): IMAD on the FMA pipe instead of an ALU LEA
-#if BQ_K4_ZERO_ADDS
         // an empty update adds 0 to its real slot (rare on C4: markers are literal groups)
         atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + rel * four), at_rel);
         atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + fe * four), at_fe);
-#else
-        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_rel ? rel : dummy) * four), at_rel);
-        atomicAdd(reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(cnt) + (at_fe ? fe : dummy) * four), at_fe);
-#endif
         carry = 0u - litv;
         if (de_raw >= Wu) return;  // the pending literal end lies past the tile
         rel = de_raw;
@@ -237,96 +208,122 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
 }
 
 
-// Phase A: warp-private, double-buffered staging.  Lane l of warp w owns stream
-// k*NT + 32w + l of batch k.  It computes its stream's segment for this tile
-// (directory entry -> marker covering the next tile boundary, widened to 16-byte
-// alignment), claims room in the warp's pool with a warp prefix sum, and copies
-// the segment with one TMA bulk copy while the previous batch is being walked;
-// one mbarrier per pool half, so the warps never meet at a CTA barrier in phase
-// A.  A segment that does not fit the pool is walked straight from HBM.
-__global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
-    constexpr int NT = kStagedThreads;
-    constexpr int kSlots = kSlotsPerBatch;
+// K4: phases A and B.  A warp's lanes are spread over kWT consecutive tiles of kWS = 32 / kWT
+// streams (until the end of round 2: one tile of 32 streams, one bulk copy per lane).  The
+// segments a stream contributes to consecutive tiles are contiguous in the stream, so one
+// TMA bulk copy stages the segments of kWT lanes (kWS copies per warp and batch instead of
+// 32: the copies' operands must be warp-uniform, and ptxas issues per-lane copies in a
+// ten-instruction ELECT / R2UR / UBLKCP loop that was a third of the kernel's instructions),
+// and the copies carry no per-segment alignment padding.  Each lane walks one (stream, tile)
+// slice from the warp's private pool with two shared-memory reductions per marker, into its
+// tile's difference array; the CTA holds kWT arrays and then runs phase B tile by tile.  A
+// batch whose segments overflow the pool walks the rest from HBM.  C4, kernel time: one tile
+// per CTA 0.647 ms; kWT = 8 (2 or 3 CTAs/SM) 0.67; kWT = 4, 256 threads, 3 CTAs/SM 0.570;
+// kWT = 2 at 4 x 256 or 7 x 128 threads per SM the same; 608-word pools (overflows) 0.68.
+#ifndef BQ_K4W_TN
+#define BQ_K4W_TN 4
+#endif
+#ifndef BQ_K4W_NT
+#define BQ_K4W_NT 256
+#endif
+#ifndef BQ_K4W_POOL
+#define BQ_K4W_POOL 704
+#endif
+#ifndef BQ_K4W_MINB
+#define BQ_K4W_MINB 3
+#endif
+constexpr int kWT = BQ_K4W_TN;              // tiles per CTA (a power of two <= 32)
+constexpr int kWS = 32 / kWT;               // streams per warp and batch
+constexpr int kWThreads = BQ_K4W_NT;
+constexpr int kWPool = BQ_K4W_POOL;         // staging words per warp (single-buffered)
+constexpr int kWStride = kRleTile + 12 + (kWS > 8 ? 8 : 0);  // words per tile array: [0, W) counts, W sentinel, W + 1 + j dummies
+static_assert((kWT & (kWT - 1)) == 0 && kWT <= 32 && kWS <= 16, "lanes = kWS streams x kWT tiles");
+constexpr size_t kWCntBytes = (size_t)kWT * kWStride * 4;
+constexpr size_t kWBarBytes = (size_t)(kWThreads / 32) * 8;
+constexpr size_t kWPoolBytes = (size_t)(kWThreads / 32) * kWPool * 8;
+constexpr size_t kWideSmem = kWCntBytes + kWBarBytes + (kWPoolBytes > (size_t)kRleTile * 2 ? kWPoolBytes : (size_t)kRleTile * 2);
+
+__global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
+    constexpr int NT = kWThreads, NW = NT / 32;
     extern __shared__ __align__(16) uint8_t rle_smem[];
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(rle_smem);  // [kRleTile + 4] packed (ones | dirty << 16)
-    uint8_t *region = rle_smem + kCntBytes;                  // phase A: warp pools; phases B/C: tile_resolve
-    __shared__ uint32_t n_undecided;
-    __shared__ uint32_t warp_sums[NT / 32], warp_reach[NT / 32];
+    uint32_t *cnt_all = reinterpret_cast<uint32_t *>(rle_smem);  // kWT packed difference arrays
+    uint64_t *bars = reinterpret_cast<uint64_t *>(rle_smem + kWCntBytes);
+    uint8_t *region = rle_smem + kWCntBytes + kWBarBytes;  // phase A: warp pools; phase B: undecided list
+    __shared__ uint32_t n_undecided, todo_slot;
+    __shared__ uint32_t warp_sums[NW], warp_reach[NW];
 
-    const uint32_t tile = blockIdx.x + a.tile_off;  // directory row; the tile's words are global
-    const uint64_t ts = (uint64_t)(a.tile0 + tile) * kRleTile;
-    const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
-    const int width = (int)(te - ts);
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int li = lane % kWT, lj = lane / kWT;  // this lane's tile within the CTA, stream within the batch
     const int n = a.n;
+    const uint32_t first = blockIdx.x * (uint32_t)kWT;              // within the launch
+    const uint32_t ntl = min((uint32_t)kWT, a.tile_cnt - first);    // tiles this CTA covers
+    const uint32_t tile = a.tile_off + first + (uint32_t)li;        // directory row
+    const bool tvalid = (uint32_t)li < ntl;
+    const uint64_t ts = (uint64_t)(a.tile0 + tile) * kRleTile;
+    const int width = tvalid ? (int)(min(ts + (uint64_t)kRleTile, a.total_words) - ts) : 0;
 
-    for (int k = tid; k <= kRleTile; k += NT) cnt[k] = 0u;
-    if (tid == 0) n_undecided = 0;
+    for (int k = tid; k < kWT * kWStride; k += NT) cnt_all[k] = 0u;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + warp);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
 
-    // ---- A: run sweep over markers only -> difference array ------------------
+    // ---- A: run sweep over markers only -> the tiles' difference arrays ---------------
     {
-        // directory metadata of a lane's stream in batch k (tile-major rows: coalesced),
-        // fetched one batch ahead of use so its latency hides behind a walk
+        uint32_t *cnt = cnt_all + (size_t)li * kWStride;
+        uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * kWPool;
+        const uint32_t pool_s = (uint32_t)__cvta_generic_to_shared(pool);
         struct Pre {
             uint2 e;
             uint32_t nx;
             uint64_t L;
             const uint64_t *p;
         };
-        auto fetch = [&](int st, Pre &q) {
+        const int nbatch = (n + kWS - 1) / kWS;
+        auto fetch = [&](int b, Pre &q) {
             q.e = make_uint2(0u, 0u);
+            q.nx = 0;
             q.L = 0;
-            if (st < n) {
+            q.p = nullptr;
+            const int st = b * kWS + lj;
+            if (b < nbatch && st < n && tvalid) {
                 q.L = a.lens[st];
-                q.e = a.dir[(size_t)tile * a.n + st];
-                q.nx = a.dir[(size_t)(tile + 1) * a.n + st].x;
+                q.e = a.dir[(size_t)tile * n + st];
+                q.nx = a.dir[(size_t)(tile + 1) * n + st].x;
                 q.p = a.ptrs[st];
             }
         };
-        uint64_t *pool = reinterpret_cast<uint64_t *>(region) + (size_t)warp * BQ_K4_BUFS * kPoolWords;
-        // one mbarrier per pool half; 32 arrivals (one per lane) + the TMA byte count complete a phase
-        uint64_t *bars = reinterpret_cast<uint64_t *>(cnt + kRleTile + 36) + warp * 2;
-        const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
-        if (lane == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar0) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar0 + 8) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        }
-        __syncwarp();
-        struct Seg {
-            const uint64_t *g;  // global address of the directory marker
-            uint32_t lim, pos, off;
-            bool staged;
-        };
-        // Stage batch k's segment of this lane's stream: one TMA bulk copy per lane.
-        auto plan = [&](const Pre &q, int k, Seg &sg) {
-            sg.lim = 0;
-            sg.staged = false;
+        Pre q;
+        fetch(warp, q);
+        uint32_t parity = 0;
+        for (int b = warp; b < nbatch; b += NW) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of the last batch before TMA writes
+            // this lane's slice: stream words [lo, hi) = directory marker .. the marker covering the tile's end
+            const bool have = q.e.x < q.L;
+            const uint32_t lo = have ? q.e.x : 0xFFFFFFFFu;
+            uint32_t hi = have ? (uint32_t)min((uint64_t)(q.nx == 0xFFFFFFFFu ? q.L : q.nx) + 1, q.L) : 0u;
+            // the batch's stream: [glo, ghi) covers its kWT slices (rows are monotone in the tile)
+            const uint32_t glo = __shfl_sync(0xffffffffu, lo, lj * kWT);
+#pragma unroll
+            for (int o = 1; o < kWT; o <<= 1) hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            const uint64_t *gp = reinterpret_cast<const uint64_t *>(__shfl_sync(0xffffffffu, (unsigned long long)q.p, lj * kWT));
             uint32_t len = 0;
             uintptr_t b0 = 0;
-            if (q.e.x < q.L) {
-                const uint64_t next = q.nx == 0xFFFFFFFFu ? q.L : q.nx;
-                sg.g = q.p + q.e.x;
-                sg.lim = (uint32_t)(q.L - q.e.x);
-                sg.pos = q.e.y;
-                b0 = reinterpret_cast<uintptr_t>(sg.g) & ~(uintptr_t)15;
-                const uintptr_t b1 = (reinterpret_cast<uintptr_t>(q.p + min(next + 1, q.L)) + 15) & ~(uintptr_t)15;
+            if (glo < hi) {
+                b0 = reinterpret_cast<uintptr_t>(gp + glo) & ~(uintptr_t)15;
+                const uintptr_t b1 = (reinterpret_cast<uintptr_t>(gp + hi) + 15) & ~(uintptr_t)15;
                 len = (uint32_t)((b1 - b0) / 8);
             }
-            uint32_t incl = len;
+            uint32_t off = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+            for (int j = 0; j < kWS; ++j) {
+                const uint32_t v = __shfl_sync(0xffffffffu, len, j * kWT);
+                if (j < lj) off += v;
             }
-            const uint32_t off = incl - len;
-            const uint32_t bar = bar0 + (BQ_K4_BUFS == 2 ? 8 * (k & 1) : 0);
-            if (len && incl <= (uint32_t)kPoolWords && a.debug < 2) {
-                sg.staged = true;
-                sg.off = off + (uint32_t)((reinterpret_cast<uintptr_t>(sg.g) >> 3) & 1);
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pool + (size_t)(k & (BQ_K4_BUFS - 1)) * kPoolWords + off);
+            const bool staged = len && off + len <= (uint32_t)kWPool && a.debug < 2;
+            if (li == 0 && staged) {
                 const uint32_t bytes = len * 8;
                 asm volatile(
                     "{\n\t.reg .b64 st;\n\t"
@@ -334,98 +331,65 @@ __global__ void __launch_bounds__(kStagedThreads, BQ_K4_MINB) rle_count_kernel(c
                     "r"(bytes)
                     : "memory");
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        pool_s + off * 8u),
                     "l"(b0), "r"(bytes), "r"(bar)
                     : "memory");
             } else {
                 asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
             }
-        };
-        auto wait_batch = [&](int k) {
-            const uint32_t bar = bar0 + (BQ_K4_BUFS == 2 ? 8 * (k & 1) : 0);
-            const uint32_t parity = (uint32_t)((BQ_K4_BUFS == 2 ? k >> 1 : k) & 1);
-            uint32_t done = 0;
-            while (!done) {
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-                    : "=r"(done)
-                    : "r"(bar), "r"(parity)
-                    : "memory");
+            const uint64_t *g = q.p + q.e.x;
+            const uint32_t lim = have ? (uint32_t)(q.L - q.e.x) : 0u;
+            const uint32_t pos = q.e.y;
+            const uint32_t soff = off + (uint32_t)((reinterpret_cast<uintptr_t>(g) - b0) / 8);
+            fetch(b + NW, q);
+            {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                        : "=r"(done)
+                        : "r"(bar), "r"(parity)
+                        : "memory");
+                parity ^= 1u;
             }
-        };
-        const int nk = (n + NT - 1) / NT;
-        const int my = warp * 32 + lane;
-        // two-batch unrolled pipeline: batch k + 2's metadata lands in q while batch k is
-        // walked, and the segment plans alternate between sa / sb (no register rotation
-        // that would wait on the metadata loads right after issuing them)
-#if BQ_K4_BUFS == 1
-        // single-buffered: batch k is copied and walked before batch k + 1 is planned;
-        // more CTAs per SM hide the copy latency instead of a second pool half
-        Seg sa;
-        Pre q;
-        fetch(my, q);
-        for (int k = 0; k < nk; ++k) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
-            plan(q, k, sa);
-            fetch((k + 1) * NT + my, q);
-            wait_batch(k);
-            if (sa.lim && !a.debug) {
-                if (sa.staged)
-                    sweep_stream<false>(pool + sa.off, sa.lim, sa.pos, ts, width, cnt, a.four);
+            if (lim && !a.debug) {
+                if (staged)
+                    sweep_stream<false>(pool + soff, lim, pos, ts, width, cnt, a.four, (uint32_t)width + 1 + lj);
                 else
-                    sweep_stream<true>(sa.g, sa.lim, sa.pos, ts, width, cnt, a.four);
+                    sweep_stream<true>(g, lim, pos, ts, width, cnt, a.four, (uint32_t)width + 1 + lj);
             }
             __syncwarp();
         }
-#else
-        Seg sa, sb;
-        Pre q;
-        fetch(my, q);
-        plan(q, 0, sa);
-        fetch(NT + my, q);
-        auto step = [&](int k, Seg &cur, Seg &nxt) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of k-1 before TMA writes
-            plan(q, k + 1, nxt);  // k + 1 == nk: nothing to copy, arrive only
-            fetch((k + 2) * NT + my, q);
-            wait_batch(k);  // every lane's bulk copy for batch k has landed
-            if (cur.lim && !a.debug) {
-                if (cur.staged)
-                    sweep_stream<false>(pool + (size_t)(k & 1) * kPoolWords + cur.off, cur.lim, cur.pos, ts, width, cnt,
-                                        a.four);
-                else
-                    sweep_stream<true>(cur.g, cur.lim, cur.pos, ts, width, cnt, a.four);
-            }
-            __syncwarp();  // batch k's pool half may be refilled for batch k + 2
-        };
-        for (int k = 0; k < nk; k += 2) {
-            step(k, sa, sb);
-            if (k + 1 < nk) step(k + 1, sb, sa);
-        }
-#endif
     }
     __syncthreads();
 
-    // ---- B: prefix sum, then decide every word the fills decide ------------------
-    const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
-    TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile,
-                 a.breaks, a.nbreak};
+    // ---- B, tile by tile: prefix sum, decide every word the fills decide; C is deferred to K4c ----
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region);
-    unsigned long long pc = tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
-    __syncthreads();
-
-    // ---- C is deferred: hand the counts of a tile with undecided words to K4c --------
-    __shared__ uint32_t todo_slot;
-    if (n_undecided) {  // block-uniform
-        if (tid == 0) {
-            todo_slot = atomicAdd(a.todo_count, 1u);
-            a.todo[todo_slot] = tile;
+    unsigned long long pc = 0;
+    for (uint32_t i = 0; i < ntl; ++i) {
+        uint32_t *cnt = cnt_all + (size_t)i * kWStride;
+        const uint32_t trow = a.tile_off + first + i;
+        const uint64_t tsi = (uint64_t)(a.tile0 + trow) * kRleTile;
+        const int wi = (int)(min(tsi + (uint64_t)kRleTile, a.total_words) - tsi);
+        if (tid == 0) n_undecided = 0;
+        const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
+        TileDecide d{tsi, wi, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile,
+                     a.breaks, a.nbreak};
+        pc += tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
+        __syncthreads();
+        if (n_undecided) {  // block-uniform
+            if (tid == 0) {
+                todo_slot = atomicAdd(a.todo_count, 1u);
+                a.todo[todo_slot] = trow;
+            }
+            __syncthreads();
+            uint4 *dst = reinterpret_cast<uint4 *>(a.todo_cnt + (size_t)todo_slot * kRleTile);
+            const uint4 *src = reinterpret_cast<const uint4 *>(cnt);
+            for (int k = tid; k < kRleTile / 4; k += NT) dst[k] = src[k];
         }
         __syncthreads();
-        uint4 *dst = reinterpret_cast<uint4 *>(a.todo_cnt + (size_t)todo_slot * kRleTile);
-        const uint4 *src = reinterpret_cast<const uint4 *>(cnt);
-        for (int k = tid; k < kRleTile / 4; k += NT) dst[k] = src[k];
     }
-
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
     if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
@@ -782,7 +746,6 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
     a.out = d_out;
     a.popcnt = d_popcnt;
     a.four = 4;
-    const size_t smem = rle_smem_bytes();
     static const char *dbg = getenv("BQ_RLE_DEBUG");
     a.debug = dbg ? atoi(dbg) : 0;
     // Tile-sliced layout policy (BQ_RLE_SLICED): "0" never; "1" build at the first
@@ -842,7 +805,7 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
             a.todo_count = static_cast<uint32_t *>(scr);
             a.todo = a.todo_count + 1;
             a.todo_cnt = reinterpret_cast<uint32_t *>(static_cast<char *>(scr) + b_todo);
-            e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            e = cudaFuncSetAttribute(rle_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideSmem);
         }
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(rle_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResolveSmem);
@@ -854,9 +817,10 @@ static int rle_eval(bq_rle_query *q, const std::vector<uint8_t> &acc, uint64_t *
         for (uint32_t t0 = 0; e == cudaSuccess && t0 < q->ntiles; t0 += chunk) {
             const uint32_t nt = std::min<uint32_t>(chunk, q->ntiles - t0);
             a.tile_off = t0;
+            a.tile_cnt = nt;
             e = cudaMemsetAsync(a.todo_count, 0, 4, s);
             if (e == cudaSuccess) {
-                rle_count_kernel<<<nt, kStagedThreads, smem, s>>>(a);
+                rle_count_kernel<<<(nt + kWT - 1) / kWT, kWThreads, kWideSmem, s>>>(a);
                 e = cudaGetLastError();
             }
             if (e == cudaSuccess) {
