@@ -73,38 +73,24 @@ struct RleCountArgs {
 };
 
 
-// Walk stream `st` across tile [ts, te) from its directory entry; Visit(fs, fe, bit, ds, de, lit)
-// is called for each marker whose runs intersect the tile (fill [fs,fe), dirty [ds,de) with the
-// first literal at stream index lit).
-template <typename Visit>
-__device__ __forceinline__ void walk_tile(const RleCountArgs &a, int st, uint32_t tile, uint64_t ts, uint64_t te,
-                                          Visit &&visit) {
-    const uint64_t *s = a.ptrs[st];
-    const uint64_t L = a.lens[st];
-    const uint2 e = a.dir[(size_t)tile * a.n + st];
-    uint64_t i = e.x, pos = e.y;
-    while (i < L && pos < te) {
-        const uint64_t mk = __ldg(s + i);
-        const uint64_t run = (mk >> 1) & 0xFFFFFFFFull;
-        const uint64_t dirty = mk >> 33;
-        const uint64_t fe = pos + run, de = fe + dirty;
-        if (de > ts) visit(pos, fe, (uint32_t)(mk & 1), fe, de, i + 1, s);
-        pos = de;
-        i += 1 + dirty;
-    }
-}
-
-
-// walk_tile over every stream st = first, first + stride, ... < n, U streams at a time
-// with their marker loads interleaved (U independent HBM loads in flight per thread
-// instead of one dependent chain): phase C's walks are latency-bound, and a tile that
-// needs them otherwise formed the tail of the grid.
+// Walk every stream st = first, first + stride, ... < n across tile [ts, te) from its
+// directory entry; visit(fs, fe, bit, ds, de, lit, s) is called for each marker whose runs
+// intersect the tile (fill [fs, fe), dirty [ds, de), first literal at s[lit]).  U streams
+// are walked at a time with their marker loads interleaved (U independent loads in flight
+// per thread instead of one dependent chain).  A stream st < nstaged whose slice the CTA
+// staged reads it from shared memory (stage_off[st] = pool word of its directory marker,
+// kNotStaged otherwise; stage_end[st] = the first stream word past the staged slice: the
+// literal words of the slice's last marker can extend beyond it, and those are read from
+// HBM); the other streams walk HBM, latency-bound.
+constexpr uint32_t kNotStaged = 0xFFFFFFFFu;
 template <int U, typename Visit>
 __device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int stride, uint32_t tile, uint64_t ts,
-                                           uint64_t te, Visit &&visit) {
+                                           uint64_t te, const uint64_t *pool, const uint32_t *stage_off,
+                                           const uint32_t *stage_end, int nstaged, Visit &&visit) {
     for (int base = first; base < a.n; base += U * stride) {
         const uint64_t *sp[U];
         uint64_t L[U], i[U], pos[U];
+        uint32_t send[U];  // staged streams: first stream word not in the pool
         bool act[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -112,6 +98,7 @@ __device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int
             act[u] = st < a.n;
             sp[u] = nullptr;
             L[u] = i[u] = pos[u] = 0;
+            send[u] = kNotStaged;
             if (act[u]) {
                 sp[u] = a.ptrs[st];
                 L[u] = a.lens[st];
@@ -119,6 +106,13 @@ __device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int
                 i[u] = e.x;
                 pos[u] = e.y;
                 act[u] = i[u] < L[u] && pos[u] < te;
+                if (st < nstaged) {
+                    const uint32_t so = stage_off[st];
+                    if (so != kNotStaged) {
+                        sp[u] = pool + so - e.x;  // sp[u][i] is stream word i, for e.x <= i < send[u]
+                        send[u] = stage_end[st];
+                    }
+                }
             }
         }
         for (;;) {
@@ -128,14 +122,26 @@ __device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int
             if (!any) break;
             uint64_t mk[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) mk[u] = act[u] ? __ldg(sp[u] + i[u]) : 0ull;
+            for (int u = 0; u < U; ++u) mk[u] = act[u] ? sp[u][i[u]] : 0ull;  // generic: HBM or the pool
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (!act[u]) continue;
                 const uint64_t run = (mk[u] >> 1) & 0xFFFFFFFFull;
                 const uint64_t dirty = mk[u] >> 33;
                 const uint64_t fe = pos[u] + run, de = fe + dirty;
-                if (de > ts) visit(pos[u], fe, (uint32_t)(mk[u] & 1), fe, de, i[u] + 1, sp[u]);
+                if (de > ts) {
+                    // literal words of this marker the tile needs: stream words [i + 1, i + 1 + (min(de, te) - fe))
+                    const uint64_t need = i[u] + 1 + (min(de, te) - min(fe, te));
+                    if (need <= send[u]) {
+                        visit(pos[u], fe, (uint32_t)(mk[u] & 1), fe, de, i[u] + 1, sp[u]);
+                    } else {  // rare: the slice's last marker, its literals run past the staged words
+                        const uint64_t in_pool = send[u] > i[u] + 1 ? send[u] - (i[u] + 1) : 0;  // literals staged
+                        const uint64_t cut = min(fe + in_pool, de);
+                        if (cut > fe) visit(pos[u], fe, (uint32_t)(mk[u] & 1), fe, cut, i[u] + 1, sp[u]);
+                        const uint64_t *gp = a.ptrs[base + u * stride];
+                        visit(pos[u], fe, (uint32_t)(mk[u] & 1), cut, de, i[u] + 1 + (cut - fe), gp);
+                    }
+                }
                 pos[u] = de;
                 i[u] += 1 + dirty;
                 act[u] = i[u] < L[u] && pos[u] < te;
@@ -402,30 +408,57 @@ __global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const
 #ifndef BQ_K4C_THREADS
 #define BQ_K4C_THREADS 512
 #endif
-#ifndef BQ_K4C_MINB
-#define BQ_K4C_MINB 2
-#endif
 #ifndef BQ_K4C_SLOTS
 #define BQ_K4C_SLOTS 1024
 #endif
 constexpr int kResolveThreads = BQ_K4C_THREADS;
 constexpr int kResolveSlots = BQ_K4C_SLOTS;
 #ifndef BQ_K4C_CAP
-#define BQ_K4C_CAP 6144
+#define BQ_K4C_CAP 4096
 #endif
 constexpr int kResolveCapC = BQ_K4C_CAP;  // literal words per batch (8 bytes each)
-constexpr size_t kResolveSmem = (size_t)(kRleTile + 4) * 4 + tile_resolve_bytes<kResolveSlots, kResolveCapC>() +
-                                (size_t)kRleTile * 2;
+// The tile's stream slices (directory marker .. the marker covering the tile's end, literal
+// words included) are staged into one CTA-wide pool by TMA bulk copies, one per stream, so
+// phase C's marker walks and literal loads read shared memory instead of following ~10-30
+// dependent HBM loads per stream; one CTA per SM.  C4 needs ~19.6 k words per tile.
+#ifndef BQ_K4C_POOL
+#define BQ_K4C_POOL 21504
+#endif
+#ifndef BQ_K4C_STAGED
+#define BQ_K4C_STAGED 1024  // streams with a stage_off entry (the rest walk HBM)
+#endif
+constexpr int kResolvePool = BQ_K4C_POOL;
+constexpr int kResolveStaged = BQ_K4C_STAGED;
+static_assert(kResolveStaged % kResolveThreads == 0, "staging plans kResolveStaged / NT streams per thread");
+constexpr size_t kResolveFixed = (size_t)(kRleTile + 4) * 4 + tile_resolve_bytes<kResolveSlots, kResolveCapC>() +
+                                 (size_t)kRleTile * 2;
+constexpr size_t kResolveSmem = kResolveFixed + (size_t)kResolveStaged * 8 + 16 + (size_t)kResolvePool * 8;
+static_assert(kResolveFixed % 16 == 0, "pool alignment");
 
-__global__ void __launch_bounds__(kResolveThreads, BQ_K4C_MINB) rle_resolve_kernel(const __grid_constant__ RleCountArgs a) {
+__global__ void __launch_bounds__(kResolveThreads, 1) rle_resolve_kernel(const __grid_constant__ RleCountArgs a) {
     constexpr int NT = kResolveThreads;
+    constexpr int kPerT = kResolveStaged / NT;
     extern __shared__ __align__(16) uint8_t rs_smem[];
     uint32_t *cnt = reinterpret_cast<uint32_t *>(rs_smem);
     uint8_t *region = rs_smem + (size_t)(kRleTile + 4) * 4;
     uint16_t *undecided = reinterpret_cast<uint16_t *>(region + tile_resolve_bytes<kResolveSlots, kResolveCapC>());
-    __shared__ uint32_t n_undecided;
-    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t *stage_off = reinterpret_cast<uint32_t *>(rs_smem + kResolveFixed);
+    uint32_t *stage_end = stage_off + kResolveStaged;
+    uint64_t *bar_p = reinterpret_cast<uint64_t *>(rs_smem + kResolveFixed + (size_t)kResolveStaged * 8);
+    uint64_t *pool = reinterpret_cast<uint64_t *>(rs_smem + kResolveFixed + (size_t)kResolveStaged * 8 + 16);
+    __shared__ uint32_t n_undecided, stage_tot[NT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.n;
+    const int nstaged = min(n, kResolveStaged);
     const uint32_t ntodo = *a.todo_count;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bar_p);
+    const uint32_t pool_s = (uint32_t)__cvta_generic_to_shared(pool);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(NT) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t parity = 0;
     unsigned long long pc = 0;
     for (uint32_t k = blockIdx.x; k < ntodo; k += gridDim.x) {
         const uint32_t tile = a.todo[k];
@@ -433,21 +466,90 @@ __global__ void __launch_bounds__(kResolveThreads, BQ_K4C_MINB) rle_resolve_kern
         const uint64_t te = min(ts + (uint64_t)kRleTile, a.total_words);
         const int width = (int)(te - ts);
         if (tid == 0) n_undecided = 0;
-        const uint4 *src = reinterpret_cast<const uint4 *>(a.todo_cnt + (size_t)k * kRleTile);
-        for (int j = tid; j < kRleTile / 4; j += NT) reinterpret_cast<uint4 *>(cnt)[j] = src[j];
+        // ---- stage the slices of streams [0, nstaged): thread tid plans streams tid * kPerT + j ----
+        uint32_t len[kPerT], head[kPerT], first_w[kPerT], sum = 0;
+        uintptr_t src[kPerT];
+#pragma unroll
+        for (int j = 0; j < kPerT; ++j) {
+            const int st = tid * kPerT + j;
+            len[j] = 0;
+            head[j] = 0;
+            first_w[j] = 0;
+            src[j] = 0;
+            if (st < nstaged && a.debug < 2) {
+                const uint64_t L = a.lens[st];
+                const uint2 e = a.dir[(size_t)tile * n + st];
+                const uint32_t nx = a.dir[(size_t)(tile + 1) * n + st].x;
+                if (e.x < L && e.y < te) {
+                    const uint64_t *p = a.ptrs[st];
+                    const uint64_t hi = min((uint64_t)(nx == 0xFFFFFFFFu ? L : nx) + 1, L);
+                    src[j] = reinterpret_cast<uintptr_t>(p + e.x) & ~(uintptr_t)15;
+                    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p + hi) + 15) & ~(uintptr_t)15;
+                    len[j] = (uint32_t)((b1 - src[j]) / 8);
+                    head[j] = (uint32_t)((reinterpret_cast<uintptr_t>(p + e.x) - src[j]) / 8);
+                    first_w[j] = e.x;
+                }
+            }
+            sum += len[j];
+        }
+        const uint32_t incl = warp_incl_scan_u32(sum, lane);
+        if (lane == 31) stage_tot[warp] = incl;
         __syncthreads();
-        // the undecided words, as phase B classified them
+        uint32_t off = incl - sum;
+        for (int w = 0; w < warp; ++w) off += stage_tot[w];
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int j = 0; j < kPerT; ++j) {
+            const int st = tid * kPerT + j;
+            const bool staged = len[j] && off + len[j] <= (uint32_t)kResolvePool;
+            stage_off[st] = staged ? off + head[j] : kNotStaged;
+            stage_end[st] = first_w[j] - head[j] + len[j];  // may exceed the stream by the alignment word: never read
+            if (!staged) len[j] = 0;
+            bytes += len[j] * 8;
+            off += len[j] ? len[j] : 0;
+        }
+        // one arrival per thread carrying its copies' bytes, then the copies
+        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
+                     "r"(bytes)
+                     : "memory");
+        {
+            uint32_t o = off;
+#pragma unroll
+            for (int j = kPerT - 1; j >= 0; --j) {
+                o -= len[j];
+                if (len[j])
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            pool_s + o * 8u),
+                        "l"(src[j]), "r"(len[j] * 8u), "r"(bar)
+                        : "memory");
+            }
+        }
+        // meanwhile: the tile's scanned counts and the undecided words, as phase B classified them
+        const uint4 *csrc = reinterpret_cast<const uint4 *>(a.todo_cnt + (size_t)k * kRleTile);
+        for (int j = tid; j < kRleTile / 4; j += NT) reinterpret_cast<uint4 *>(cnt)[j] = csrc[j];
+        __syncthreads();
         for (int j = tid; j < width; j += NT) {
             const uint32_t c = cnt[j];
             const uint32_t ones = c & 0xFFFFu, dirty = c >> 16;
             if (ones + dirty > __ldg(a.const_until + ones)) undecided[atomicAdd(&n_undecided, 1u)] = (uint16_t)j;
+        }
+        {
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(done)
+                    : "r"(bar), "r"(parity)
+                    : "memory");
+            parity ^= 1u;
         }
         __syncthreads();
         TileDecide d{ts, width, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out,
                      (uint64_t)a.tile0 * kRleTile, a.breaks, a.nbreak};
         pc += tile_resolve<NT, kResolveSlots, kResolveCapC>(
             d, cnt, undecided, n_undecided, region, [&](const uint16_t *slot_of, auto &&add_bits) {
-                walk_tiles<BQ_K4_C_ILP>(a, tid, NT, tile, ts, te,
+                walk_tiles<BQ_K4_C_ILP>(a, tid, NT, tile, ts, te, pool, stage_off, stage_end, nstaged,
                                         [&](uint64_t, uint64_t, uint32_t, uint64_t ds, uint64_t de, uint64_t lit,
                                             const uint64_t *s) {
                                             const uint64_t lo = max(ds, ts), hi = min(de, te);
@@ -458,6 +560,7 @@ __global__ void __launch_bounds__(kResolveThreads, BQ_K4C_MINB) rle_resolve_kern
                                         });
             });
         __syncthreads();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of the pool before the next tile's copies
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);

@@ -119,7 +119,8 @@ __device__ __forceinline__ void ripple(uint64_t (&c)[16], uint64_t carry) {
 }
 
 // Bit-sliced sum of the n literal words at addrs[0..n) into M planes (plane j = bit j
-// of the 64 counts); four independent loads in flight at a time.
+// of the 64 counts); four independent loads in flight at a time.  The addresses are
+// generic: literal words in HBM, or in the shared-memory pool K4c staged them into.
 template <int M>
 __device__ __forceinline__ void planes_sum(const uint64_t *addrs, uint32_t n, uint64_t (&c)[16]) {
 #pragma unroll
@@ -128,11 +129,11 @@ __device__ __forceinline__ void planes_sum(const uint64_t *addrs, uint32_t n, ui
     for (; i + 4 <= n; i += 4) {
         uint64_t x[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const uint64_t *>(addrs[i + k]));
+        for (int k = 0; k < 4; ++k) x[k] = *reinterpret_cast<const uint64_t *>(addrs[i + k]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) ripple<M>(c, x[k]);
     }
-    for (; i < n; ++i) ripple<M>(c, __ldg(reinterpret_cast<const uint64_t *>(addrs[i])));
+    for (; i < n; ++i) ripple<M>(c, *reinterpret_cast<const uint64_t *>(addrs[i]));
 }
 
 // count >= k per bit position, for the bit-sliced count c (planes 0..M-1 in use, the
@@ -238,7 +239,7 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
             for (int k = tid; k < 32; k += NT) big[k] = 0u;
             __syncthreads();
             auto add_big = [&](uint16_t, const uint64_t *p) {
-                const uint64_t x = __ldg(p);
+                const uint64_t x = *p;
                 uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
 #pragma unroll 1
                 for (int j = 0; (lo | hi) && j < 16; ++j) {
@@ -284,7 +285,7 @@ __device__ __forceinline__ unsigned long long tile_resolve(const TileDecide &d, 
                 const uint64_t *lits = entries + soff[u];
                 uint32_t c_lo = 0, c_hi = 0;  // counts of bit `lane` and bit `lane + 32`
                 for (uint32_t b0 = 0; b0 < dirty; b0 += 32) {
-                    const uint64_t x = b0 + lane < dirty ? __ldg(reinterpret_cast<const uint64_t *>(lits[b0 + lane])) : 0ull;
+                    const uint64_t x = b0 + lane < dirty ? *reinterpret_cast<const uint64_t *>(lits[b0 + lane]) : 0ull;
 #pragma unroll
                     for (int bit = 0; bit < 32; ++bit) {
                         const uint32_t m_lo = __ballot_sync(0xffffffffu, (x >> bit) & 1u);
