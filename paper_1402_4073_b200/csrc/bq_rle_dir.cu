@@ -122,13 +122,19 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     const int lane = threadIdx.x;
 
     unsigned int t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1u);  // tickets in start order: a block's predecessor started earlier
+    // tickets in start order: a block's predecessor started earlier.  The counter starts at
+    // 0xFFFFFFFF (it shares one 0xFF memset with the links and the error word).  A ticket
+    // taken any earlier than its block starts (persistent warps prefetching the next one,
+    // even after publishing: 0.78 / 0.70 ms instead of 0.66 on C4) lets start order drift from
+    // ticket order, and blocks then spin on predecessors whose warps are still busy.
+    if (lane == 0) t = atomicAdd(a.ticket, 1u) + 1u;
     t = __shfl_sync(0xffffffffu, t, 0);
     const uint32_t full = a.full_levels * (uint32_t)a.n;
     const uint2 job = t < full ? make_uint2(t % (uint32_t)a.n, t / (uint32_t)a.n) : a.jobs[t - full];
     const uint32_t stream = job.x, blk = job.y;
     const uint64_t *s = a.ptrs[stream];
     const uint32_t L = (uint32_t)a.lens[stream];  // < 2^32 - 2 (bq_rle_query_create)
+    const bool last_block = blk + 1 == a.nblocks[stream];  // loaded here: the publish below is on the look-back chain
     const uint64_t total = a.total_words;
 
     // ---- this lane's segment [q, qe) and its staging: words [q - kHalo, qe) --------
@@ -232,6 +238,41 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     uint64_t span = 0, exit_ = entry;
     if (active && entry < qe) exit_ = walk(entry, span);
 
+    // ---- resolution: every entry must be the previous segment's exit -------------
+    // All lanes check at once; a lane whose predecessor's exit lies past its segment
+    // holds no marker start (it passes the exit through), a lane whose guess differs
+    // re-walks from the true entry.  Repeat while any exit changed (typically never).
+    // Then the inclusive prefix of the spans (positions relative to the block).
+    uint64_t incl = 0;
+    auto resolve = [&](uint64_t n_in) {
+        for (;;) {
+            uint64_t prev = __shfl_up_sync(0xffffffffu, exit_, 1);
+            if (lane == 0) prev = n_in;
+            bool changed = false;
+            if (!active || prev >= qe) {
+                changed = exit_ != prev || span;
+                entry = (uint32_t)min(prev, (uint64_t)L + 1);
+                exit_ = prev;
+                span = 0;
+            } else if (prev != entry) {
+                entry = (uint32_t)prev;
+                exit_ = walk(entry, span);
+                changed = true;
+            }
+            if (!__ballot_sync(0xffffffffu, changed)) break;
+        }
+        incl = span;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+    };
+    // The block resolves itself before its entry is known, on lane 0's guess: the look-back
+    // chain (one hop per block of a stream, ~290 on C4) then carries only a compare, an add
+    // and the store below instead of the ballot round and the prefix sum.
+    const uint64_t n_guess = __shfl_sync(0xffffffffu, (uint64_t)entry, 0);
+    resolve(n_guess);
     // ---- the block's entry: the previous block's exit (decoupled look-back) --------
     uint64_t n_in = 0, p_in = 0;
     if (blk > 0) {
@@ -248,46 +289,20 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
         n_in = __shfl_sync(0xffffffffu, n_in, 0);
         p_in = __shfl_sync(0xffffffffu, p_in, 0);
     }
-    // ---- resolution: every entry must be the previous segment's exit -------------
-    // All lanes check at once; a lane whose predecessor's exit lies past its segment
-    // holds no marker start (it passes the exit through), a lane whose guess differs
-    // re-walks from the true entry.  Repeat while any exit changed (typically never).
-    for (;;) {
-        uint64_t prev = __shfl_up_sync(0xffffffffu, exit_, 1);
-        if (lane == 0) prev = n_in;
-        bool changed = false;
-        if (!active || prev >= qe) {
-            changed = exit_ != prev || span;
-            entry = (uint32_t)min(prev, (uint64_t)L + 1);
-            exit_ = prev;
-            span = 0;
-        } else if (prev != entry) {
-            entry = (uint32_t)prev;
-            exit_ = walk(entry, span);
-            changed = true;
-        }
-        if (!__ballot_sync(0xffffffffu, changed)) break;
+    if (n_in != n_guess) resolve(n_in);  // warp-uniform; rare
+    // publish this block's exit for the next block of the stream (clamped: > L is a
+    // truncated group, > total overlong; both below the ~0 sentinel)
+    if (lane == 31 && !last_block) {
+        const uint64_t ex = min(exit_, (uint64_t)L + 1), pe = min(p_in + incl, total + 1);
+        st_link(a.link + (size_t)blk * a.n + stream, ex | (pe << 32));
     }
-    // absolute word positions: exclusive prefix of the spans
-    uint64_t incl = span;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
+    // absolute word positions
     const uint64_t pos0 = p_in + incl - span;
     const uint64_t p_end = __shfl_sync(0xffffffffu, p_in + incl, 31);
     const uint64_t x_end = __shfl_sync(0xffffffffu, exit_, 31);
-    // publish this block's exit for the next block of the stream (clamped: > L is a
-    // truncated group, > total overlong; both below the ~0 sentinel)
-    const bool last_block = blk + 1 == a.nblocks[stream];
-    if (lane == 31) {
-        const uint64_t ex = min(x_end, (uint64_t)L + 1), pe = min(p_end, total + 1);
-        if (!last_block) st_link(a.link + (size_t)blk * a.n + stream, ex | (pe << 32));
-        else {
-            if (x_end > L) dir_fail(a, DIR_ERR_TRUNCATED, stream);
-            else if (p_end > total) dir_fail(a, DIR_ERR_OVERLONG, stream);
-        }
+    if (lane == 31 && last_block) {
+        if (x_end > L) dir_fail(a, DIR_ERR_TRUNCATED, stream);
+        else if (p_end > total) dir_fail(a, DIR_ERR_OVERLONG, stream);
     }
 
     // ---- directory rows of the tile boundaries this segment's markers cover ------
@@ -391,11 +406,11 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
     static char *staging = nullptr;
     static size_t staging_cap = 0;
     std::lock_guard<std::mutex> staging_guard(staging_mu);
-    if (staging_cap < up_bytes) {
+    if (staging_cap < up_bytes + 16) {
         if (staging) cudaFreeHost(staging);
         staging = nullptr;
         staging_cap = 0;
-        const size_t cap = std::max<size_t>(up_bytes, 1 << 16);
+        const size_t cap = std::max<size_t>(up_bytes + 16, 1 << 16);
         if (cudaHostAlloc(reinterpret_cast<void **>(&staging), cap, cudaHostAllocDefault) != cudaSuccess) {
             cudaGetLastError();
             staging = nullptr;
@@ -411,20 +426,20 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
             for (int i = 0; i < n; ++i)
                 if (b < nblk[i]) jt[k++] = make_uint2((uint32_t)i, b);
     }
+    // scratch: block counts | job table | links | ticket | error word (the last three are
+    // adjacent: one memset)
     char *sc = static_cast<char *>(d_scratch);
-    unsigned long long *d_link = reinterpret_cast<unsigned long long *>(sc);
-    uint32_t *d_nblk = reinterpret_cast<uint32_t *>(sc + a_link);
-    uint2 *d_jobs = reinterpret_cast<uint2 *>(sc + a_link + a_nblk);
-    unsigned int *d_ticket = reinterpret_cast<unsigned int *>(sc + a_link + a_nblk + a_jobs);
-    unsigned long long *d_err = reinterpret_cast<unsigned long long *>(sc + a_link + a_nblk + a_jobs + 8);
+    uint32_t *d_nblk = reinterpret_cast<uint32_t *>(sc);
+    uint2 *d_jobs = reinterpret_cast<uint2 *>(sc + a_nblk);
+    unsigned long long *d_link = reinterpret_cast<unsigned long long *>(sc + a_nblk + a_jobs);
+    unsigned int *d_ticket = reinterpret_cast<unsigned int *>(sc + a_nblk + a_jobs + a_link);
+    unsigned long long *d_err = reinterpret_cast<unsigned long long *>(sc + a_nblk + a_jobs + a_link + 8);
     // nblk and the job table are adjacent in both buffers: one copy
     if (extra_bytes) memcpy(staging + a_up, h_extra, extra_bytes);
     cudaError_t e = cudaMemcpyAsync(d_nblk, staging, a_nblk + rem * 8, cudaMemcpyHostToDevice, 0);
     if (e == cudaSuccess && extra_bytes)
         e = cudaMemcpyAsync(d_extra, staging + a_up, extra_bytes, cudaMemcpyHostToDevice, 0);
-    if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, (size_t)maxb * n * 8, 0);
-    if (e == cudaSuccess) e = cudaMemsetAsync(d_ticket, 0, 8, 0);
-    if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0xFF, 8, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, a_link + 16, 0);
     if (e == cudaSuccess) {
         DirArgs a;
         a.ptrs = d_ptrs;
@@ -444,10 +459,13 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
         rle_dir_kernel<<<(unsigned)njobs, 32, 0, 0>>>(a);
         e = cudaGetLastError();
     }
-    unsigned long long herr = ~0ull;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, 8, cudaMemcpyDeviceToHost, 0);
+    // the verdict comes back into the pinned staging buffer (a pageable destination would
+    // go through the driver's own staging copy)
+    unsigned long long *h_verdict = reinterpret_cast<unsigned long long *>(staging + ((up_bytes + 7) & ~(size_t)7));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_verdict, d_err, 8, cudaMemcpyDeviceToHost, 0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) return cuda_error(e, "rle directory (K3)");
+    const unsigned long long herr = *h_verdict;
     if (herr != ~0ull) {
         const uint32_t code = (uint32_t)(herr & 0xFFFFFFFFull);
         *err_code = code == DIR_ERR_TRUNCATED ? 1 : code == DIR_ERR_OVERLONG ? 2 : 3;
