@@ -333,15 +333,27 @@ class DeviceBitmap:
 class DeviceRleBitmap:
     """RLE stream (reference marker format) in HBM: 1-D int64 CUDA tensor."""
 
-    __slots__ = ("data", "bit_length", "n_words")
+    __slots__ = ("data", "bit_length", "n_words", "_span")
 
     def __init__(self, data, bit_length: int, n_words: int | None = None):
         self.data = data
         self.bit_length = bit_length
         self.n_words = data.numel() if n_words is None else int(n_words)
+        self._span = None
 
     def data_ptr(self) -> int:
         return self.data.data_ptr()
+
+    def span(self) -> tuple:
+        """(device pointer or 0, stream words), computed once: streams are immutable
+        (bitmaps.py:12-13), and a query over 1024 of them is ~1 ms of device work, so
+        the per-stream torch attribute calls would show."""
+        sp = self._span
+        if sp is None:
+            if not self.data.is_cuda:
+                raise InputError("RLE streams must be CUDA tensors")
+            sp = self._span = (self.data.data_ptr() if self.n_words else 0, self.n_words)
+        return sp
 
     def to_host(self, cls=RleBitmap):
         return cls(self.data[: self.n_words].cpu().numpy().view(np.uint64).tolist(), self.bit_length)

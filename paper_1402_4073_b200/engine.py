@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 from array import array
+from itertools import chain
 import threading
 from collections import OrderedDict
 from typing import Sequence
@@ -215,12 +216,18 @@ class RleQuery:
         self.r_bits = int(r_bits)
         # one pass per column (a fresh query over 1024 streams is ~1 ms of device work,
         # so the marshalling stays vectorised: no per-stream ctypes structs)
-        ts = [s.data if isinstance(s, DeviceRleBitmap) else s for s in streams]
-        nws = [s.n_words if isinstance(s, DeviceRleBitmap) else s.numel() for s in streams]
-        if not all(t.is_cuda for t in ts):
-            raise InputError("RLE streams must be CUDA tensors")
-        self._keep = ts
-        self._spans = _lib.span_columns([t.data_ptr() if n else 0 for t, n in zip(ts, nws)], nws)
+        try:  # all DeviceRleBitmap: their cached (pointer, words) pairs, one pass
+            pairs = [s.span() for s in streams]
+            self._keep = [s.data for s in streams]
+        except AttributeError:
+            ts = [s.data if isinstance(s, DeviceRleBitmap) else s for s in streams]
+            nws = [s.n_words if isinstance(s, DeviceRleBitmap) else s.numel() for s in streams]
+            if not all(isinstance(t, torch.Tensor) and t.is_cuda for t in ts):
+                raise InputError("RLE streams must be CUDA tensors")
+            self._keep = ts
+            pairs = [(t.data_ptr() if n else 0, n) for t, n in zip(ts, nws)]
+        self._spans = (np.fromiter(chain.from_iterable(pairs), dtype=np.uint64, count=2 * len(pairs)).reshape(-1, 2)
+                       if pairs else np.zeros((1, 2), dtype=np.uint64))
         self._create(word_range)
 
     @classmethod

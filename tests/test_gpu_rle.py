@@ -302,6 +302,46 @@ def test_all_literal_streams_overflow_pools(bq):
     assert np.array_equal(host(out, nw), exp)
 
 
+def test_phase_c_staging_edges(bq):
+    """K4c's staged slices: literal groups that straddle tile ends (the words of a
+    slice's last marker past the staged part are read from HBM), more streams than
+    the staging table holds (1100 > 1024), streams that end inside a tile, and a
+    threshold low enough that nearly every tile reaches phase C."""
+    from oracle import oracle as Or
+
+    rng = np.random.default_rng(37)
+    n, r = 1100, 64 * 4096 + 21
+    nw = (r + 63) // 64
+    streams = []
+    for i in range(n):
+        w = np.zeros(nw, dtype=np.uint64)
+        if i % 5 == 0:  # a long literal group across every tile end
+            for b in range(1024, nw, 1024):
+                lo, hi = b - int(rng.integers(1, 40)), min(nw, b + int(rng.integers(1, 40)))
+                w[lo:hi] = rng.integers(1, 2**63, size=hi - lo, dtype=np.uint64)
+        elif i % 5 == 1:  # sparse literals and one-fills
+            idx = rng.integers(0, nw, size=200)
+            w[idx] = rng.integers(1, 2**63, size=idx.size, dtype=np.uint64)
+            w[int(rng.integers(0, nw - 300)):][:300] = np.uint64(2**64 - 1)
+        elif i % 5 == 2:  # ends inside the second tile (implicit zero tail)
+            w[: 1024 + int(rng.integers(1, 900))] = rng.integers(0, 2**64 - 1, size=1, dtype=np.uint64)[0] | np.uint64(5)
+        else:  # a few dense windows
+            for _ in range(3):
+                a = int(rng.integers(0, nw - 64))
+                w[a:a + 64] = rng.integers(0, 2**64 - 1, size=64, dtype=np.uint64)
+        w[-1] &= np.uint64((1 << (r % 64)) - 1)
+        streams.append(Or.rle_compress(Or.trim(w), r))
+    q = bq.RleQuery(dev(streams), r)
+    for t in (1, 2, 3, 50, 221):
+        out, pc = q.threshold(t)
+        exp = O.cdom_threshold(streams, r, t)
+        assert np.array_equal(host(out, nw), exp), t
+        assert int(pc.item()) == popcount(exp)
+    acc = [k % 2 == 1 for k in range(n + 1)]
+    out, pc = q.symmetric(acc)
+    assert np.array_equal(host(out, nw), O.cdom_symmetric(streams, r, acc))
+
+
 def test_heavy_words_and_bank_skewed_events(bq):
     """K4s phase C's warp path (words with >= 128 literal words) next to its thread
     path in the same tiles, and event lists skewed onto a few shared-memory banks
