@@ -1,7 +1,6 @@
-# A/B of the default library (K4w and BQ_K4_WIDE=0) and every _variants/ build on the C4 fresh-query line
+# A/B of the default library and every _variants/ build on the C4 fresh-query line
 mkdir -p gpurun_out
 for rep in 1 2; do
-  BQ_K4_WIDE=0 timeout 600 python bench.py --workload c4 --steps 30 --no-e2e --no-cpu-baseline > gpurun_out/abw_k4_$rep.log 2>&1
   timeout 600 python bench.py --workload c4 --steps 30 --no-e2e --no-cpu-baseline > gpurun_out/abw_default_$rep.log 2>&1
   for v in _variants/libbq_*.so; do
     n=$(basename $v .so)
