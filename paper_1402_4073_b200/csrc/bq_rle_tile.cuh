@@ -1,7 +1,7 @@
-// Phases B and C shared by the RLE tile kernels K4 (bq_rle.cu) and K4s
-// (bq_rle_sliced.cu): one CTA per 1024-word tile, after phase A has built the
-// packed difference array cnt[0..1024] (one-fills in bits 0-15, dirty inputs in
-// bits 16-31).  This is the decision half of runmerge.cdom_threshold /
+// Phases B and C shared by the RLE tile kernels K4 / K4c (bq_rle.cu) and K4s
+// (bq_rle_sliced.cu): the whole CTA works on one 1024-word tile at a time, after
+// phase A has built the tile's packed difference array cnt[0..1024] (one-fills in
+// bits 0-15, dirty inputs in bits 16-31).  This is the decision half of runmerge.cdom_threshold /
 // cdom_symmetric (runmerge.py:198-299): a word is decided by the fills alone when
 // accept[] is constant on [ones, ones + dirty]; otherwise its
 // literal bits are counted per position (dirty_segment_solver, runmerge.py:99-125).
