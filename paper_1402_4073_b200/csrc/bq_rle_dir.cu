@@ -170,6 +170,11 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     } else {
         asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar_s) : "memory");
     }
+    // lane 0's halo words are the previous block's last words, read from HBM: issued here so
+    // their latency hides behind the copies (after the wait they stalled the whole warp)
+    uint64_t halo0[kHalo];
+#pragma unroll
+    for (int j = 0; j < kHalo; ++j) halo0[j] = (lane == 0 && active && q > 0) ? __ldg(s + (q - kHalo + j)) : 0ull;
     // the previous block's exit is published by now in the common case: fetch it while
     // the copies land
     uint64_t link_prev = 0;
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
 #pragma unroll
         for (int j = kHalo - 1; j >= 0; --j) {
             const uint32_t h = q - kHalo + j;
-            const uint64_t hw = lane ? lds64(halo_s + (uint32_t)j * 8u) : __ldg(s + h);
+            const uint64_t hw = lane ? lds64(halo_s + (uint32_t)j * 8u) : halo0[j];
             const uint64_t nx64 = (uint64_t)h + 1 + (hw >> 33);
             const uint32_t nx = nx64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)nx64;
             nxs[j] = nx;
