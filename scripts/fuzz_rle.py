@@ -1,14 +1,16 @@
 """Randomised differential test of the RLE path at multi-tile sizes (GPU box).
 
-    python scripts/fuzz_rle.py [seconds] [first_seed]
+    python scripts/fuzz_rle.py [seconds] [first_seed] [eval|validate]
 
 Random instances of 1-300 streams over up to 12 tiles -- canonical encodings of
 Markov / dense / sparse / all-literal words and valid non-canonical streams (empty
 markers, split fills, runs ending on tile boundaries, implicit tails) -- are
 evaluated through K3 + K4 / K4c (first evaluation) and K3 + K4s (tile-sliced layout)
 at random thresholds, accept vectors and word-range shards, and compared with the
-oracle's cdom sweep word for word.  Prints one line per failure and a summary;
-exit code 1 on any mismatch.
+oracle's cdom sweep word for word.  ``validate`` instead corrupts single streams
+(truncation, bumped dirty / run fields, bits past r, extra markers, random words) and
+checks that K3 and the oracle's decompress accept or reject the same streams.  Prints
+one line per failure and a summary; exit code 1 on any mismatch.
 """
 import os
 import sys
@@ -131,19 +133,71 @@ def run_case(seed):
     return fails
 
 
+def validate_case(seed):
+    """K3's validation against the oracle's decompress on corrupted streams: both must
+    accept or both reject (FormatError); accepted streams must decode identically."""
+    rng = np.random.default_rng(seed)
+    nw = int(rng.choice([1, 3, 40, 1024, 1500, 5000, 40000]))
+    r = 64 * nw - (int(rng.integers(0, 64)) if rng.random() < 0.6 else 0)
+    r = max(r, 1)
+    nw = (r + 63) // 64
+    if rng.random() < 0.3 and r % 64 == 0:
+        s = noncanonical(rng, nw)
+    else:
+        s = canonical(rng, r, nw, ["markov", "literal", "sparse", "windows", "short"][int(rng.integers(5))])
+    s = s.copy()
+    kind = int(rng.integers(7))
+    if s.size and kind == 1:
+        s = s[: int(rng.integers(0, s.size))]
+    elif s.size and kind == 2:  # bump a word's dirty field (a marker's, if it is one)
+        i = int(rng.integers(s.size))
+        s[i] = np.uint64((int(s[i]) + (int(rng.integers(1, 4)) << 33)) & ((1 << 64) - 1))
+    elif s.size and kind == 3:  # bump a run
+        i = int(rng.integers(s.size))
+        s[i] = np.uint64((int(s[i]) + (int(rng.integers(1, 3000)) << 1)) & ((1 << 64) - 1))
+    elif s.size and kind == 4:  # high bits of the last word
+        s[-1] = np.uint64(int(s[-1]) | (1 << 63) | (1 << int(rng.integers(64))))
+    elif kind == 5:  # one more marker at the end
+        s = np.append(s, np.uint64(marker(int(rng.integers(2)), int(rng.integers(0, 3)), 0)))
+    elif s.size and kind == 6:  # a random word
+        s[int(rng.integers(s.size))] = rng.integers(0, 2**64 - 1, dtype=np.uint64)
+    try:
+        exp = O.rle_decompress(s, r)
+        ok = True
+    except O.OracleError:
+        ok = False
+    t = torch.from_numpy(s.view(np.int64)).cuda() if s.size else torch.zeros(1, dtype=torch.int64, device="cuda")
+    d = [bq.DeviceRleBitmap(t, 0, s.size)]
+    try:
+        q = bq.RleQuery(d, r)
+        got_ok = True
+    except bq.FormatError:
+        got_ok = False
+    if ok != got_ok:
+        return [f"validate seed {seed} kind {kind} r {r} words {s.size}: oracle {'ok' if ok else 'rejects'}, K3 {'ok' if got_ok else 'rejects'}"]
+    if ok:
+        os.environ["BQ_RLE_SLICED"] = "0"
+        out, _ = q.threshold(1)
+        if not np.array_equal(out[:nw].cpu().numpy().view(np.uint64), exp):
+            return [f"validate seed {seed} kind {kind} r {r}: decode differs"]
+        q.close()
+    return []
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    mode = sys.argv[3] if len(sys.argv) > 3 else "eval"
     t0 = time.time()
     cases = bad = 0
     while time.time() - t0 < budget:
-        f = run_case(seed)
+        f = validate_case(seed) if mode == "validate" else run_case(seed)
         for line in f:
             print("MISMATCH", line, flush=True)
         bad += bool(f)
         cases += 1
         seed += 1
-    print(f"fuzz_rle: {cases} cases, {bad} with mismatches, seeds up to {seed - 1}", flush=True)
+    print(f"fuzz_rle ({mode}): {cases} cases, {bad} with mismatches, seeds up to {seed - 1}", flush=True)
     sys.exit(1 if bad else 0)
 
 
