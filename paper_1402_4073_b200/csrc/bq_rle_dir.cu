@@ -79,6 +79,7 @@ struct DirArgs {
     const uint64_t *const *ptrs;
     const uint64_t *lens;
     int n;
+    uint64_t n_recip;            // ceil(2^64 / n), 0 when n = 1
     uint64_t total_words;        // ceil(r / 64)
     uint64_t tail_mask;          // valid bits of word total_words - 1 when r % 64 != 0, else 0
     uint32_t tile0, nrows;       // directory rows: tile boundaries tile0 .. tile0 + nrows - 1
@@ -130,7 +131,9 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     if (lane == 0) t = atomicAdd(a.ticket, 1u) + 1u;
     t = __shfl_sync(0xffffffffu, t, 0);
     const uint32_t full = a.full_levels * (uint32_t)a.n;
-    const uint2 job = t < full ? make_uint2(t % (uint32_t)a.n, t / (uint32_t)a.n) : a.jobs[t - full];
+    // t / n by a multiply with ceil(2^64 / n) (exact for t < 2^32; the host passes 0 for n = 1)
+    const uint32_t tq = a.n_recip ? (uint32_t)__umul64hi((uint64_t)t, a.n_recip) : t;
+    const uint2 job = t < full ? make_uint2(t - tq * (uint32_t)a.n, tq) : a.jobs[t - full];
     const uint32_t stream = job.x, blk = job.y;
     const uint64_t *s = a.ptrs[stream];
     const uint32_t L = (uint32_t)a.lens[stream];  // < 2^32 - 2 (bq_rle_query_create)
@@ -207,8 +210,10 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
         for (int j = kHalo - 1; j >= 0; --j) {
             const uint32_t h = q - kHalo + j;
             const uint64_t hw = lane ? lds64(halo_s + (uint32_t)j * 8u) : halo0[j];
-            const uint64_t nx64 = (uint64_t)h + 1 + (hw >> 33);
-            const uint32_t nx = nx64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)nx64;
+            // h + 1 + dirty, saturated: dirty < 2^31 and h + 1 < 2^32, so a wrapped sum is < dirty
+            const uint32_t hd = (uint32_t)(hw >> 33);
+            const uint32_t hsum = h + 1u + hd;
+            const uint32_t nx = hsum < hd ? 0xFFFFFFFFu : hsum;
             nxs[j] = nx;
             // nx > h, so a landing inside the halo is a later halo word k > j
             const uint32_t r = nx < q ? (rootp >> (4u * (nx - (q - kHalo)))) & 15u : (uint32_t)j;
@@ -450,6 +455,7 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
         a.ptrs = d_ptrs;
         a.lens = d_lens;
         a.n = n;
+        a.n_recip = n > 1 ? ~0ull / (uint64_t)n + 1 : 0ull;
         a.total_words = total_words;
         a.tail_mask = tail_mask;
         a.tile0 = tile0;
