@@ -164,25 +164,32 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
     auto load = [src](uint32_t k) { return GLOBAL ? __ldg(src + k) : src[k]; };
     if (lim == 0) return;
     const uint32_t Wu = (uint32_t)W;
-    // first marker: its fill starts at or before the tile (64-bit positions)
+    // first marker: the directory's entry, whose runs cover the tile's first word, so its fill
+    // starts d = ts - pos >= 0 words before the tile (both < 2^32: 32-bit arithmetic throughout)
     uint64_t mk = load(0);
     uint32_t dirty = (uint32_t)(mk >> 33);
     uint32_t carry;  // -dirty pending at the next marker's start (where this marker's literals end)
     uint32_t rel;
     {
-        const int64_t fs64 = (int64_t)pos - (int64_t)ts;
-        const int64_t fe64 = fs64 + (int64_t)(uint32_t)(mk >> 1);
-        const int64_t de64 = fe64 + dirty;
-        auto cl = [W](int64_t v) { return (uint32_t)(v < 0 ? 0 : (v > W ? W : v)); };
-        const uint32_t fs = cl(fs64), fe = cl(fe64), de = cl(de64);
-        const uint32_t ones = ((mk & 1) && fe > fs) ? 1u : 0u;
+        const uint32_t run = (uint32_t)(mk >> 1);
+        const uint32_t d = (uint32_t)ts - pos;
+        // tile-relative ends of the fill and of the literals, clamped to W (exact below W)
+        uint32_t fe, de;
+        if (run >= d) {
+            fe = min(run - d, Wu);
+            de = min(fe + min(dirty, Wu), Wu);
+        } else {
+            fe = 0u;
+            de = min(dirty - (d - run), Wu);  // > 0: the marker covers word ts
+        }
+        const uint32_t ones = ((uint32_t)mk & 1u) && fe ? 1u : 0u;
         const bool lit = de > fe;
-        atomicAdd(&cnt[ones ? fs : dummy], ones);
+        atomicAdd(&cnt[ones ? 0u : dummy], ones);
         const uint32_t at_fe = (lit ? 0x10000u : 0u) - ones;
         atomicAdd(&cnt[at_fe ? fe : dummy], at_fe);
-        if (de64 >= W) return;
+        if (de >= Wu) return;
         carry = lit ? 0xFFFF0000u : 0u;
-        rel = (uint32_t)de64;
+        rel = de;
     }
     uint32_t i = 1 + dirty;
     while (i < lim) {
