@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const
             const uint32_t glo = __shfl_sync(0xffffffffu, lo, lj * kWT);
 #pragma unroll
             for (int o = 1; o < kWT; o <<= 1) hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-            const uint64_t *gp = reinterpret_cast<const uint64_t *>(__shfl_sync(0xffffffffu, (unsigned long long)q.p, lj * kWT));
+            const uint64_t *gp = q.p;  // the batch's stream: the same pointer in every valid lane of the group
             uint32_t len = 0;
             uintptr_t b0 = 0;
             if (glo < hi) {
@@ -329,12 +329,8 @@ __global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const
                 const uintptr_t b1 = (reinterpret_cast<uintptr_t>(gp + hi) + 15) & ~(uintptr_t)15;
                 len = (uint32_t)((b1 - b0) / 8);
             }
-            uint32_t off = 0;
-#pragma unroll
-            for (int j = 0; j < kWS; ++j) {
-                const uint32_t v = __shfl_sync(0xffffffffu, len, j * kWT);
-                if (j < lj) off += v;
-            }
+            // pool offsets: prefix sum of the groups' lengths (carried by their first lanes)
+            const uint32_t off = warp_incl_scan_u32(li == 0 ? len : 0u, lane) - len;
             const bool staged = len && off + len <= (uint32_t)kWPool && a.debug < 2;
             if (li == 0 && staged) {
                 const uint32_t bytes = len * 8;
