@@ -254,7 +254,8 @@ static_assert((kWT & (kWT - 1)) == 0 && kWT <= 32 && kWS <= 16, "lanes = kWS str
 constexpr size_t kWCntBytes = (size_t)kWT * kWStride * 4;
 constexpr size_t kWBarBytes = (size_t)(kWThreads / 32) * 8;
 constexpr size_t kWPoolBytes = (size_t)(kWThreads / 32) * kWPool * 8;
-constexpr size_t kWideSmem = kWCntBytes + kWBarBytes + (kWPoolBytes > (size_t)kRleTile * 2 ? kWPoolBytes : (size_t)kRleTile * 2);
+constexpr size_t kWideSmem = kWCntBytes + kWBarBytes +
+                             (kWPoolBytes > (size_t)kWT * kRleTile * 2 ? kWPoolBytes : (size_t)kWT * kRleTile * 2);
 
 __global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const __grid_constant__ RleCountArgs a) {
     constexpr int NT = kWThreads, NW = NT / 32;
@@ -262,8 +263,8 @@ __global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const
     uint32_t *cnt_all = reinterpret_cast<uint32_t *>(rle_smem);  // kWT packed difference arrays
     uint64_t *bars = reinterpret_cast<uint64_t *>(rle_smem + kWCntBytes);
     uint8_t *region = rle_smem + kWCntBytes + kWBarBytes;  // phase A: warp pools; phase B: undecided list
-    __shared__ uint32_t n_undecided, todo_slot;
-    __shared__ uint32_t warp_sums[NW], warp_reach[NW];
+    __shared__ uint32_t n_und[kWT], todo_slot[kWT];
+    __shared__ uint32_t wsum_all[kWT * NW], wreach_all[kWT * NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int li = lane % kWT, lj = lane / kWT;  // this lane's tile within the CTA, stream within the batch
@@ -373,35 +374,80 @@ __global__ void __launch_bounds__(kWThreads, BQ_K4W_MINB) rle_count_kernel(const
     }
     __syncthreads();
 
-    // ---- B, tile by tile: prefix sum, decide every word the fills decide; C is deferred to K4c ----
-    uint16_t *undecided = reinterpret_cast<uint16_t *>(region);
-    unsigned long long pc = 0;
-    for (uint32_t i = 0; i < ntl; ++i) {
-        uint32_t *cnt = cnt_all + (size_t)i * kWStride;
-        const uint32_t trow = a.tile_off + first + i;
-        const uint64_t tsi = (uint64_t)(a.tile0 + trow) * kRleTile;
-        const int wi = (int)(min(tsi + (uint64_t)kRleTile, a.total_words) - tsi);
-        if (tid == 0) n_undecided = 0;
-        const uint32_t reach = tile_scan<NT>(cnt, warp_sums, warp_reach);
-        TileDecide d{tsi, wi, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out, (uint64_t)a.tile0 * kRleTile,
-                     a.breaks, a.nbreak};
-        pc += tile_decide<NT>(d, cnt, reach, undecided, &n_undecided);
-        __syncthreads();
-        if (n_undecided) {  // block-uniform
-            if (tid == 0) {
-                todo_slot = atomicAdd(a.todo_count, 1u);
-                a.todo[todo_slot] = trow;
+    // ---- B, all of the CTA's tiles between the same barriers: prefix sums, then decide every
+    // word the fills decide; C is deferred to K4c.  (Tile by tile it was 4 barrier rounds per
+    // tile with 4 words per thread between them.)
+    {
+        constexpr int kPer = kRleTile / NT;
+        uint32_t *warp_sums = wsum_all, *warp_reach = wreach_all;  // [kWT][NW]
+        uint32_t local[kWT][kPer], run_sum[kWT], incl[kWT];
+#pragma unroll
+        for (int i = 0; i < kWT; ++i) {
+            const uint32_t *cnt = cnt_all + (size_t)i * kWStride;
+            uint32_t rs = 0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                rs += cnt[tid * kPer + k];
+                local[i][k] = rs;
             }
-            __syncthreads();
-            uint4 *dst = reinterpret_cast<uint4 *>(a.todo_cnt + (size_t)todo_slot * kRleTile);
-            const uint4 *src = reinterpret_cast<const uint4 *>(cnt);
-            for (int k = tid; k < kRleTile / 4; k += NT) dst[k] = src[k];
+            run_sum[i] = rs;
+            incl[i] = warp_incl_scan_u32(rs, lane);
+            if (lane == 31) warp_sums[i * NW + warp] = incl[i];
+        }
+        if (tid < kWT) n_und[tid] = 0;
+        __syncthreads();
+        uint32_t reach[kWT];
+#pragma unroll
+        for (int i = 0; i < kWT; ++i) {
+            uint32_t *cnt = cnt_all + (size_t)i * kWStride;
+            uint32_t warp_off = 0;
+            for (int w = 0; w < warp; ++w) warp_off += warp_sums[i * NW + w];
+            const uint32_t excl = warp_off + incl[i] - run_sum[i];
+            uint32_t r = 0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const uint32_t c = local[i][k] + excl;
+                cnt[tid * kPer + k] = c;
+                r = max(r, (c & 0xFFFFu) + (c >> 16));
+            }
+            r = __reduce_max_sync(0xffffffffu, r);
+            if (lane == 0) warp_reach[i * NW + warp] = r;
         }
         __syncthreads();
-    }
+        unsigned long long pc = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
-    if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
+        for (int i = 0; i < kWT; ++i) {
+            if ((uint32_t)i >= ntl) break;  // block-uniform
+            uint32_t r = 0;
+            for (int w = 0; w < NW; ++w) r = max(r, warp_reach[i * NW + w]);
+            reach[i] = r;
+            const uint32_t trow = a.tile_off + first + (uint32_t)i;
+            const uint64_t tsi = (uint64_t)(a.tile0 + trow) * kRleTile;
+            const int wi = (int)(min(tsi + (uint64_t)kRleTile, a.total_words) - tsi);
+            TileDecide d{tsi, wi, a.total_words, a.last_mask, a.accept_bits, a.const_until, a.out,
+                         (uint64_t)a.tile0 * kRleTile, a.breaks, a.nbreak};
+            pc += tile_decide<NT>(d, cnt_all + (size_t)i * kWStride, reach[i],
+                                  reinterpret_cast<uint16_t *>(region) + (size_t)i * kRleTile, &n_und[i]);
+        }
+        __syncthreads();
+        // tiles with undecided words: a slot in K4c's list each, and their scanned counts
+        if (tid < (int)ntl && n_und[tid]) {
+            const uint32_t slot = atomicAdd(a.todo_count, 1u);
+            a.todo[slot] = a.tile_off + first + (uint32_t)tid;
+            todo_slot[tid] = slot;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kWT; ++i) {
+            if ((uint32_t)i >= ntl || !n_und[i]) continue;  // block-uniform
+            uint4 *dst = reinterpret_cast<uint4 *>(a.todo_cnt + (size_t)todo_slot[i] * kRleTile);
+            const uint4 *src = reinterpret_cast<const uint4 *>(cnt_all + (size_t)i * kWStride);
+            for (int k = tid; k < kRleTile / 4; k += NT) dst[k] = src[k];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pc += __shfl_down_sync(0xffffffffu, pc, o);
+        if (lane == 0 && pc && a.popcnt) atomicAdd(a.popcnt, pc);
+    }
 }
 
 // K4c: phase C of the tiles K4 deferred (the same tile_resolve, one CTA of kResolveThreads
