@@ -151,7 +151,7 @@ __device__ __forceinline__ void walk_tiles(const RleCountArgs &a, int first, int
 }
 
 
-// Marker sweep of one stream over a tile of W words// Marker sweep of one stream over a tile of W words in 32-bit tile-relative
+// Marker sweep of one stream over a tile of W words in 32-bit tile-relative
 // coordinates.  src[0] is the marker named by the stream's directory entry
 // (its fill run starts at word `pos`, at or before the tile); lim = stream
 // words available from there.  Each marker adds at most three entries to the
@@ -229,7 +229,7 @@ __device__ __forceinline__ void sweep_stream(const uint64_t *src, uint32_t lim, 
 // ten-instruction ELECT / R2UR / UBLKCP loop that was a third of the kernel's instructions),
 // and the copies carry no per-segment alignment padding.  Each lane walks one (stream, tile)
 // slice from the warp's private pool with two shared-memory reductions per marker, into its
-// tile's difference array; the CTA holds kWT arrays and then runs phase B tile by tile.  A
+// tile's difference array; the CTA holds kWT arrays and then runs phase B on all of them.  A
 // batch whose segments overflow the pool walks the rest from HBM.  C4, kernel time: one tile
 // per CTA 0.647 ms; kWT = 8 (2 or 3 CTAs/SM) 0.67; kWT = 4, 256 threads, 3 CTAs/SM 0.570;
 // kWT = 2 at 4 x 256 or 7 x 128 threads per SM the same; 608-word pools (overflows) 0.68.
