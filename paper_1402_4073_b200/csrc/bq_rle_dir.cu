@@ -53,6 +53,12 @@ namespace bq {
 #ifndef BQ_DIR_SEG
 #define BQ_DIR_SEG 32
 #endif
+// Measurement probe (never in the shipped library; profiles/README.md): the second walk also
+// issues phase A's difference-array updates as global reductions into one array for the whole
+// word range, the cost a single-read fresh query would add to this kernel.
+#ifndef BQ_K3_RED_PROBE
+#define BQ_K3_RED_PROBE 0
+#endif
 #ifndef BQ_DIR_LDS
 #define BQ_DIR_LDS 1
 #endif
@@ -90,6 +96,9 @@ struct DirArgs {
     unsigned long long *link;    // [block][stream]: exit | end position << 32, ~0 until published
     unsigned int *ticket;
     unsigned long long *err;     // min over (stream << 32 | precedence): the first failing stream
+#if BQ_K3_RED_PROBE
+    uint32_t *probe;             // measurement only: packed difference array of the whole range
+#endif
 };
 
 enum { DIR_ERR_TRUNCATED = 0, DIR_ERR_OVERLONG = 1, DIR_ERR_BEYOND_R = 2 };
@@ -326,6 +335,9 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
     if (nb >= rlim) nb = ~0ull;
     uint64_t pos = pos0;
     uint32_t i = active ? (uint32_t)((int64_t)entry - sbase) : iend;
+#if BQ_K3_RED_PROBE
+    uint32_t probe_carry = 0u;
+#endif
     auto dir_walk = [&](auto tail_check) {
         while (i < iend) {
             const uint64_t w = BQ_DIR_LDS ? lds64(slot_s + i * 8u) : slot[i];
@@ -341,10 +353,22 @@ __global__ void __launch_bounds__(32) rle_dir_kernel(const __grid_constant__ Dir
                     if (nb >= rlim) nb = ~0ull;
                 }
             }
+#if BQ_K3_RED_PROBE
+            {
+                const uint32_t ones = (uint32_t)w & 1u, litv = dirty ? 0x10000u : 0u;
+                const uint32_t at_pos = probe_carry + ones, at_fe = litv - ones;
+                if (at_pos) atomicAdd(a.probe + pos, at_pos);
+                if (at_fe) atomicAdd(a.probe + pos + (uint32_t)(w >> 1), at_fe);
+                probe_carry = 0u - litv;
+            }
+#endif
             tail_check(w, dirty, end);
             pos = end;
             i += 1 + dirty;
         }
+#if BQ_K3_RED_PROBE
+        if (probe_carry) atomicAdd(a.probe + pos, probe_carry);
+#endif
     };
     if (a.tail_mask) {
         dir_walk([&](uint64_t w, uint32_t dirty, uint64_t end) {
@@ -450,6 +474,17 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
     if (e == cudaSuccess && extra_bytes)
         e = cudaMemcpyAsync(d_extra, staging + a_up, extra_bytes, cudaMemcpyHostToDevice, 0);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_link, 0xFF, a_link + 16, 0);
+#if BQ_K3_RED_PROBE
+    static uint32_t *probe_buf = nullptr;
+    static size_t probe_cap = 0;
+    const size_t probe_bytes = (total_words + 2) * 4;
+    if (e == cudaSuccess && probe_cap < probe_bytes) {
+        if (probe_buf) cudaFree(probe_buf);
+        e = cudaMalloc(reinterpret_cast<void **>(&probe_buf), probe_bytes);
+        probe_cap = e == cudaSuccess ? probe_bytes : 0;
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(probe_buf, 0, probe_bytes, 0);
+#endif
     if (e == cudaSuccess) {
         DirArgs a;
         a.ptrs = d_ptrs;
@@ -467,6 +502,9 @@ int build_rle_directory(const uint64_t *const *d_ptrs, const uint64_t *d_lens, c
         a.link = d_link;
         a.ticket = d_ticket;
         a.err = d_err;
+#if BQ_K3_RED_PROBE
+        a.probe = probe_buf;
+#endif
         rle_dir_kernel<<<(unsigned)njobs, 32, 0, 0>>>(a);
         e = cudaGetLastError();
     }
