@@ -75,3 +75,43 @@ def test_shard_threshold_contract(bq):
     out = torch.empty(16, dtype=torch.int64, device="cuda")
     optr = (ctypes.c_void_p * 1)(out.data_ptr())
     assert lib.bq_shard_threshold(1, devices, spans.ctypes.data, 1, 640, wb, we, 1, optr, None, None) == -1
+
+
+@pytest.mark.parametrize("n,r", [(1, 64 * 7 + 5), (9, 64 * 3000 + 1), (130, 64 * 2048)])
+def test_one_shot_forms(bq, n, r):
+    """bq_threshold_u64 / bq_symmetric_u64 (create + evaluate + destroy in one call)
+    against the oracle's ScanCount (counters.py:46-83), ragged trimmed inputs."""
+    lib = bq._lib.load()
+    nw = (r + 63) // 64
+    rng = np.random.default_rng(n + r)
+    host, keep = [], []
+    spans = np.zeros((n, 2), dtype=np.uint64)
+    for i in range(n):
+        a = rng.integers(0, 2**63, nw, dtype=np.uint64) & rng.integers(0, 2**63, nw, dtype=np.uint64)
+        if r % 64:
+            a[-1] &= np.uint64((1 << (r % 64)) - 1)
+        a = a[: max(0, nw - (i % 4) * 3)]
+        host.append(a)
+        d = torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda() if a.size else None
+        keep.append(d)
+        spans[i] = (d.data_ptr() if a.size else 0, a.size)
+    out = torch.empty(max(nw, 2), dtype=torch.int64, device="cuda")
+    pc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for t in sorted({1, max(1, n // 3), n}):
+        pc.zero_()
+        torch.cuda.synchronize()
+        rc = lib.bq_threshold_u64(spans.ctypes.data, n, r, t, out.data_ptr(), pc.data_ptr(), None)
+        assert rc == 0, lib.bq_last_error()
+        exp = O.scan_count(host, r, t)
+        assert np.array_equal(out[:nw].cpu().numpy().view(np.uint64), exp), t
+        assert int(pc.item()) == int(np.unpackbits(exp.view(np.uint8)).sum())
+    acc = np.array([k % 3 == 1 for k in range(n + 1)], dtype=np.uint8)
+    pc.zero_()
+    torch.cuda.synchronize()
+    rc = lib.bq_symmetric_u64(spans.ctypes.data, n, r, acc.ctypes.data, out.data_ptr(), pc.data_ptr(), None)
+    assert rc == 0, lib.bq_last_error()
+    exp = O.scan_count_symmetric(host, r, [bool(x) for x in acc])
+    assert np.array_equal(out[:nw].cpu().numpy().view(np.uint64), exp)
+    assert int(pc.item()) == int(np.unpackbits(exp.view(np.uint8)).sum())
+    # the threshold contract of the one-shot form is the query's: t outside [1, n] is an InputError
+    assert lib.bq_threshold_u64(spans.ctypes.data, n, r, n + 1, out.data_ptr(), None, None) != 0
