@@ -42,6 +42,17 @@ def test_library_exports_every_declared_symbol(lib):
     assert lib.bq_version() >= 100
 
 
+def test_integration_doc_names_every_entry_point():
+    """INTEGRATION.md maps each exported function to the reference interface it replaces
+    (or says it has none): no declared symbol may be missing from it."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    patterns = set(re.findall(r"bq_[a-z_0-9]+", doc))
+    for name in declared_symbols():
+        covered = name in patterns or (name.endswith("_destroy") and "bq_*_destroy" in doc) or \
+            any(p.endswith("_") and name.startswith(p) for p in patterns)
+        assert covered, f"{name} is not mentioned in INTEGRATION.md"
+
+
 @pytest.mark.parametrize("case", [c for c in load_golden("codec") if c.meta["kind"] == "compress"],
                          ids=lambda c: c.id)
 def test_host_encoder_matches_reference_compress(case):
